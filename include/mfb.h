@@ -1,0 +1,186 @@
+/*
+ * mfb.h -- C ABI of the B200 (sm_100a) stochastic multiscale-flux-basis path.
+ *
+ * The reference (sdmortar 0.1.0, pure Python/numpy/scipy) has no FFI; its
+ * seam is the Python function API of `sdmortar/interface.py`. Each entry
+ * point below replaces one piece of that API's compute; the Python host
+ * (paper_1802_06263_b200/interface.py) keeps the reference signatures and
+ * binds these through ctypes.
+ *
+ *   mfb_kl_realize        <- LogPermField.realize / evaluate_log
+ *                            (random_field.py:232-243, 125-140)
+ *   mfb_systems_solve     <- problem.assemble_subdomain + DarcyOperator /
+ *                            StokesOperator factor + the N_dof star solves of
+ *                            compute_flux_basis and the bar solve
+ *                            (problem.py:98-112, darcy.py:67-154,
+ *                             stokes.py:112-322, interface.py:218-235, 166-177)
+ *   mfb_systems_extract   <- compute_flux_basis readout (interface.py:210-235),
+ *                            side_functionals (problem.py:132-148),
+ *                            postprocess (problem.py:150-158)
+ *   mfb_cg_batched        <- the S3 main loop's compute_rhs + cg_solve with
+ *                            basis_apply (interface.py:107-139, 238-247,
+ *                            331-334), all collocation points at once
+ *   mfb_group_stats,
+ *   mfb_group_fields,
+ *   mfb_moments_reduce    <- recover_fields + MomentAccumulator for field keys
+ *                            (interface.py:250-268, moments.py:25-58)
+ *   mfb_lambda_moments    <- MomentAccumulator for the "lambda" key
+ *                            (moments.py:25-58), fixed realization order
+ *
+ * Conventions: every pointer argument is a DEVICE pointer unless named
+ * `host_*`; buffers are caller-allocated and never freed by the library;
+ * calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ * default stream); return 0 on success or an MFB_ERR_* code. Per-item
+ * numerical failures (singular pivots, CG breakdown) are reported in the
+ * caller's `info` / `status` arrays, which the Python layer maps onto the
+ * reference exceptions (SingularOperatorError, ConvergenceError).
+ */
+#ifndef MFB_H
+#define MFB_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFB_OK 0
+#define MFB_ERR_ARG 1
+#define MFB_ERR_LAUNCH 2
+#define MFB_ERR_SMEM 3
+
+/* term kinds of a parametrised matrix / rhs entry */
+#define MFB_TERM_CONST 0      /* c                */
+#define MFB_TERM_INV_K 1      /* c / K[k]         */
+#define MFB_TERM_INV_SQRT_K 2 /* c / sqrt(K[k])   */
+
+/* CG per-point status */
+#define MFB_CG_CONVERGED 0
+#define MFB_CG_NOT_SPD 1      /* p.Sp <= 0  (interface.py:123-126) */
+#define MFB_CG_MAX_ITER 2     /* budget exhausted (interface.py:137-139) */
+#define MFB_CG_ZERO_RHS 3     /* ||g|| = 0, zero iterations (interface.py:111-113) */
+
+/*
+ * Structure of one subdomain's linear system (shared by all its local
+ * realizations). Interior unknowns 0..n-1 are in banded order (lower/upper
+ * half-bandwidths kl, ku); border unknowns n..n+nb-1 (Stokes rigid-body
+ * pinning dofs and kernel multipliers) couple densely through E / G.
+ * Right-hand sides: ndof mortar columns Q (sparse, CSC) and one bar column.
+ * All index/coefficient arrays are device pointers.
+ */
+typedef struct MfbPattern {
+    int n, kl, ku, ldab, nb, ndof, nfield;
+    int n_entries;                 /* interior matrix entries          */
+    const int *e_row, *e_col;      /* band-order row/col per entry      */
+    const int *e_tptr;             /* [n_entries+1] term ranges         */
+    const int *t_kind;             /* MFB_TERM_*                        */
+    const double *t_c;
+    const int *t_k;                /* index into the system's K slice   */
+    const double *E;               /* n x nb row-major (constant)       */
+    const double *G;               /* nb x nb row-major (constant)      */
+    const int *q_ptr, *q_row;      /* CSC of Q: ndof columns, rows < n+nb */
+    const double *q_val;
+    const double *bar_const;       /* [n+nb] constant bar rhs           */
+    int n_bar_rows;                /* parametrised bar rhs rows         */
+    const int *b_row, *b_tptr;     /* rows and term ranges              */
+    const int *bt_kind;
+    const double *bt_c;
+    const int *bt_k;
+    const double *h_lift;          /* [ndof] bar readout of lifted data */
+    const int *p_ptr, *p_col;      /* CSR postprocess: nfield rows      */
+    const double *p_val;
+    const double *f_lift;          /* [nfield] lifted data in the fields */
+} MfbPattern;
+
+const char *mfb_version(void);
+const char *mfb_strerror(int code);
+
+/* K[l*n_cells + c] = exp(mean[c] + sum_j phi[c*n_term + j] * xi[l*n_term + j]) */
+int mfb_kl_realize(const double *phi, const double *mean, int n_cells, int n_term,
+                   const double *xi, int n_loc, double *K, void *stream);
+
+/*
+ * Assemble, factor (banded LU, partial pivoting) and solve every system s
+ * in one launch. pats: device array of patterns; sys_pat[s] selects one;
+ * the system's K slice is Kbuf + sys_koff[s]; workspace at work +
+ * sys_woff[s] holds ldab*n band + n*(nb+ndof+1) doubles; the solution
+ * X (n+nb rows x ndof+1 columns, row-major) goes to X + sys_xoff[s].
+ * info[s]: 0 ok, j+1 zero pivot at band column j, -1 singular border.
+ * threads: 128/256/512/1024 per system; smem_doubles >= max over the
+ * patterns used of (2*kl + ku + 3 + nb + ndof + 1).
+ */
+int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *sys_pat,
+                      const double *Kbuf, const long long *sys_koff,
+                      double *work, const long long *sys_woff,
+                      double *X, const long long *sys_xoff, int *info,
+                      int threads, int smem_doubles, void *stream);
+
+/*
+ * From X: basis block Bt (column-major ndof x ndof, i.e. Bt[c*ndof+r] =
+ * B[r][c] with B = Q^T X_Q), bar jump h = Q^T x_bar + h_lift, field
+ * responses M = P X_Q (nfield x ndof row-major) and bar fields
+ * Fb = P x_bar + f_lift. Any of the output pointers may be NULL.
+ */
+int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
+                        const double *X, const long long *sys_xoff,
+                        double *blocks, const long long *sys_boff,
+                        double *hbar, const long long *sys_hoff,
+                        double *M, const long long *sys_moff,
+                        double *Fb, const long long *sys_fboff, void *stream);
+
+/*
+ * Batched interface CG over points k0..k0+n_pts-1 (global indices).
+ * Subdomain i: ndof[i] local dofs with global ids dof_map[dof_ptr[i]..],
+ * block of point k at blocks + blk_base[i] + loc*ndof[i]^2 and bar jump at
+ * hbar + h_base[i] + loc*ndof[i], where loc = local_idx[region[i]*n_real+k]
+ * (region[i] < 0: loc = 0). Outputs per point (indexed k-k0): lam
+ * [n_lambda], iters, status (MFB_CG_*), rel. residual history res_hist
+ * [hist_cap] (entries beyond hist_cap are dropped), g (may be NULL).
+ */
+int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
+                   const int *dof_map, const int *region, const long long *blk_base,
+                   const long long *h_base, const int *local_idx, int n_real,
+                   const double *blocks, const double *hbar, int k0, int n_pts,
+                   double tol, int max_iter, double *lam, int *iters, int *status,
+                   double *res_hist, int hist_cap, double *g, void *stream);
+
+/*
+ * Shifted sufficient statistics per group (one subdomain x one local
+ * realization): members grp_members[grp_ptr[g]..grp_ptr[g+1]) (increasing
+ * k), W = sum w_k, lamstar = lam_{first member}|_i, s = sum w_k d_k,
+ * C = sum w_k d_k d_k^T with d_k = lam_k|_i - lamstar.
+ */
+int mfb_group_stats(int n_groups, const int *grp_sid, const int *grp_ptr,
+                    const int *grp_members, const int *ndof, const int *dof_ptr,
+                    const int *dof_map, int n_lambda, const double *lam,
+                    const double *weights, const long long *grp_voff,
+                    const long long *grp_coff, double *W, double *lamstar,
+                    double *s, double *C, void *stream);
+
+/* Per group: fstar = Fb - M lamstar, t = -M s, q = diag(M C M^T). */
+int mfb_group_fields(int n_groups, const int *grp_sid, const int *ndof,
+                     const int *nfield, const double *M, const long long *grp_moff,
+                     const double *Fb, const long long *grp_fboff,
+                     const long long *grp_voff, const long long *grp_coff,
+                     const double *lamstar, const double *s, const double *C,
+                     double *fstar, double *t, double *q, void *stream);
+
+/*
+ * Per subdomain i, groups gptr[i]..gptr[i+1] in local order: mean =
+ * sum_l (W_l fstar_l + t_l); var = sum_l [W_l (fstar_l-m)^2 + 2 (fstar_l-m)
+ * t_l + q_l] + m^2 (1 - wtot), unclamped (the host applies the clamp).
+ */
+int mfb_moments_reduce(int n_sub, const int *gptr, const int *nfield,
+                       const long long *grp_fboff, const double *W,
+                       const double *fstar, const double *t, const double *q,
+                       double wtot, const long long *sid_out_off, double *mean,
+                       double *var, void *stream);
+
+/* Streaming s += w*v, q += (w*v)*v in realization order, then m = s,
+ * var = q - m*m (unclamped), no FMA contraction (moments.py:34-35, 50). */
+int mfb_lambda_moments(int n_lambda, int n_real, const double *lam,
+                       const double *weights, double *mean, double *var,
+                       double *sumsq, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MFB_H */

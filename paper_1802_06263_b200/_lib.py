@@ -1,0 +1,82 @@
+"""ctypes binding of the sm_100a library `_mfb.so` (C ABI in include/mfb.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, `lib()` raises NativeLibraryError.
+"""
+
+import ctypes
+import os
+
+from .errors import NativeLibraryError
+
+_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_mfb.so")
+_lib = None
+
+_p = ctypes.c_void_p
+_i = ctypes.c_int
+_d = ctypes.c_double
+
+
+class MfbPattern(ctypes.Structure):
+    _fields_ = [
+        ("n", _i), ("kl", _i), ("ku", _i), ("ldab", _i), ("nb", _i), ("ndof", _i),
+        ("nfield", _i), ("n_entries", _i),
+        ("e_row", _p), ("e_col", _p), ("e_tptr", _p), ("t_kind", _p), ("t_c", _p),
+        ("t_k", _p), ("E", _p), ("G", _p), ("q_ptr", _p), ("q_row", _p), ("q_val", _p),
+        ("bar_const", _p), ("n_bar_rows", _i), ("b_row", _p), ("b_tptr", _p),
+        ("bt_kind", _p), ("bt_c", _p), ("bt_k", _p), ("h_lift", _p), ("p_ptr", _p),
+        ("p_col", _p), ("p_val", _p), ("f_lift", _p),
+    ]
+
+
+_SIGS = {
+    "mfb_version": ([], ctypes.c_char_p),
+    "mfb_strerror": ([_i], ctypes.c_char_p),
+    "mfb_kl_realize": ([_p, _p, _i, _i, _p, _i, _p, _p], _i),
+    "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p], _i),
+    "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
+    "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
+                        _p, _p, _p, _p, _i, _p, _p], _i),
+    "mfb_group_stats": ([_i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p,
+                         _p], _i),
+    "mfb_group_fields": ([_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                          _p], _i),
+    "mfb_moments_reduce": ([_i, _p, _p, _p, _p, _p, _p, _p, _d, _p, _p, _p, _p], _i),
+    "mfb_lambda_moments": ([_i, _i, _p, _p, _p, _p, _p, _p], _i),
+}
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+def load(path=_SO):
+    """Open the shared library and declare signatures (no device needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeLibraryError(
+            f"{path} is missing; build it with `python -m paper_1802_06263_b200._build` "
+            f"(there is no CPU fallback)")
+    lib_ = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib_, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib_
+    return _lib
+
+
+def lib():
+    """The loaded library, after checking a CUDA device is usable."""
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("no CUDA device: the B200 path has no CPU fallback")
+    return load()
+
+
+def check(code, what):
+    if code != 0:
+        msg = load().mfb_strerror(code).decode()
+        raise NativeLibraryError(f"{what} failed: {msg} (code {code})")

@@ -1,0 +1,123 @@
+"""Device plan: the problem's realization-independent data resident in HBM.
+
+`DevicePlan(problem, grid)` flattens the host setup into device tensors once
+per (problem, grid): per-subdomain system patterns (discretization.py), the
+KL mode tables, mortar dof maps, local-index tables and the S3 group member
+lists. PyTorch is used only as the allocator/stream provider; all compute
+goes through the sm_100a library (`_lib.py`).
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .discretization import darcy_pattern, stokes_pattern
+
+
+def _dev(a, dtype):
+    import torch
+    t = torch.as_tensor(np.ascontiguousarray(a), dtype=dtype)
+    return t.to("cuda", non_blocking=False)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else ctypes.c_void_p(0)
+
+
+class DevicePlan:
+    """Everything about (problem, grid) that does not depend on lambda."""
+
+    def __init__(self, problem, grid):
+        import torch
+        self.torch = torch
+        self.problem, self.grid = problem, grid
+        lay = problem.layout
+        self.n_sub = lay.n_subdomains
+        self.n_lambda = problem.space.n_dof
+        self.darcy = problem.darcy_sids()
+        # concatenated mean-field K layout over Darcy subdomains
+        self.k0_off, off = {}, 0
+        for s in self.darcy:
+            self.k0_off[s] = off
+            off += problem.meshes[s].n_cells
+        self.k0_len = off
+        # host K0 (exp(mean)) only for the Stokes kernel-structure test
+        K0_host = np.zeros(self.k0_len)
+        for s in self.darcy:
+            c = problem.meshes[s].centroids
+            _, mean = problem.perm.mode_table(lay.blocks[s].kl_region, c[:, 0], c[:, 1])
+            K0_host[self.k0_off[s]:self.k0_off[s] + len(mean)] = np.exp(mean)
+        self.patterns = []
+        for sid in range(self.n_sub):
+            if lay.physics(sid) == "darcy":
+                self.patterns.append(darcy_pattern(problem, sid))
+            else:
+                self.patterns.append(stokes_pattern(problem, sid, self.k0_off, K0_host))
+        self.ndof = np.array([p.ndof for p in self.patterns], dtype=np.int32)
+        self.nfield = np.array([p.nfield for p in self.patterns], dtype=np.int32)
+        dofs = [problem.space.sub_dofs(lay, s) for s in range(self.n_sub)]
+        self.dof_ptr = np.cumsum([0] + [len(d) for d in dofs]).astype(np.int32)
+        self.dof_map = np.concatenate(dofs).astype(np.int32)
+        self.region = np.array([lay.blocks[s].kl_region if lay.physics(s) == "darcy" else -1
+                                for s in range(self.n_sub)], dtype=np.int32)
+        self.n_loc = np.array([grid.local_counts[r] if r >= 0 else 1 for r in self.region],
+                              dtype=np.int64)
+        self._upload_patterns()
+        self._upload_tables()
+
+    # ---------------------------------------------------------------- upload
+    def _upload_patterns(self):
+        torch = self.torch
+        i32, f64, i64 = torch.int32, torch.float64, torch.int64
+        self._keep = []
+        structs = (_lib.MfbPattern * self.n_sub)()
+        for s, p in enumerate(self.patterns):
+            arrs = {
+                "e_row": _dev(p.e_row, i32), "e_col": _dev(p.e_col, i32),
+                "e_tptr": _dev(p.e_tptr, i32), "t_kind": _dev(p.t_kind, i32),
+                "t_c": _dev(p.t_c, f64), "t_k": _dev(p.t_k, i32),
+                "E": _dev(p.E.ravel(), f64), "G": _dev(p.G.ravel(), f64),
+                "q_ptr": _dev(p.q_ptr, i32), "q_row": _dev(p.q_row, i32),
+                "q_val": _dev(p.q_val, f64), "bar_const": _dev(p.bar_const, f64),
+                "b_row": _dev(p.b_row, i32), "b_tptr": _dev(p.b_tptr, i32),
+                "bt_kind": _dev(p.bt_kind, i32), "bt_c": _dev(p.bt_c, f64),
+                "bt_k": _dev(p.bt_k, i32), "h_lift": _dev(p.h_lift, f64),
+                "p_ptr": _dev(p.p_ptr, i32), "p_col": _dev(p.p_col, i32),
+                "p_val": _dev(p.p_val, f64), "f_lift": _dev(p.f_lift, f64),
+            }
+            self._keep.append(arrs)
+            st = structs[s]
+            st.n, st.kl, st.ku, st.ldab = p.n, p.kl, p.ku, p.ldab
+            st.nb, st.ndof, st.nfield = p.nb, p.ndof, p.nfield
+            st.n_entries = len(p.e_row)
+            st.n_bar_rows = len(p.b_row)
+            for name, t in arrs.items():
+                setattr(st, name, _ptr(t).value or 0)
+        raw = bytes(structs)
+        host = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
+        self.pat_dev = host.to("cuda")
+
+    def _upload_tables(self):
+        torch = self.torch
+        g = self.grid
+        self.d_ndof = _dev(self.ndof, torch.int32)
+        self.d_nfield = _dev(self.nfield, torch.int32)
+        self.d_dof_ptr = _dev(self.dof_ptr, torch.int32)
+        self.d_dof_map = _dev(self.dof_map, torch.int32)
+        self.d_region = _dev(self.region, torch.int32)
+        li = np.stack(g.local_indices).astype(np.int32) if g.local_indices else \
+            np.zeros((1, g.n_real), dtype=np.int32)
+        self.d_local = _dev(li, torch.int32)
+        self.d_weights = _dev(g.weights, torch.float64)
+
+    # ---------------------------------------------------------- system list
+    def s3_systems(self):
+        """(sid, loc) of every S3 basis system, sid-major (interface.py:357-373)."""
+        out = []
+        for s in range(self.n_sub):
+            out += [(s, l) for l in range(int(self.n_loc[s]))]
+        return out
+
+    def basis_bytes(self):
+        return [8 * int(self.ndof[s]) ** 2 * int(self.n_loc[s]) for s in range(self.n_sub)]

@@ -1,0 +1,62 @@
+"""Shared fixtures: golden fixtures (generated from the reference) and cases."""
+
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+def golden(name):
+    path = os.path.join(GOLDEN, name + ".npz")
+    if not os.path.exists(path):
+        pytest.skip(f"golden fixture {name}.npz not generated")
+    return np.load(path)
+
+
+def case_from_golden(name, **patch):
+    """(cfg, problem, grid, options) rebuilt from the config stored in a fixture."""
+    from paper_1802_06263_b200.config import build_from_config, validate_config
+    z = golden(name)
+    raw = json.loads(str(z["config_json"]))
+    raw.update(patch)
+    cfg = validate_config(raw)
+    problem, grid, options = build_from_config(cfg)
+    return cfg, problem, grid, options
+
+
+def case_from_config(path, **patch):
+    from paper_1802_06263_b200.config import build_from_config, validate_config
+    with open(path) as fh:
+        raw = json.load(fh)
+    raw.update(patch)
+    cfg = validate_config(raw)
+    return (cfg,) + build_from_config(cfg)
+
+
+def has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        return False
+
+
+@pytest.fixture(scope="session")
+def gpu():
+    if not has_gpu():
+        pytest.skip("no CUDA device")
+    from paper_1802_06263_b200 import _build
+    _build.build()
+    return True
