@@ -1,0 +1,364 @@
+"""Benchmark: Method-S3 stochastic-MFB sweep on B200.
+
+A "step" is one full S3 sweep of the workload config (default: BASELINE
+configs[1] = configs/cfg2.json): KL fields for every local realization,
+assembly + factor + multi-RHS solve of every (subdomain, local realization)
+system, the batched interface CG over all collocation points, and the
+moments. `value` = collocation realizations/s with the problem resident in
+HBM (device time, CUDA events); `e2e` = the same metric through the public
+API `run_method(problem, grid, "S3", tol)` with host inputs and host
+results (H2D of the step's KL/collocation tables, D2H of lambdas, residual
+histories and moments inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+    python bench.py --impl reference ...   # the reference CPU algorithm (oracle port)
+
+Under torchrun (N > 1) every rank runs the same sweep on its own GPU
+(weak scaling, replicas); timing is the max over ranks.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--tol", type=float, default=1e-11)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _config_path(name):
+    return name if name.endswith(".json") else os.path.join(ROOT, "configs", name + ".json")
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001 - clocks are best effort
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {}
+    if os.path.exists(path):
+        with open(path) as fh:
+            peaks = json.load(fh)
+    fp64 = None
+    fpath = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(fpath):
+        with open(fpath) as fh:
+            fp64 = json.load(fh)
+    return peaks, fp64
+
+
+def cpu_baseline(cfg_path, tol, sample_points=None):
+    """Reference CPU algorithm (oracle port of sdmortar S3), 1 thread."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import s3_cpu
+    from paper_1802_06263_b200.config import load_config
+    problem, grid, _ = load_config(cfg_path)
+    pts = None if sample_points is None else list(range(min(sample_points, grid.n_real)))
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        ops, bases = s3_cpu.prepare_s3(problem, grid)
+        t_pre = time.perf_counter() - t0
+        solves = sum(len(b) * b[0][1].shape[0] for b in bases.values())
+        t1 = time.perf_counter()
+        _run_points(s3_cpu, problem, grid, ops, bases, tol, pts)
+        t_main = time.perf_counter() - t1
+    n_done = grid.n_real if pts is None else len(pts)
+    per_point = t_main / max(n_done, 1)
+    est_total = t_pre + per_point * grid.n_real
+    return {
+        "realizations_per_s": grid.n_real / est_total,
+        "basis_local_solves_per_s": solves / t_pre,
+        "pre_loop_s": t_pre, "main_loop_s": t_main, "points_timed": n_done,
+        "n_real": grid.n_real, "extrapolated": pts is not None,
+    }
+
+
+def _run_points(s3_cpu, problem, grid, ops, bases, tol, pts):
+    """The S3 main loop of the oracle for a subset of points (no re-prepare)."""
+    n_sub = problem.layout.n_subdomains
+    space = problem.space
+    acc = s3_cpu.Moments()
+    for k in (range(grid.n_real) if pts is None else pts):
+        loc = [s3_cpu.local_of(problem, grid, s, k) for s in range(n_sub)]
+        pick_ops = [ops[s][loc[s]] for s in range(n_sub)]
+        pick_b = [bases[s][loc[s]] for s in range(n_sub)]
+
+        def apply_fn(lam, pick_b=pick_b):
+            out = np.zeros(space.n_dof)
+            for dofs, B in pick_b:
+                out[dofs] += B @ lam[dofs]
+            return out
+
+        bars, entries = [], []
+        for s in range(n_sub):
+            u, p = s3_cpu.bar_solve(pick_ops[s])
+            bars.append((u, p))
+            entries += s3_cpu.side_values(problem, s, pick_ops[s], u)
+        g = s3_cpu.jump(space, entries)
+        lam, _, _ = s3_cpu.cg_solve(apply_fn, g, tol=tol)
+        fields = {"lambda": lam}
+        for s in range(n_sub):
+            us, ps = s3_cpu.star_solve(problem, s, pick_ops[s], lam)
+            f = pick_ops[s].postprocess(bars[s][0] + us, bars[s][1] + ps)
+            for name, arr in f.items():
+                fields[f"{s}:{name}"] = arr
+        acc.add(grid.weights[k], fields)
+    return acc
+
+
+def run_reference(a):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_1802_06263_b200.config import load_config
+    cfg_path = _config_path(a.config)
+    problem, grid, _ = load_config(cfg_path)
+    cores = len(os.sched_getaffinity(0))
+    # each step: full pre-loop + a bounded prefix of the main loop, extrapolated
+    sample = 8
+    vals = []
+    t_all = time.perf_counter()
+    for i in range(a.warmup + a.steps):
+        from oracle import s3_cpu
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=cores):
+            t0 = time.perf_counter()
+            ops, bases = s3_cpu.prepare_s3(problem, grid)
+            t_pre = time.perf_counter() - t0
+            t1 = time.perf_counter()
+            _run_points(s3_cpu, problem, grid, ops, bases, a.tol, list(range(min(sample, grid.n_real))))
+            t_main = time.perf_counter() - t1
+        n_done = min(sample, grid.n_real)
+        est = t_pre + t_main / n_done * grid.n_real
+        if i >= a.warmup:
+            vals.append(grid.n_real / est)
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": f"collocation realizations/s (S3 sweep, {a.config})",
+        "value": v, "unit": "realizations/s", "n_gpus": ws, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1000.0 * grid.n_real / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic collocation grid of the config)",
+        "config": {"workload": a.config, "n_real": grid.n_real, "tol": a.tol},
+        "cpu_baseline": {"value": v, "unit": "realizations/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"oracle/s3_cpu.py (restated sdmortar S3: SuperLU + numpy CG), "
+                                   f"full pre-loop + first {sample} of {grid.n_real} points per "
+                                   f"step, extrapolated to the full sweep"},
+        "e2e": {"value": v, "unit": "realizations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a):
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_1802_06263_b200 import _build
+    from paper_1802_06263_b200.config import load_config
+    from paper_1802_06263_b200.interface import S3Engine, get_plan, run_method
+    _build.build()
+    cfg_path = _config_path(a.config)
+    problem, grid, _ = load_config(cfg_path)
+    nl = problem.space.n_dof
+    max_iter = max(50, 10 * nl)
+    t0 = time.perf_counter()
+    plan = get_plan(problem, grid)
+    plan_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step(eng):
+        eng.kl_fields()
+        eng.build_bases()
+        lam, iters, status, hist, _ = eng.solve_points(a.tol, max_iter)
+        mom = eng.moments(lam)
+        return lam, iters, status, mom
+
+    for _ in range(a.warmup):
+        eng = S3Engine(plan)
+        step(eng)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    dev_ms, e2e_s = [], []
+    solve_ms, solve_flops, launches = [], [], 0
+    iters_host = None
+    with ClockSampler(local) as clocks:
+        for _ in range(a.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            eng = S3Engine(plan)
+            eng.timing = True
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            lam, iters, status, mom = step(eng)   # moments include D2H of the results
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dev_ms.append(e0.elapsed_time(e1))
+            launches = eng.launches
+            for (s0, s1), fl in zip(eng.solve_events, eng.solve_flops):
+                solve_ms.append(s0.elapsed_time(s1))
+                solve_flops.append(fl)
+            iters_host = iters.cpu().numpy()
+            eng.check_info()
+        # end-to-end through the public API, host in / host out
+        for _ in range(a.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            res = run_method(problem, grid, method="S3", tol=a.tol)
+            e2e_s.append(time.perf_counter() - t)
+    if ws > 1:
+        tmax = torch.tensor([sum(dev_ms), sum(e2e_s)], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tot_ms, tot_e2e = float(tmax[0]), float(tmax[1])
+    else:
+        tot_ms, tot_e2e = sum(dev_ms), sum(e2e_s)
+    ms_step = tot_ms / a.steps
+    value = ws * grid.n_real / (ms_step / 1000.0)
+    e2e_val = ws * grid.n_real / (tot_e2e / a.steps)
+    systems = plan.s3_systems()
+    local_solves = int(sum(int(plan.ndof[s]) for s, _ in systems))
+    peaks, fp64 = _peaks()
+    # dominant kernel: the batched basis solve (assembly + banded LU + multi-RHS)
+    fl_launch = float(np.mean(solve_flops)) if solve_flops else 0.0
+    t_launch = float(np.mean(solve_ms)) / 1000.0 if solve_ms else float("nan")
+    achieved = fl_launch / t_launch / 1e12 if solve_ms else None
+    peak = fp64["dmma_tflops"] if fp64 else None
+    share = sum(solve_ms) / tot_ms if tot_ms else None
+    # bytes of the per-step inputs uploaded by run_method (KL tables + xi)
+    h2d = 0
+    for s in plan.darcy:
+        r = problem.layout.blocks[s].kl_region
+        nc = problem.meshes[s].n_cells
+        nt = problem.perm.regions[r].n_term
+        h2d += 8 * (nc * nt + nc + (1 + int(plan.n_loc[s])) * nt)
+    d2h = 8 * grid.n_real * nl + 8 * grid.n_real * max_iter + 8 * grid.n_real * 2 + \
+        16 * (nl + int(plan.nfield.sum()))
+    if rank == 0:
+        line = {
+            "metric": f"collocation realizations/s (S3 sweep, {a.config})",
+            "value": value, "unit": "realizations/s", "n_gpus": ws, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (deterministic Gauss-Hermite/Smolyak collocation of the "
+                    "config; no dataset)",
+            "config": {"workload": a.config, "n_real": grid.n_real, "n_lambda": nl,
+                       "systems": len(systems), "tol": a.tol,
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "plan_cached": True, "plan_build_s": plan_s},
+            "basis_local_solves_per_s": local_solves / (sum(solve_ms) / len(dev_ms) / 1000.0)
+            if solve_ms else None,
+            "cg_iters_mean": float(iters_host.mean()), "cg_iters_max": int(iters_host.max()),
+            "roofline": {"kernel": "band_solve_kernel (assembly + banded LU + multi-RHS)",
+                         "bound": "fp64", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": (achieved / peak) if (achieved and peak)
+                         else None, "peak_source": "profiles/fp64_peak.json (DMMA "
+                         "microbenchmark; MEASURED_PEAKS.json has no FP64 figure)",
+                         "algorithmic_flops_per_launch": fl_launch,
+                         "launch_ms": t_launch * 1000.0, "share_of_step": share,
+                         "traffic": None},
+            "gpu_launches": launches,
+            "e2e": {"value": e2e_val, "unit": "realizations/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "run_method(problem, grid, 'S3', tol)"},
+            "clocks": clocks.summary(),
+        }
+        if not a.no_cpu_baseline and ws == 1:
+            cb = cpu_baseline(cfg_path, a.tol)
+            line["cpu_baseline"] = {
+                "value": cb["realizations_per_s"], "unit": "realizations/s", "cores": 1,
+                "kind": "port",
+                "sample": f"oracle/s3_cpu.py full {a.config} S3 sweep ({cb['n_real']} points), "
+                          f"1 BLAS thread",
+                "basis_local_solves_per_s": cb["basis_local_solves_per_s"],
+                "pre_loop_s": cb["pre_loop_s"], "main_loop_s": cb["main_loop_s"]}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

@@ -180,6 +180,10 @@ int mfb_lambda_moments(int n_lambda, int n_real, const double *lam,
                        const double *weights, double *mean, double *var,
                        double *sumsq, void *stream);
 
+/* Self test of the FP64 tensor-core (DMMA m8n8k4) fragment layout the
+ * elimination kernels rely on; writes max |error| to *err (device). */
+int mfb_selftest_dmma(double *err, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,7 @@ _SIGS = {
                           _p], _i),
     "mfb_moments_reduce": ([_i, _p, _p, _p, _p, _p, _p, _p, _d, _p, _p, _p, _p], _i),
     "mfb_lambda_moments": ([_i, _i, _p, _p, _p, _p, _p, _p], _i),
+    "mfb_selftest_dmma": ([_p, _p], _i),
 }
 
 

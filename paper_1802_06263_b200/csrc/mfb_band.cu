@@ -23,9 +23,16 @@ namespace {
 
 constexpr int MAX_NB = 8;
 constexpr int MAX_NCY = 160;
+constexpr int BAND_NB = 16;
 
 __device__ __forceinline__ long long bidx(int i, int k, int kl, int ku, int ldab) {
     return (long long)k * ldab + (kl + ku + i - k);
+}
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
 template <int NT>
@@ -35,11 +42,17 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                   double *__restrict__ work, const long long *__restrict__ sys_woff,
                   double *__restrict__ Xout, const long long *__restrict__ sys_xoff,
                   int *__restrict__ info) {
+    constexpr int NB = BAND_NB;
+    constexpr int PST = NB + 1;          // odd stride: lane-varying rows hit distinct banks
+    constexpr int NW = NT / 32;
     extern __shared__ double smem[];
-    __shared__ double red_v[NT / 32];
-    __shared__ int red_i[NT / 32];
+    __shared__ double red_v[NW];
+    __shared__ int red_i[NW];
     __shared__ int s_piv;
-    __shared__ double s_pivval;
+    __shared__ int s_ipiv[NB];
+    __shared__ int s_low[NB];
+    __shared__ int s_nlow;
+    __shared__ double s_u11[NB * NB];
     __shared__ double s_bord[MAX_NB * MAX_NCY];
     __shared__ double s_z[MAX_NB * MAX_NCY];
     __shared__ int s_flag;
@@ -50,12 +63,14 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     const int n = P.n, kl = P.kl, ku = P.ku, ldab = P.ldab, nb = P.nb;
     const int nrhs = P.ndof + 1;
     const int ncy = nb + nrhs;
+    const int UST = kl + ku + 8;
     double *AB = work + sys_woff[s];
     double *Y = AB + (long long)ldab * n;
-    double *s_l = smem;                 // kl multipliers
-    double *s_u = s_l + kl + 1;         // kl+ku+1 pivot-row entries
-    double *s_y = s_u + kl + ku + 2;    // ncy pivot rhs row
-    const int tid = threadIdx.x;
+    double *Pnl = smem;                          // (kl + NB) x PST   panel L | U11
+    double *U12s = Pnl + (kl + NB) * PST;        // NB x UST          U12 of the panel
+    double *Ytop = U12s + NB * UST;              // NB x ncy          rhs rows of the panel
+    int *s_perm = reinterpret_cast<int *>(Ytop + NB * ncy);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
     // ---- 1. assembly ---------------------------------------------------
     const long long nab = (long long)ldab * n, ny = (long long)n * ncy;
@@ -86,85 +101,234 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     }
     __syncthreads();
 
-    // ---- 2. banded LU with partial pivoting + forward elimination --------
-    for (int j = 0; j < n; ++j) {
-        const int iend = min(n - 1, j + kl);
-        const int kend = min(n - 1, j + kl + ku);
-        double best = -1.0;
-        int bi = j;
-        for (int i = j + tid; i <= iend; i += NT) {
-            double a = fabs(AB[bidx(i, j, kl, ku, ldab)]);
-            if (a > best) { best = a; bi = i; }
+    // ---- 2. blocked banded LU with partial pivoting (gbtrf) --------------
+    for (int j0 = 0; j0 < n; j0 += NB) {
+        const int pnb = min(NB, n - j0);
+        const int r1 = min(n, j0 + pnb + kl);
+        const int nr = r1 - j0;
+        const int c0 = j0 + pnb;
+        const int c1 = min(n, j0 + pnb + kl + ku);
+        const int nc = max(0, c1 - c0);
+        // panel columns j0..j0+pnb of rows j0..r1 (zero beyond the band / pnb)
+        for (int t = tid; t < nr * NB; t += NT) {
+            const int i = t % nr, c = t / nr;
+            const int r = j0 + i, col = j0 + c;
+            Pnl[i * PST + c] = (c < pnb && r - col <= kl && col - r <= kl + ku)
+                                   ? AB[bidx(r, col, kl, ku, ldab)] : 0.0;
         }
+        __syncthreads();
+        for (int c = 0; c < pnb; ++c) {
+            double best = -1.0;
+            int bi = c;
+            for (int i = c + tid; i < nr; i += NT) {
+                const double a = fabs(Pnl[i * PST + c]);
+                if (a > best) { best = a; bi = i; }
+            }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            double ov = __shfl_down_sync(0xffffffffu, best, o);
-            int oi = __shfl_down_sync(0xffffffffu, bi, o);
-            if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_down_sync(0xffffffffu, best, o);
+                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+            }
+            if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+            __syncthreads();
+            if (tid == 0) {
+                double bv = red_v[0];
+                int bx = red_i[0];
+                for (int w = 1; w < NW; ++w)
+                    if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bx)) { bv = red_v[w]; bx = red_i[w]; }
+                s_piv = bx;
+                s_ipiv[c] = bx;
+            }
+            __syncthreads();
+            const int p = s_piv;
+            if (Pnl[p * PST + c] == 0.0) {
+                if (tid == 0) info[s] = j0 + c + 1;
+                return;
+            }
+            if (p != c)
+                for (int cc = tid; cc < NB; cc += NT) {
+                    const double t0 = Pnl[c * PST + cc];
+                    Pnl[c * PST + cc] = Pnl[p * PST + cc];
+                    Pnl[p * PST + cc] = t0;
+                }
+            __syncthreads();
+            const double piv = Pnl[c * PST + c];
+            for (int i = c + 1 + tid; i < nr; i += NT) {
+                const double l = Pnl[i * PST + c] / piv;
+                Pnl[i * PST + c] = l;
+                for (int cc = c + 1; cc < pnb; ++cc) Pnl[i * PST + cc] -= l * Pnl[c * PST + cc];
+            }
+            __syncthreads();
         }
-        if ((tid & 31) == 0) { red_v[tid >> 5] = best; red_i[tid >> 5] = bi; }
-        __syncthreads();
+        // net row permutation of the panel's swaps
         if (tid == 0) {
-            double bv = red_v[0];
-            int bx = red_i[0];
-            for (int w = 1; w < NT / 32; ++w)
-                if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bx)) { bv = red_v[w]; bx = red_i[w]; }
-            s_piv = bx;
-            s_pivval = AB[bidx(bx, j, kl, ku, ldab)];
+            for (int i = 0; i < nr; ++i) s_perm[i] = i;
+            int nl = 0;
+            for (int q = 0; q < pnb; ++q) {
+                const int p = s_ipiv[q];
+                const int t0 = s_perm[q];
+                s_perm[q] = s_perm[p];
+                s_perm[p] = t0;
+                if (p >= pnb) {
+                    bool seen = false;
+                    for (int z = 0; z < nl; ++z) seen |= (s_low[z] == p);
+                    if (!seen) s_low[nl++] = p;
+                }
+            }
+            s_nlow = nl;
         }
         __syncthreads();
-        const int p = s_piv;
-        const double piv = s_pivval;
-        if (piv == 0.0) {
-            if (tid == 0) info[s] = j + 1;
-            return;
+        for (int t = tid; t < nr * pnb; t += NT) {
+            const int i = t % nr, c = t / nr;
+            const int r = j0 + i, col = j0 + c;
+            if (r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = Pnl[i * PST + c];
         }
-        // swap rows j <-> p over columns j..kend, stage pivot row and multipliers
-        for (int k = j + tid; k <= kend; k += NT) {
-            long long aj = bidx(j, k, kl, ku, ldab), ap = bidx(p, k, kl, ku, ldab);
-            double vj = AB[aj], vp = AB[ap];
-            if (p != j) { AB[aj] = vp; AB[ap] = vj; }
-            s_u[k - j] = vp;
+        // phase A: trailing columns -- permute, U12 = L11^-1 A12 (thread per column)
+        const int nlow = s_nlow;
+        const int ncpad = (nc + 7) & ~7;
+        for (int t = tid; t < ncpad; t += NT) {
+            const int col = c0 + t;
+            double u[NB], low[NB];
+            if (t < nc) {
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    u[q] = 0.0;
+                    if (q < pnb) {
+                        const int src = j0 + s_perm[q];
+                        if (col - src <= kl + ku && src - col <= kl) u[q] = AB[bidx(src, col, kl, ku, ldab)];
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < NB; ++z) {
+                    low[z] = 0.0;
+                    if (z < nlow) {
+                        const int src = j0 + s_perm[s_low[z]];
+                        if (col - src <= kl + ku && src - col <= kl) low[z] = AB[bidx(src, col, kl, ku, ldab)];
+                    }
+                }
+#pragma unroll
+                for (int z = 0; z < NB; ++z)
+                    if (z < nlow && (j0 + s_low[z]) - col <= kl) AB[bidx(j0 + s_low[z], col, kl, ku, ldab)] = low[z];
+#pragma unroll
+                for (int q = 1; q < NB; ++q) {
+                    double v = u[q];
+#pragma unroll
+                    for (int qq = 0; qq < q; ++qq) v -= Pnl[q * PST + qq] * u[qq];
+                    u[q] = v;
+                }
+#pragma unroll
+                for (int q = 0; q < NB; ++q)
+                    if (q < pnb && col - (j0 + q) <= kl + ku) AB[bidx(j0 + q, col, kl, ku, ldab)] = u[q];
+            } else {
+#pragma unroll
+                for (int q = 0; q < NB; ++q) u[q] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NB; ++q) U12s[q * UST + t] = q < pnb ? u[q] : 0.0;
         }
-        for (int c = tid; c < ncy; c += NT) {
-            long long yj = (long long)j * ncy + c, yp = (long long)p * ncy + c;
-            double vj = Y[yj], vp = Y[yp];
-            if (p != j) { Y[yj] = vp; Y[yp] = vj; }
-            s_y[c] = vp;
+        // phase A': right-hand sides -- permute + forward substitution (thread per column)
+        for (int cy = tid; cy < ncy; cy += NT) {
+            double u[NB], low[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+                u[q] = q < pnb ? Y[(long long)(j0 + s_perm[q]) * ncy + cy] : 0.0;
+#pragma unroll
+            for (int z = 0; z < NB; ++z)
+                low[z] = z < nlow ? Y[(long long)(j0 + s_perm[s_low[z]]) * ncy + cy] : 0.0;
+#pragma unroll
+            for (int z = 0; z < NB; ++z)
+                if (z < nlow) Y[(long long)(j0 + s_low[z]) * ncy + cy] = low[z];
+#pragma unroll
+            for (int q = 1; q < NB; ++q) {
+                double v = u[q];
+#pragma unroll
+                for (int qq = 0; qq < q; ++qq) v -= Pnl[q * PST + qq] * u[qq];
+                u[q] = v;
+            }
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                if (q < pnb) Y[(long long)(j0 + q) * ncy + cy] = u[q];
+                Ytop[q * ncy + cy] = q < pnb ? u[q] : 0.0;
+            }
         }
         __syncthreads();
-        // column j after the swap: row p holds the old row-j value
-        for (int i = j + 1 + tid; i <= iend; i += NT)
-            s_l[i - j - 1] = AB[bidx(i, j, kl, ku, ldab)] / piv;
-        __syncthreads();
-        const int nr = iend - j, nc = kend - j;
-        for (int t = tid; t < nr * nc; t += NT) {
-            const int ii = t % nr, kk = t / nr;
-            const int i = j + 1 + ii, k = j + 1 + kk;
-            AB[bidx(i, k, kl, ku, ldab)] -= s_l[ii] * s_u[kk + 1];
+        // phase B: A22 -= L21 U12 on FP64 tensor cores (DMMA 8x8x4 tiles)
+        {
+            const int mrows = nr - pnb;
+            const int tr = (mrows + 7) >> 3, tcn = ncpad >> 3;
+            const int g = lane >> 2, q4 = lane & 3;
+            for (int tile = wid; tile < tr * tcn; tile += NW) {
+                const int ti = tile % tr, tj = tile / tr;
+                const int prow = pnb + ti * 8;           // panel-local row of the tile
+                const int row = j0 + prow + g;
+                const int ca = c0 + tj * 8 + 2 * q4, cb = ca + 1;
+                const bool va = row < r1 && ca < c1 && row - ca <= kl;
+                const bool vb = row < r1 && cb < c1 && row - cb <= kl;
+                double d0 = va ? AB[bidx(row, ca, kl, ku, ldab)] : 0.0;
+                double d1 = vb ? AB[bidx(row, cb, kl, ku, ldab)] : 0.0;
+                const bool ra = prow + g < nr;
+#pragma unroll
+                for (int k0 = 0; k0 < NB; k0 += 4) {
+                    const double a = ra ? -Pnl[(prow + g) * PST + k0 + q4] : 0.0;
+                    const double b = U12s[(k0 + q4) * UST + tj * 8 + g];
+                    dmma884(d0, d1, a, b);
+                }
+                if (va) AB[bidx(row, ca, kl, ku, ldab)] = d0;
+                if (vb) AB[bidx(row, cb, kl, ku, ldab)] = d1;
+            }
         }
-        for (int t = tid; t < nr * ncy; t += NT) {
-            const int ii = t / ncy, c = t % ncy;
-            Y[(long long)(j + 1 + ii) * ncy + c] -= s_l[ii] * s_y[c];
+        // phase B': rhs rows below the panel
+        {
+            const int tot = (nr - pnb) * ncy;
+            for (int t = tid; t < tot; t += NT) {
+                const int ii = t / ncy, cy = t % ncy;
+                const double *lrow = Pnl + (pnb + ii) * PST;
+                const long long a = (long long)(j0 + pnb + ii) * ncy + cy;
+                double acc = Y[a];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) acc -= lrow[q] * Ytop[q * ncy + cy];
+                Y[a] = acc;
+            }
         }
         __syncthreads();
     }
 
-    // ---- 3. back substitution with U (kl+ku superdiagonals) -------------
-    for (int j = n - 1; j >= 0; --j) {
-        const double ujj = AB[bidx(j, j, kl, ku, ldab)];
-        for (int c = tid; c < ncy; c += NT) {
-            double y = Y[(long long)j * ncy + c] / ujj;
-            Y[(long long)j * ncy + c] = y;
-            s_y[c] = y;
+    // ---- 3. blocked column-oriented back substitution with U ---------------
+    const int last = ((n - 1) / NB) * NB;
+    for (int j0 = last; j0 >= 0; j0 -= NB) {
+        const int pnb = min(NB, n - j0);
+        for (int t = tid; t < NB * NB; t += NT) {
+            const int r = t / NB, c = t % NB;
+            s_u11[t] = (r < pnb && c < pnb && c >= r) ? AB[bidx(j0 + r, j0 + c, kl, ku, ldab)] : 0.0;
         }
         __syncthreads();
-        const int i0 = max(0, j - kl - ku);
-        const int nr = j - i0;
-        for (int t = tid; t < nr * ncy; t += NT) {
-            const int ii = t / ncy, c = t % ncy;
-            const int i = i0 + ii;
-            Y[(long long)i * ncy + c] -= AB[bidx(i, j, kl, ku, ldab)] * s_y[c];
+        for (int cy = tid; cy < ncy; cy += NT) {
+            double x[NB];
+#pragma unroll
+            for (int r = NB - 1; r >= 0; --r) {
+                if (r >= pnb) { x[r] = 0.0; continue; }
+                double v = Y[(long long)(j0 + r) * ncy + cy];
+#pragma unroll
+                for (int rr = r + 1; rr < NB; ++rr) v -= s_u11[r * NB + rr] * x[rr];
+                x[r] = v / s_u11[r * NB + r];
+            }
+#pragma unroll
+            for (int r = 0; r < NB; ++r) {
+                if (r < pnb) Y[(long long)(j0 + r) * ncy + cy] = x[r];
+                Ytop[r * ncy + cy] = x[r];
+            }
+        }
+        __syncthreads();
+        const int i0 = max(0, j0 - kl - ku);
+        const int tot = (j0 - i0) * ncy;
+        for (int t = tid; t < tot; t += NT) {
+            const int i = i0 + t / ncy, cy = t % ncy;
+            const long long a = (long long)i * ncy + cy;
+            double acc = Y[a];
+            const int qend = min(pnb, i + kl + ku + 1 - j0);
+            for (int q = 0; q < qend; ++q) acc -= AB[bidx(i, j0 + q, kl, ku, ldab)] * Ytop[q * ncy + cy];
+            Y[a] = acc;
         }
         __syncthreads();
     }
@@ -302,34 +466,34 @@ extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *s
                                  const long long *sys_xoff, int *info, int threads,
                                  int smem_doubles, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
-    // dynamic smem: multipliers + pivot row + rhs row of the widest band
+    // dynamic smem: see Pattern.smem_doubles (discretization.py)
     const int nt = threads;
     size_t smem = (size_t)smem_doubles * sizeof(double);
     cudaStream_t st = mfb_stream(stream);
     switch (nt) {
         case 128:
-            if (smem > 48 * 1024 && cudaFuncSetAttribute(band_solve_kernel<128>,
+            if (cudaFuncSetAttribute(band_solve_kernel<128>,
                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return MFB_ERR_SMEM;
             band_solve_kernel<128><<<n_sys, 128, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
                                                              work, sys_woff, X, sys_xoff, info);
             break;
         case 256:
-            if (smem > 48 * 1024 && cudaFuncSetAttribute(band_solve_kernel<256>,
+            if (cudaFuncSetAttribute(band_solve_kernel<256>,
                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return MFB_ERR_SMEM;
             band_solve_kernel<256><<<n_sys, 256, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
                                                              work, sys_woff, X, sys_xoff, info);
             break;
         case 512:
-            if (smem > 48 * 1024 && cudaFuncSetAttribute(band_solve_kernel<512>,
+            if (cudaFuncSetAttribute(band_solve_kernel<512>,
                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return MFB_ERR_SMEM;
             band_solve_kernel<512><<<n_sys, 512, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
                                                              work, sys_woff, X, sys_xoff, info);
             break;
         case 1024:
-            if (smem > 48 * 1024 && cudaFuncSetAttribute(band_solve_kernel<1024>,
+            if (cudaFuncSetAttribute(band_solve_kernel<1024>,
                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
                 return MFB_ERR_SMEM;
             band_solve_kernel<1024><<<n_sys, 1024, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,

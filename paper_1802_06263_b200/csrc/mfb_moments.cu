@@ -248,3 +248,32 @@ extern "C" const char *mfb_strerror(int code) {
         default: return "unknown error";
     }
 }
+
+// ---- self test: FP64 tensor-core fragment layout used by the band kernel ----
+namespace {
+__global__ void selftest_dmma_kernel(double *err) {
+    const int lane = threadIdx.x;
+    const int g = lane >> 2, q4 = lane & 3;
+    // A[i][k] = 1 + i + 0.5 k, B[k][j] = 2 - 0.25 j + k, C[i][j] = i - j
+    const double a = 1.0 + g + 0.5 * q4;
+    const double b = 2.0 - 0.25 * g + q4;
+    double d0 = g - 2 * q4, d1 = g - (2 * q4 + 1);
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+    double e = 0.0;
+    for (int h = 0; h < 2; ++h) {
+        const int i = g, j = 2 * q4 + h;
+        double ref = i - j;
+        for (int k = 0; k < 4; ++k) ref += (1.0 + i + 0.5 * k) * (2.0 - 0.25 * j + k);
+        e = fmax(e, fabs((h ? d1 : d0) - ref));
+    }
+    for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_down_sync(0xffffffffu, e, o));
+    if (lane == 0) *err = e;
+}
+}  // namespace
+
+extern "C" int mfb_selftest_dmma(double *err, void *stream) {
+    selftest_dmma_kernel<<<1, 32, 0, mfb_stream(stream)>>>(err);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}

@@ -91,8 +91,17 @@ class Pattern:
         return (self.n + self.nb) * (self.ndof + 1)
 
     @property
+    def algorithmic_flops(self):
+        """F = 2 n w^2 + 4 n w N_dof, w = half-bandwidth of the ordering."""
+        w = max(self.kl, self.ku)
+        return 2.0 * self.n * w * w + 4.0 * self.n * w * self.ndof
+
+    @property
     def smem_doubles(self):
-        return 2 * self.kl + self.ku + 3 + self.nb + self.ndof + 1
+        # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 16 x (kl + ku + 8),
+        # rhs rows 16 x (nb + ndof + 1), (kl + 16) ints of row permutation
+        return ((self.kl + 16) * 17 + 16 * (self.kl + self.ku + 8)
+                + 16 * (self.nb + self.ndof + 1) + (self.kl + 16) // 2 + 1)
 
 
 class _TermTable:

@@ -112,6 +112,15 @@ class S3Engine:
         self.L = _lib.lib()
         self.stream = torch.cuda.current_stream() if stream is None else stream
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
+        self.launches = 0            # kernels launched through the C ABI
+        self.timing = False          # record CUDA events around the basis solves
+        self.solve_events = []
+        self.solve_flops = []
+
+    def _ev(self):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        return ev
 
     # ------------------------------------------------------------ (1) KL --
     def kl_fields(self):
@@ -144,6 +153,7 @@ class S3Engine:
             self._kl_tabs.append((d_phi, d_mean, d_xi))
             nc = len(mean)
             # mean field -> K0 slot, local realizations -> their system slots
+            self.launches += 2
             _lib.check(self.L.mfb_kl_realize(_ptr(d_phi), _ptr(d_mean), nc, nt, _ptr(d_xi),
                                              1, ctypes.c_void_p(K.data_ptr() + 8 * plan.k0_off[s]),
                                              self.sp), "mfb_kl_realize")
@@ -187,9 +197,11 @@ class S3Engine:
         d_koff = _dev(self.koff, torch.int64)
         d_boff, d_hoff = _dev(boff[:-1], torch.int64), _dev(hoff[:-1], torch.int64)
         d_moff, d_fboff = _dev(moff[:-1], torch.int64), _dev(fboff[:-1], torch.int64)
+        phys = [plan.problem.layout.physics(s) for s, _ in systems]
         while start < nsys:
             end, acc = start, 0
-            while end < nsys and (end == start or acc + per[end] <= WORK_BUDGET_BYTES):
+            while end < nsys and (end == start or (acc + per[end] <= WORK_BUDGET_BYTES
+                                                   and phys[end] == phys[start])):
                 acc += per[end]
                 end += 1
             cnt = end - start
@@ -201,10 +213,17 @@ class S3Engine:
             nt = threads or (512 if max(pats[s].kl for s, _ in systems[start:end]) > 128
                              else 256)
             sub = lambda t, elt=8: ctypes.c_void_p(t.data_ptr() + elt * start)
+            if self.timing:
+                e0 = self._ev()
             _lib.check(self.L.mfb_systems_solve(
                 _ptr(plan.pat_dev), cnt, sub(d_pat, 4), _ptr(self.K), sub(d_koff),
                 _ptr(work), _ptr(d_woff), _ptr(X), _ptr(d_xoff), sub(self.info, 4), nt, smem,
                 self.sp), "mfb_systems_solve")
+            if self.timing:
+                self.solve_events.append((e0, self._ev()))
+                self.solve_flops.append(sum(pats[s].algorithmic_flops for s, _ in
+                                            systems[start:end]))
+            self.launches += 2
             _lib.check(self.L.mfb_systems_extract(
                 _ptr(plan.pat_dev), cnt, sub(d_pat, 4), _ptr(X), _ptr(d_xoff),
                 _ptr(self.blocks), sub(d_boff), _ptr(self.hbar), sub(d_hoff),
@@ -243,6 +262,7 @@ class S3Engine:
         hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=torch.float64, device="cuda")
         g = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda") if keep_g else None
         d_blk, d_h = _dev(self.blk_base, torch.int64), _dev(self.h_base, torch.int64)
+        self.launches += 1
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
             _ptr(plan.d_region), _ptr(d_blk), _ptr(d_h), _ptr(plan.d_local), n_real,
@@ -260,6 +280,7 @@ class S3Engine:
         m = torch.empty(nl, dtype=torch.float64, device="cuda")
         v = torch.empty_like(m)
         q = torch.empty_like(m)
+        self.launches += 4
         _lib.check(self.L.mfb_lambda_moments(nl, n_real, _ptr(lam), _ptr(plan.d_weights),
                                              _ptr(m), _ptr(v), _ptr(q), self.sp),
                    "mfb_lambda_moments")

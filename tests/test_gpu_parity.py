@@ -22,6 +22,15 @@ def _rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
 
 
+def test_dmma_fragment_layout(gpu):
+    import ctypes
+    import torch
+    from paper_1802_06263_b200 import _lib
+    err = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")
+    assert _lib.lib().mfb_selftest_dmma(ctypes.c_void_p(err.data_ptr()), None) == 0
+    assert float(err.item()) == 0.0
+
+
 def _engine(problem, grid):
     from paper_1802_06263_b200.interface import S3Engine, get_plan
     plan = get_plan(problem, grid)
