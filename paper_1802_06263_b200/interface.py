@@ -376,6 +376,7 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     if method != "S3":
         raise NotImplementedError(
             f"method {method} is not on this B200 path (S3 only); no CPU fallback")
+    _lib.lib()                      # raises NativeLibraryError: no CPU fallback
     import torch
     t0 = time.perf_counter()
     n_sub = problem.layout.n_subdomains
