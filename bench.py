@@ -274,9 +274,8 @@ def run_ours(a):
             torch.cuda.synchronize()
             dev_ms.append(e0.elapsed_time(e1))
             launches = eng.launches
-            for (s0, s1), fl in zip(eng.solve_events, eng.solve_flops):
-                solve_ms.append(s0.elapsed_time(s1))
-                solve_flops.append(fl)
+            for kind, s0, s1, fl, sfl in eng.solve_events:
+                solve_ms.append((kind, s0.elapsed_time(s1), fl, sfl))
             iters_host = iters.cpu().numpy()
             eng.check_info()
         # end-to-end through the public API, host in / host out
@@ -298,19 +297,34 @@ def run_ours(a):
     systems = plan.s3_systems()
     local_solves = int(sum(int(plan.ndof[s]) for s, _ in systems))
     peaks, fp64 = _peaks()
-    # dominant kernel: the batched basis solve (assembly + banded LU + multi-RHS)
-    fl_launch = float(np.mean(solve_flops)) if solve_flops else 0.0
-    t_launch = float(np.mean(solve_ms)) / 1000.0 if solve_ms else float("nan")
-    achieved = fl_launch / t_launch / 1e12 if solve_ms else None
+    # dominant basis kernel of the step (per-kind CUDA-event totals over the timed steps)
+    kinds = {}
+    for kind, ms, fl, sfl in solve_ms:
+        k = kinds.setdefault(kind, [0.0, 0.0, 0.0, 0])
+        k[0] += ms
+        k[1] += fl
+        k[2] += sfl
+        k[3] += 1
+    dom = max(kinds, key=lambda x: kinds[x][0]) if kinds else None
     peak = fp64["dmma_tflops"] if fp64 else None
-    share = sum(solve_ms) / tot_ms if tot_ms else None
-    # bytes of the per-step inputs uploaded by run_method (KL tables + xi)
-    h2d = 0
-    for s in plan.darcy:
-        r = problem.layout.blocks[s].kl_region
-        nc = problem.meshes[s].n_cells
-        nt = problem.perm.regions[r].n_term
-        h2d += 8 * (nc * nt + nc + (1 + int(plan.n_loc[s])) * nt)
+    roof = None
+    if dom:
+        t_ms, fl, sfl, cnt = kinds[dom]
+        achieved = fl / (t_ms / 1000.0) / 1e12
+        roof = {"kernel": {"band": "band_solve_kernel (Stokes: assembly + banded LU + multi-RHS)",
+                           "hybrid": "condense_kernel (Darcy: SPD static condensation)"}[dom],
+                "bound": "fp64 (DMMA)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None,
+                "peak_source": "profiles/fp64_peak.json (our DMMA microbenchmark; "
+                               "MEASURED_PEAKS.json has no FP64 figure)",
+                "flops_per_launch": fl / cnt, "launch_ms": t_ms / cnt,
+                "share_of_step": t_ms / tot_ms if tot_ms else None,
+                "survey_algorithmic_tflops": sfl / (t_ms / 1000.0) / 1e12,
+                "traffic": None,
+                "per_kind_ms_per_step": {k: v[0] / len(dev_ms) for k, v in kinds.items()}}
+    basis_ms = sum(v[0] for v in kinds.values()) / max(len(dev_ms), 1)
+    # bytes of the per-step inputs run_method uploads (collocation + KL tables)
+    h2d = int(res.timings.get("h2d_bytes", 0))
     d2h = 8 * grid.n_real * nl + 8 * grid.n_real * max_iter + 8 * grid.n_real * 2 + \
         16 * (nl + int(plan.nfield.sum()))
     if rank == 0:
@@ -326,17 +340,9 @@ def run_ours(a):
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single",
                        "l2": "flushed (256 MB write) before every timed step",
                        "plan_cached": True, "plan_build_s": plan_s},
-            "basis_local_solves_per_s": local_solves / (sum(solve_ms) / len(dev_ms) / 1000.0)
-            if solve_ms else None,
+            "basis_local_solves_per_s": local_solves / (basis_ms / 1000.0) if basis_ms else None,
             "cg_iters_mean": float(iters_host.mean()), "cg_iters_max": int(iters_host.max()),
-            "roofline": {"kernel": "band_solve_kernel (assembly + banded LU + multi-RHS)",
-                         "bound": "fp64", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": (achieved / peak) if (achieved and peak)
-                         else None, "peak_source": "profiles/fp64_peak.json (DMMA "
-                         "microbenchmark; MEASURED_PEAKS.json has no FP64 figure)",
-                         "algorithmic_flops_per_launch": fl_launch,
-                         "launch_ms": t_launch * 1000.0, "share_of_step": share,
-                         "traffic": None},
+            "roofline": roof,
             "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": "realizations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "run_method(problem, grid, 'S3', tol)"},

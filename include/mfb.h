@@ -90,6 +90,26 @@ typedef struct MfbPattern {
     const double *f_lift;          /* [nfield] lifted data in the fields */
 } MfbPattern;
 
+/*
+ * Hybridised (SPD) Darcy subdomain: unknown edge multipliers 0..n-1 in line
+ * order (half-bandwidth w); every cell contributes K_T * Hhat over its
+ * (west, east, south, north) edges. Interface edges carry the mortar data
+ * through G (gam_*: edge -> mortar dofs; dof_*: the transpose), pressure
+ * edges carry p_val. See paper_1802_06263_b200/hybrid.py.
+ */
+typedef struct MfbHybPattern {
+    int n, w, ws, ndof, nfield, n_edges, n_cells, has_src;
+    double hx, hy, nu, s2;
+    double Hhat[16];
+    const int *row_edge, *edge_kind, *edge_idx, *edge_cells, *edge_slot, *edge_noflow;
+    const int *cell_edges;
+    const int *gam_ptr, *gam_d;
+    const double *gam_c;
+    const int *dof_ptr, *dof_edge;
+    const double *dof_coef;
+    const double *p_val, *src_k, *src_c, *cell_f, *cell_q;
+} MfbHybPattern;
+
 const char *mfb_version(void);
 const char *mfb_strerror(int code);
 
@@ -179,6 +199,35 @@ int mfb_moments_reduce(int n_sub, const int *gptr, const int *nfield,
 int mfb_lambda_moments(int n_lambda, int n_real, const double *lam,
                        const double *weights, double *mean, double *var,
                        double *sumsq, void *stream);
+
+/*
+ * Darcy flux basis by static condensation of the SPD hybridised system in
+ * shared memory (band Cholesky, panel width `panel` = 8 or 16, trailing
+ * updates on DMMA): per system B (column-major into blocks + sys_boff) and
+ * the bar jump h. If Lstore != NULL the factor panels are kept for
+ * mfb_darcy_backsolve (layout: per panel m*(panel+4) L doubles then
+ * panel*Cp rhs doubles, m = w + panel, Cp = ndof+1 rounded up to 8).
+ * info[s] = -(pivot index + 1) if a pivot is not positive. smem_bytes:
+ * 8 * (m*ws + m*Cp + Cp*Cp + m*(panel+4) + panel*Cp) for the widest pattern.
+ */
+int mfb_darcy_condense(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
+                       const double *Kbuf, const long long *sys_koff, double *blocks,
+                       const long long *sys_boff, double *hbar, const long long *sys_hoff,
+                       double *Lstore, const long long *sys_loff, int *info, int panel,
+                       int smem_bytes, void *stream);
+
+/* X = H_II^-1 [V | v_b] (n x Cp, row-major) from the stored factor panels;
+ * smem_bytes = 8 * (m*Cp + m*(panel+4) + panel*Cp). */
+int mfb_darcy_backsolve(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
+                        const double *Lstore, const long long *sys_loff, double *X,
+                        const long long *sys_xoff, int panel, int smem_bytes, void *stream);
+
+/* Cell-local recovery of the fields: M (nfield x ndof, fields = Fb - M lam)
+ * and Fb, in the layout u(edges) | p(cells) | cv(cells x 2) | cp(cells). */
+int mfb_darcy_recover(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
+                      const double *Kbuf, const long long *sys_koff, const double *X,
+                      const long long *sys_xoff, double *M, const long long *sys_moff,
+                      double *Fb, const long long *sys_fboff, void *stream);
 
 /* Self test of the FP64 tensor-core (DMMA m8n8k4) fragment layout the
  * elimination kernels rely on; writes max |error| to *err (device). */

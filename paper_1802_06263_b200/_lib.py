@@ -29,6 +29,18 @@ class MfbPattern(ctypes.Structure):
     ]
 
 
+class MfbHybPattern(ctypes.Structure):
+    _fields_ = [
+        ("n", _i), ("w", _i), ("ws", _i), ("ndof", _i), ("nfield", _i), ("n_edges", _i),
+        ("n_cells", _i), ("has_src", _i), ("hx", _d), ("hy", _d), ("nu", _d), ("s2", _d),
+        ("Hhat", _d * 16),
+        ("row_edge", _p), ("edge_kind", _p), ("edge_idx", _p), ("edge_cells", _p),
+        ("edge_slot", _p), ("edge_noflow", _p), ("cell_edges", _p), ("gam_ptr", _p),
+        ("gam_d", _p), ("gam_c", _p), ("dof_ptr", _p), ("dof_edge", _p), ("dof_coef", _p),
+        ("p_val", _p), ("src_k", _p), ("src_c", _p), ("cell_f", _p), ("cell_q", _p),
+    ]
+
+
 _SIGS = {
     "mfb_version": ([], ctypes.c_char_p),
     "mfb_strerror": ([_i], ctypes.c_char_p),
@@ -44,6 +56,9 @@ _SIGS = {
     "mfb_moments_reduce": ([_i, _p, _p, _p, _p, _p, _p, _p, _d, _p, _p, _p, _p], _i),
     "mfb_lambda_moments": ([_i, _i, _p, _p, _p, _p, _p, _p], _i),
     "mfb_selftest_dmma": ([_p, _p], _i),
+    "mfb_darcy_condense": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p], _i),
+    "mfb_darcy_backsolve": ([_p, _i, _p, _p, _p, _p, _p, _i, _i, _p], _i),
+    "mfb_darcy_recover": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
 }
 
 

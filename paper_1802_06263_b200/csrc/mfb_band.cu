@@ -253,42 +253,67 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             }
         }
         __syncthreads();
-        // phase B: A22 -= L21 U12 on FP64 tensor cores (DMMA 8x8x4 tiles)
+        // phase B: A22 -= L21 U12 on FP64 tensor cores (DMMA 8x8x4 tiles).
+        // A warp owns a column tile: its U12 fragments stay in registers while
+        // it walks down the row tiles, prefetching the next C tile.
         {
             const int mrows = nr - pnb;
             const int tr = (mrows + 7) >> 3, tcn = ncpad >> 3;
             const int g = lane >> 2, q4 = lane & 3;
-            for (int tile = wid; tile < tr * tcn; tile += NW) {
-                const int ti = tile % tr, tj = tile / tr;
-                const int prow = pnb + ti * 8;           // panel-local row of the tile
-                const int row = j0 + prow + g;
-                const int ca = c0 + tj * 8 + 2 * q4, cb = ca + 1;
-                const bool va = row < r1 && ca < c1 && row - ca <= kl;
-                const bool vb = row < r1 && cb < c1 && row - cb <= kl;
-                double d0 = va ? AB[bidx(row, ca, kl, ku, ldab)] : 0.0;
-                double d1 = vb ? AB[bidx(row, cb, kl, ku, ldab)] : 0.0;
-                const bool ra = prow + g < nr;
+            for (int tj = wid; tj < tcn; tj += NW) {
+                double bf[NB / 4];
 #pragma unroll
-                for (int k0 = 0; k0 < NB; k0 += 4) {
-                    const double a = ra ? -Pnl[(prow + g) * PST + k0 + q4] : 0.0;
-                    const double b = U12s[(k0 + q4) * UST + tj * 8 + g];
-                    dmma884(d0, d1, a, b);
+                for (int kk = 0; kk < NB / 4; ++kk) bf[kk] = U12s[(4 * kk + q4) * UST + tj * 8 + g];
+                const int ca = c0 + tj * 8 + 2 * q4, cb = ca + 1;
+                auto load_c = [&](int ti, double &x0, double &x1) {
+                    const int row = j0 + pnb + ti * 8 + g;
+                    x0 = (row < r1 && ca < c1 && row - ca <= kl) ? AB[bidx(row, ca, kl, ku, ldab)] : 0.0;
+                    x1 = (row < r1 && cb < c1 && row - cb <= kl) ? AB[bidx(row, cb, kl, ku, ldab)] : 0.0;
+                };
+                double n0 = 0.0, n1 = 0.0;
+                if (tr > 0) load_c(0, n0, n1);
+                for (int ti = 0; ti < tr; ++ti) {
+                    double d0 = n0, d1 = n1;
+                    if (ti + 1 < tr) load_c(ti + 1, n0, n1);
+                    const int prow = pnb + ti * 8 + g;
+                    const bool ra = prow < nr;
+#pragma unroll
+                    for (int kk = 0; kk < NB / 4; ++kk) {
+                        const double a = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
+                        dmma884(d0, d1, a, bf[kk]);
+                    }
+                    const int row = j0 + prow;
+                    if (row < r1 && ca < c1 && row - ca <= kl) AB[bidx(row, ca, kl, ku, ldab)] = d0;
+                    if (row < r1 && cb < c1 && row - cb <= kl) AB[bidx(row, cb, kl, ku, ldab)] = d1;
                 }
-                if (va) AB[bidx(row, ca, kl, ku, ldab)] = d0;
-                if (vb) AB[bidx(row, cb, kl, ku, ldab)] = d1;
             }
         }
-        // phase B': rhs rows below the panel
+        // phase B': rhs rows below the panel, Y -= L21 Ytop (DMMA tiles; a warp
+        // owns a row tile and keeps its L21 fragments in registers)
         {
-            const int tot = (nr - pnb) * ncy;
-            for (int t = tid; t < tot; t += NT) {
-                const int ii = t / ncy, cy = t % ncy;
-                const double *lrow = Pnl + (pnb + ii) * PST;
-                const long long a = (long long)(j0 + pnb + ii) * ncy + cy;
-                double acc = Y[a];
+            const int mrows = nr - pnb;
+            const int tr = (mrows + 7) >> 3, tcy = (ncy + 7) >> 3;
+            const int g = lane >> 2, q4 = lane & 3;
+            for (int ti = wid; ti < tr; ti += NW) {
+                const int prow = pnb + ti * 8 + g;
+                const bool ra = prow < nr;
+                double af[NB / 4];
 #pragma unroll
-                for (int q = 0; q < NB; ++q) acc -= lrow[q] * Ytop[q * ncy + cy];
-                Y[a] = acc;
+                for (int kk = 0; kk < NB / 4; ++kk) af[kk] = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
+                const long long row = j0 + prow;
+                for (int tc = 0; tc < tcy; ++tc) {
+                    const int ca = tc * 8 + 2 * q4, cb = ca + 1;
+                    double d0 = (ra && ca < ncy) ? Y[row * ncy + ca] : 0.0;
+                    double d1 = (ra && cb < ncy) ? Y[row * ncy + cb] : 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < NB / 4; ++kk) {
+                        const int cc = tc * 8 + g;
+                        const double b = cc < ncy ? Ytop[(4 * kk + q4) * ncy + cc] : 0.0;
+                        dmma884(d0, d1, af[kk], b);
+                    }
+                    if (ra && ca < ncy) Y[row * ncy + ca] = d0;
+                    if (ra && cb < ncy) Y[row * ncy + cb] = d1;
+                }
             }
         }
         __syncthreads();
@@ -320,15 +345,37 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             }
         }
         __syncthreads();
-        const int i0 = max(0, j0 - kl - ku);
-        const int tot = (j0 - i0) * ncy;
-        for (int t = tid; t < tot; t += NT) {
-            const int i = i0 + t / ncy, cy = t % ncy;
-            const long long a = (long long)i * ncy + cy;
-            double acc = Y[a];
-            const int qend = min(pnb, i + kl + ku + 1 - j0);
-            for (int q = 0; q < qend; ++q) acc -= AB[bidx(i, j0 + q, kl, ku, ldab)] * Ytop[q * ncy + cy];
-            Y[a] = acc;
+        // push the solved panel into the rows above: Y[i] -= U(i, panel) x_panel
+        // (DMMA tiles; A = U block straight from the band, B = x from smem)
+        {
+            const int i0 = max(0, j0 - kl - ku);
+            const int mrows = j0 - i0;
+            const int tr = (mrows + 7) >> 3, tcy = (ncy + 7) >> 3;
+            const int g = lane >> 2, q4 = lane & 3;
+            for (int ti = wid; ti < tr; ti += NW) {
+                const int i = i0 + ti * 8 + g;
+                const bool ri = i < j0;
+                double af[NB / 4];
+#pragma unroll
+                for (int kk = 0; kk < NB / 4; ++kk) {
+                    const int k = 4 * kk + q4;
+                    af[kk] = (ri && k < pnb && (j0 + k) - i <= kl + ku)
+                                 ? -AB[bidx(i, j0 + k, kl, ku, ldab)] : 0.0;
+                }
+                for (int tc = 0; tc < tcy; ++tc) {
+                    const int ca = tc * 8 + 2 * q4, cb = ca + 1;
+                    double d0 = (ri && ca < ncy) ? Y[(long long)i * ncy + ca] : 0.0;
+                    double d1 = (ri && cb < ncy) ? Y[(long long)i * ncy + cb] : 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < NB / 4; ++kk) {
+                        const int cc = tc * 8 + g;
+                        const double b = cc < ncy ? Ytop[(4 * kk + q4) * ncy + cc] : 0.0;
+                        dmma884(d0, d1, af[kk], b);
+                    }
+                    if (ri && ca < ncy) Y[(long long)i * ncy + ca] = d0;
+                    if (ri && cb < ncy) Y[(long long)i * ncy + cb] = d1;
+                }
+            }
         }
         __syncthreads();
     }

@@ -1,0 +1,436 @@
+// Darcy flux basis by static condensation of the hybridised SPD system.
+//
+// Reference: the Darcy subdomain operator is the mixed RT0/P0 saddle matrix
+// factored with SuperLU (darcy.py:67-147); the flux basis costs one
+// backsolve per mortar dof (interface.py:218-235). Here the same discrete
+// problem is solved in its hybridised form (paper_1802_06263_b200/hybrid.py):
+// one SPD unknown per non-Dirichlet edge, every cell contributing K_T Hhat.
+// The flux-basis block B and the bar jump h are the Schur complement left
+// after eliminating all unknown edges from the bordered matrix
+//     [ H_II  V ]      V = [H_IG G | v_b],   Z = initial border block,
+//     [ V^T   Z ]
+// so one CTA per (subdomain, local realization) runs a band Cholesky over a
+// sliding window held entirely in shared memory -- rows enter the window as
+// they are assembled from K, leave it once eliminated -- and never touches
+// global memory for the factor. Per panel of BP pivots, one warp factors the
+// panel (Cholesky + forward substitution of the border rows) while the other
+// warps assemble the rows entering the window; then all warps apply the
+// rank-BP trailing update to the window, the border panel and the Schur
+// block on FP64 tensor cores (mma.sync m8n8k4 f64 -> SASS DMMA).
+// Field mode additionally stores the panels so that mfb_darcy_backsolve can
+// form X = H_II^-1 V and mfb_darcy_recover the cell fields.
+#include "mfb_common.cuh"
+
+namespace {
+
+constexpr int HYB_NT = 256;
+constexpr int HYB_NW = HYB_NT / 32;
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int cpad(int nd) { return (nd + 1 + 7) & ~7; }
+
+__device__ __forceinline__ double gcoef(const MfbHybPattern &P, int gi, int d) {
+    for (int t = P.gam_ptr[gi]; t < P.gam_ptr[gi + 1]; ++t)
+        if (P.gam_d[t] == d) return P.gam_c[t];
+    return 0.0;
+}
+
+// one thread assembles one window row r: lower band of H_II and border
+__device__ void assemble_row(const MfbHybPattern &P, const double *K, int r, double *W,
+                             double *Pb, int m, int ws, int Cp) {
+    const int w = P.w, nd = P.ndof;
+    double *wrow = W + (r % m) * ws;
+    double *prow = Pb + (r % m) * Cp;
+    for (int t = 0; t < ws; ++t) wrow[t] = 0.0;
+    for (int t = 0; t < Cp; ++t) prow[t] = 0.0;
+    const int e = P.row_edge[r];
+    for (int side = 0; side < 2; ++side) {
+        const int T = P.edge_cells[2 * e + side];
+        if (T < 0) continue;
+        const int a = P.edge_slot[2 * e + side];
+        const double k = K[T];
+        for (int b = 0; b < 4; ++b) {
+            const int e2 = P.cell_edges[4 * T + b];
+            const double h = k * P.Hhat[4 * a + b];
+            const int kind = P.edge_kind[e2], id = P.edge_idx[e2];
+            if (kind == 0) {
+                if (id <= r && r - id <= w) wrow[id - r + w] += h;
+            } else if (kind == 1) {
+                for (int t = P.gam_ptr[id]; t < P.gam_ptr[id + 1]; ++t)
+                    prow[P.gam_d[t]] += h * P.gam_c[t];
+            } else {
+                prow[nd] -= h * P.p_val[id];
+            }
+        }
+        if (P.has_src) prow[nd] += k * P.src_k[4 * T + a] + P.src_c[4 * T + a];
+    }
+}
+
+template <int BP>
+__global__ void __launch_bounds__(HYB_NT)
+condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ sys_pat,
+                const double *__restrict__ Kbuf, const long long *__restrict__ sys_koff,
+                double *__restrict__ blocks, const long long *__restrict__ sys_boff,
+                double *__restrict__ hbar, const long long *__restrict__ sys_hoff,
+                double *__restrict__ Lstore, const long long *__restrict__ sys_loff,
+                int *__restrict__ info) {
+    constexpr int LS = BP + 4;
+    extern __shared__ double sm[];
+    __shared__ int s_bad;
+    const int s = blockIdx.x;
+    const MfbHybPattern &P = pats[sys_pat[s]];
+    const double *K = Kbuf + sys_koff[s];
+    const int n = P.n, w = P.w, ws = P.ws, nd = P.ndof;
+    const int Cp = cpad(nd), m = w + BP;
+    double *W = sm;                 // m x ws      window rows, lower band
+    double *Pb = W + m * ws;        // m x Cp      border columns of the window rows
+    double *S = Pb + m * Cp;        // Cp x Cp     Schur block
+    double *Lb = S + Cp * Cp;       // m x LS      current panel (L11 | L21)
+    double *Yb = Lb + m * LS;       // BP x Cp     L11^-1 (border rows of the panel)
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int g = lane >> 2, q4 = lane & 3;
+    if (tid == 0) s_bad = 0;
+    for (int t = tid; t < Cp * Cp; t += HYB_NT) S[t] = 0.0;
+    __syncthreads();
+    // initial Schur block Z (thread per entry; sums in a fixed order)
+    for (int t = tid; t < nd * (nd + 1); t += HYB_NT) {
+        const int d1 = t / (nd + 1), d2 = t % (nd + 1);
+        double z = 0.0;
+        for (int u = P.dof_ptr[d1]; u < P.dof_ptr[d1 + 1]; ++u) {
+            const int e1 = P.dof_edge[u];
+            const double c1 = P.dof_coef[u];
+            const int T = P.edge_cells[2 * e1], a = P.edge_slot[2 * e1];
+            const double k = K[T];
+            for (int b = 0; b < 4; ++b) {
+                const int e2 = P.cell_edges[4 * T + b];
+                const int kind = P.edge_kind[e2], id = P.edge_idx[e2];
+                const double h = k * P.Hhat[4 * a + b];
+                if (d2 < nd) {
+                    if (kind == 1) z += c1 * h * gcoef(P, id, d2);
+                } else if (kind == 2) {
+                    z -= c1 * h * P.p_val[id];
+                }
+            }
+            if (d2 == nd && P.has_src) z += c1 * (k * P.src_k[4 * T + a] + P.src_c[4 * T + a]);
+        }
+        S[d1 * Cp + d2] = z;
+    }
+    for (int r = tid; r < min(n, m); r += HYB_NT) assemble_row(P, K, r, W, Pb, m, ws, Cp);
+    __syncthreads();
+
+    const int n_pan = (n + BP - 1) / BP;
+    const long long pstride = (long long)m * LS + (long long)BP * Cp;
+    for (int pi = 0; pi < n_pan; ++pi) {
+        const int k = pi * BP;
+        const int nb = min(BP, n - k);
+        const int rend = min(n, k + BP + w);
+        const int nrow = rend - k;
+        for (int t = tid; t < nrow * BP; t += HYB_NT) {
+            const int i = t / BP, p = t % BP;
+            double v = 0.0;
+            if (p < nb && i >= p && i - p <= w) v = W[((k + i) % m) * ws + (p - i + w)];
+            Lb[i * LS + p] = v;
+        }
+        for (int t = tid; t < BP * Cp; t += HYB_NT) {
+            const int p = t / Cp, c = t % Cp;
+            Yb[t] = p < nb ? Pb[((k + p) % m) * Cp + c] : 0.0;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            // panel Cholesky + forward substitution of the border rows (one warp)
+            for (int p = 0; p < nb; ++p) {
+                double d = Lb[p * LS + p];
+                if (!(d > 0.0)) {
+                    if (lane == 0) { s_bad = 1; info[s] = -(k + p + 1); }
+                    break;
+                }
+                d = sqrt(d);
+                __syncwarp();
+                for (int i = p + 1 + lane; i < nrow; i += 32) Lb[i * LS + p] /= d;
+                for (int c = lane; c < Cp; c += 32) Yb[p * Cp + c] /= d;
+                if (lane == 0) Lb[p * LS + p] = d;
+                __syncwarp();
+                for (int i = p + 1 + lane; i < nrow; i += 32) {
+                    const double lip = Lb[i * LS + p];
+                    const int qe = min(nb - 1, i);
+                    for (int q = p + 1; q <= qe; ++q) Lb[i * LS + q] -= lip * Lb[q * LS + p];
+                }
+                for (int c = lane; c < Cp; c += 32) {
+                    const double yp = Yb[p * Cp + c];
+                    for (int q = p + 1; q < nb; ++q) Yb[q * Cp + c] -= Lb[q * LS + p] * yp;
+                }
+                __syncwarp();
+            }
+        } else {
+            // rows entering the window take the freed slots of this panel
+            for (int r = k + m + (tid - 32); r < min(n, k + m + BP); r += HYB_NT - 32)
+                assemble_row(P, K, r, W, Pb, m, ws, Cp);
+        }
+        __syncthreads();
+        if (s_bad) return;
+        if (Lstore) {
+            double *dst = Lstore + sys_loff[s] + (long long)pi * pstride;
+            for (int t = tid; t < nrow * LS; t += HYB_NT) dst[t] = Lb[t];
+            for (int t = tid; t < BP * Cp; t += HYB_NT) dst[(long long)m * LS + t] = Yb[t];
+        }
+        // trailing updates on DMMA: window (lower band), border panel, Schur block
+        const int R = nrow - nb;
+        const int tr = (R + 7) >> 3, tc = Cp >> 3;
+        const int nd_t = tr * (tr + 1) / 2, ne_t = tr * tc, nf_t = tc * tc;
+        for (int t = wid; t < nd_t + ne_t + nf_t; t += HYB_NW) {
+            if (t < nd_t) {
+                int ti = 0;
+                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                const int tj = t - ti * (ti + 1) / 2;
+                const int ii = ti * 8 + g;
+                const int ja = tj * 8 + 2 * q4, jb = ja + 1;
+                const bool va = ii < R && ja <= ii, vb = ii < R && jb <= ii;
+                const int rr = (k + nb + ii) % m;
+                double d0 = va ? W[rr * ws + (ja - ii + w)] : 0.0;
+                double d1 = vb ? W[rr * ws + (jb - ii + w)] : 0.0;
+                const int ra = nb + ti * 8 + g, rb = nb + tj * 8 + g;
+#pragma unroll
+                for (int k0 = 0; k0 < BP; k0 += 4) {
+                    const double a = ra < nrow ? -Lb[ra * LS + k0 + q4] : 0.0;
+                    const double b = rb < nrow ? Lb[rb * LS + k0 + q4] : 0.0;
+                    dmma(d0, d1, a, b);
+                }
+                if (va) W[rr * ws + (ja - ii + w)] = d0;
+                if (vb) W[rr * ws + (jb - ii + w)] = d1;
+            } else if (t < nd_t + ne_t) {
+                const int u = t - nd_t;
+                const int ti = u / tc, tcol = u % tc;
+                const int ii = ti * 8 + g;
+                const int ca = tcol * 8 + 2 * q4;
+                const bool v = ii < R;
+                const int rr = (k + nb + ii) % m;
+                double d0 = v ? Pb[rr * Cp + ca] : 0.0;
+                double d1 = v ? Pb[rr * Cp + ca + 1] : 0.0;
+                const int ra = nb + ti * 8 + g;
+#pragma unroll
+                for (int k0 = 0; k0 < BP; k0 += 4) {
+                    const double a = ra < nrow ? -Lb[ra * LS + k0 + q4] : 0.0;
+                    const double b = Yb[(k0 + q4) * Cp + tcol * 8 + g];
+                    dmma(d0, d1, a, b);
+                }
+                if (v) {
+                    Pb[rr * Cp + ca] = d0;
+                    Pb[rr * Cp + ca + 1] = d1;
+                }
+            } else {
+                const int u = t - nd_t - ne_t;
+                const int t1 = u / tc, t2 = u % tc;
+                const int ca = t2 * 8 + 2 * q4;
+                double d0 = S[(t1 * 8 + g) * Cp + ca];
+                double d1 = S[(t1 * 8 + g) * Cp + ca + 1];
+#pragma unroll
+                for (int k0 = 0; k0 < BP; k0 += 4) {
+                    const double a = -Yb[(k0 + q4) * Cp + t1 * 8 + g];
+                    const double b = Yb[(k0 + q4) * Cp + t2 * 8 + g];
+                    dmma(d0, d1, a, b);
+                }
+                S[(t1 * 8 + g) * Cp + ca] = d0;
+                S[(t1 * 8 + g) * Cp + ca + 1] = d1;
+            }
+        }
+        __syncthreads();
+    }
+    for (int t = tid; t < nd * nd; t += HYB_NT) {
+        const int r = t % nd, c = t / nd;
+        blocks[sys_boff[s] + t] = S[r * Cp + c];      // column-major: Bt[c*nd + r]
+    }
+    for (int r = tid; r < nd; r += HYB_NT) hbar[sys_hoff[s] + r] = S[r * Cp + nd];
+    if (tid == 0) info[s] = 0;
+}
+
+template <int BP>
+__global__ void __launch_bounds__(HYB_NT)
+backsolve_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ sys_pat,
+                 const double *__restrict__ Lstore, const long long *__restrict__ sys_loff,
+                 double *__restrict__ X, const long long *__restrict__ sys_xoff) {
+    constexpr int LS = BP + 4;
+    extern __shared__ double sm[];
+    const int s = blockIdx.x;
+    const MfbHybPattern &P = pats[sys_pat[s]];
+    const int n = P.n, w = P.w, nd = P.ndof;
+    const int Cp = cpad(nd), m = w + BP;
+    double *Xw = sm;                // m x Cp   solved rows (circular)
+    double *Lp = Xw + m * Cp;       // m x LS   panel factor
+    double *Tp = Lp + m * LS;       // BP x Cp  panel rhs
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int g = lane >> 2, q4 = lane & 3;
+    const long long pstride = (long long)m * LS + (long long)BP * Cp;
+    double *Xs = X + sys_xoff[s];
+    const int n_pan = (n + BP - 1) / BP;
+    for (int pi = n_pan - 1; pi >= 0; --pi) {
+        const int k = pi * BP;
+        const int nb = min(BP, n - k);
+        const int rend = min(n, k + BP + w);
+        const int nrow = rend - k, R = nrow - nb;
+        const double *src = Lstore + sys_loff[s] + (long long)pi * pstride;
+        for (int t = tid; t < nrow * LS; t += HYB_NT) Lp[t] = src[t];
+        for (int t = tid; t < BP * Cp; t += HYB_NT) Tp[t] = src[(long long)m * LS + t];
+        __syncthreads();
+        // Tp -= L21^T X[k+nb .. rend)   (DMMA; a warp owns one 8x8 output tile)
+        const int ti_n = BP / 8, tc = Cp >> 3;
+        for (int t = wid; t < ti_n * tc; t += HYB_NW) {
+            const int ti = t / tc, tj = t % tc;
+            const int ca = tj * 8 + 2 * q4;
+            double d0 = Tp[(ti * 8 + g) * Cp + ca];
+            double d1 = Tp[(ti * 8 + g) * Cp + ca + 1];
+            for (int k0 = 0; k0 < R; k0 += 4) {
+                const int kk = k0 + q4;
+                const double a = kk < R ? -Lp[(nb + kk) * LS + ti * 8 + g] : 0.0;
+                const double b = kk < R ? Xw[((k + nb + kk) % m) * Cp + tj * 8 + g] : 0.0;
+                dmma(d0, d1, a, b);
+            }
+            Tp[(ti * 8 + g) * Cp + ca] = d0;
+            Tp[(ti * 8 + g) * Cp + ca + 1] = d1;
+        }
+        __syncthreads();
+        // L11^T x = Tp (backward, one thread per column)
+        for (int c = tid; c < Cp; c += HYB_NT) {
+            for (int q = nb - 1; q >= 0; --q) {
+                double v = Tp[q * Cp + c];
+                for (int qq = q + 1; qq < nb; ++qq) v -= Lp[qq * LS + q] * Tp[qq * Cp + c];
+                v /= Lp[q * LS + q];
+                Tp[q * Cp + c] = v;
+                Xw[((k + q) % m) * Cp + c] = v;
+                Xs[(long long)(k + q) * Cp + c] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(HYB_NT)
+recover_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ sys_pat,
+               const double *__restrict__ Kbuf, const long long *__restrict__ sys_koff,
+               const double *__restrict__ X, const long long *__restrict__ sys_xoff,
+               double *__restrict__ M, const long long *__restrict__ sys_moff,
+               double *__restrict__ Fb, const long long *__restrict__ sys_fboff) {
+    const int s = blockIdx.y;
+    const MfbHybPattern &P = pats[sys_pat[s]];
+    const double *K = Kbuf + sys_koff[s];
+    const int nd = P.ndof, Cp = cpad(nd);
+    const int ne = P.n_edges, nc = P.n_cells;
+    const double *Xs = X + sys_xoff[s];
+    double *Ms = M + sys_moff[s];
+    double *Fs = Fb + sys_fboff[s];
+    const double hx = P.hx, hy = P.hy, s2 = P.s2;
+    const double B[4] = {hy, -hy, hx, -hx};
+    for (int T = blockIdx.x * HYB_NT + threadIdx.x; T < nc; T += gridDim.x * HYB_NT) {
+        const double kap = K[T] / (P.nu * hx * hy);
+        int e[4], kind[4], id[4];
+        for (int a = 0; a < 4; ++a) {
+            e[a] = P.cell_edges[4 * T + a];
+            kind[a] = P.edge_kind[e[a]];
+            id[a] = P.edge_idx[e[a]];
+        }
+        for (int c = 0; c <= nd; ++c) {
+            const bool bar = c == nd;
+            double gv[4], f[4], bg = 0.0, bf = 0.0, b2mu = 0.0;
+            for (int a = 0; a < 4; ++a) {
+                double mu;
+                if (kind[a] == 0) mu = bar ? Xs[(long long)id[a] * Cp + nd] : -Xs[(long long)id[a] * Cp + c];
+                else if (kind[a] == 1) mu = bar ? 0.0 : gcoef(P, id[a], c);
+                else mu = bar ? P.p_val[id[a]] : 0.0;
+                f[a] = (bar && P.has_src) ? P.cell_f[4 * T + a] : 0.0;
+                gv[a] = f[a] + B[a] * mu;
+                bg += B[a] * gv[a];
+                bf += B[a] * f[a];
+                b2mu += B[a] * B[a] * mu;
+            }
+            const double q = (bar && P.has_src) ? P.cell_q[T] : 0.0;
+            double u[4];
+            u[0] = kap * (4.0 * gv[0] - 2.0 * gv[1] - 3.0 * B[0] * bg / s2) - B[0] * q / (2.0 * s2);
+            u[1] = kap * (-2.0 * gv[0] + 4.0 * gv[1] - 3.0 * B[1] * bg / s2) - B[1] * q / (2.0 * s2);
+            u[2] = kap * (4.0 * gv[2] - 2.0 * gv[3] - 3.0 * B[2] * bg / s2) - B[2] * q / (2.0 * s2);
+            u[3] = kap * (-2.0 * gv[2] + 4.0 * gv[3] - 3.0 * B[3] * bg / s2) - B[3] * q / (2.0 * s2);
+            const double p = (bf + b2mu) / (2.0 * s2) + (q != 0.0 ? q / (12.0 * kap * s2) : 0.0);
+            const double cvx = 0.5 * (u[0] + u[1]), cvy = 0.5 * (u[2] + u[3]);
+            const double sg = bar ? 1.0 : -1.0;
+            auto put = [&](long long row, double v) {
+                if (bar) Fs[row] = v;
+                else Ms[row * nd + c] = sg * v;
+            };
+            for (int a = 0; a < 4; ++a)
+                if (P.edge_cells[2 * e[a]] == T) put(e[a], P.edge_noflow[e[a]] ? 0.0 : u[a]);
+            put(ne + T, p);
+            put(ne + nc + 2 * T, cvx);
+            put(ne + nc + 2 * T + 1, cvy);
+            put(ne + 3 * nc + T, p);
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int mfb_darcy_condense(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
+                                  const double *Kbuf, const long long *sys_koff, double *blocks,
+                                  const long long *sys_boff, double *hbar,
+                                  const long long *sys_hoff, double *Lstore,
+                                  const long long *sys_loff, int *info, int panel,
+                                  int smem_bytes, void *stream) {
+    if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
+    cudaStream_t st = mfb_stream(stream);
+    if (panel == 16) {
+        if (cudaFuncSetAttribute(condense_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes) != cudaSuccess)
+            return MFB_ERR_SMEM;
+        condense_kernel<16><<<n_sys, HYB_NT, smem_bytes, st>>>(
+            pats, sys_pat, Kbuf, sys_koff, blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
+    } else if (panel == 8) {
+        if (cudaFuncSetAttribute(condense_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes) != cudaSuccess)
+            return MFB_ERR_SMEM;
+        condense_kernel<8><<<n_sys, HYB_NT, smem_bytes, st>>>(
+            pats, sys_pat, Kbuf, sys_koff, blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
+    } else {
+        return MFB_ERR_ARG;
+    }
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_darcy_backsolve(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
+                                   const double *Lstore, const long long *sys_loff, double *X,
+                                   const long long *sys_xoff, int panel, int smem_bytes,
+                                   void *stream) {
+    if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
+    cudaStream_t st = mfb_stream(stream);
+    if (panel == 16) {
+        if (cudaFuncSetAttribute(backsolve_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes) != cudaSuccess)
+            return MFB_ERR_SMEM;
+        backsolve_kernel<16><<<n_sys, HYB_NT, smem_bytes, st>>>(pats, sys_pat, Lstore, sys_loff,
+                                                                X, sys_xoff);
+    } else if (panel == 8) {
+        if (cudaFuncSetAttribute(backsolve_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes) != cudaSuccess)
+            return MFB_ERR_SMEM;
+        backsolve_kernel<8><<<n_sys, HYB_NT, smem_bytes, st>>>(pats, sys_pat, Lstore, sys_loff,
+                                                               X, sys_xoff);
+    } else {
+        return MFB_ERR_ARG;
+    }
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_darcy_recover(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
+                                 const double *Kbuf, const long long *sys_koff, const double *X,
+                                 const long long *sys_xoff, double *M, const long long *sys_moff,
+                                 double *Fb, const long long *sys_fboff, void *stream) {
+    if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
+    dim3 grid(4, n_sys);
+    recover_kernel<<<grid, HYB_NT, 0, mfb_stream(stream)>>>(pats, sys_pat, Kbuf, sys_koff, X,
+                                                            sys_xoff, M, sys_moff, Fb, sys_fboff);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}

@@ -102,75 +102,49 @@ def get_plan(problem, grid):
     return plan
 
 
-class S3Engine:
-    """Device state of one S3 sweep; methods map 1:1 onto the C ABI calls."""
+class _S3Static:
+    """Everything an S3 sweep needs that depends only on (problem, grid).
 
-    def __init__(self, plan, stream=None):
+    Built once per DevicePlan and kept resident: the system list and its
+    offsets, the KL tables, the wave partition of the basis launches with
+    their workspaces, the output pools and the moment group tables. A call
+    to run_method then only launches kernels and copies results back.
+    """
+
+    def __init__(self, plan, keep_fields=True, darcy_kernel="hybrid"):
         import torch
-        self.torch = torch
-        self.plan = plan
-        self.L = _lib.lib()
-        self.stream = torch.cuda.current_stream() if stream is None else stream
-        self.sp = ctypes.c_void_p(self.stream.cuda_stream)
-        self.launches = 0            # kernels launched through the C ABI
-        self.timing = False          # record CUDA events around the basis solves
-        self.solve_events = []
-        self.solve_flops = []
-
-    def _ev(self):
-        ev = self.torch.cuda.Event(enable_timing=True)
-        ev.record(self.stream)
-        return ev
-
-    # ------------------------------------------------------------ (1) KL --
-    def kl_fields(self):
-        """K for every (Darcy sid, loc) system plus the mean-field K0 buffer."""
-        torch, plan = self.torch, self.plan
-        pb = plan.problem
+        self.darcy_kernel = darcy_kernel
+        pb, grid = plan.problem, plan.grid
         lay = pb.layout
-        systems = plan.s3_systems()
-        koff = np.zeros(len(systems), dtype=np.int64)
-        sys_of = {}
+        f64, i32, i64 = torch.float64, torch.int32, torch.int64
+        self.systems = systems = plan.s3_systems()
+        nsys = len(systems)
+        # (1) KL: K buffer = [K0 | K(sid, loc) for Darcy systems]
+        koff = np.zeros(nsys, dtype=np.int64)
+        first = {}
         cur = plan.k0_len
         for idx, (s, l) in enumerate(systems):
-            sys_of[(s, l)] = idx
+            first.setdefault(s, idx)
             if lay.physics(s) == "darcy":
                 koff[idx] = cur
                 cur += pb.meshes[s].n_cells
-            else:
-                koff[idx] = 0                       # Stokes: the K0 buffer
-        K = torch.empty(max(cur, 1), dtype=torch.float64, device="cuda")
-        self._kl_tabs = []
+        self.koff, self.sys_first = koff, first
+        self.K = torch.empty(max(cur, 1), dtype=f64, device="cuda")
+        self.kl = []
         for s in plan.darcy:
             r = lay.blocks[s].kl_region
             c = pb.meshes[s].centroids
             phi, mean = pb.perm.mode_table(r, c[:, 0], c[:, 1])
             nt = phi.shape[1]
             xi = np.zeros((1 + int(plan.n_loc[s]), nt))
-            xi[1:] = plan.grid.local_points[r][:, :nt]
-            d_phi, d_mean, d_xi = (_dev(phi, torch.float64), _dev(mean, torch.float64),
-                                   _dev(xi, torch.float64))
-            self._kl_tabs.append((d_phi, d_mean, d_xi))
-            nc = len(mean)
-            # mean field -> K0 slot, local realizations -> their system slots
-            self.launches += 2
-            _lib.check(self.L.mfb_kl_realize(_ptr(d_phi), _ptr(d_mean), nc, nt, _ptr(d_xi),
-                                             1, ctypes.c_void_p(K.data_ptr() + 8 * plan.k0_off[s]),
-                                             self.sp), "mfb_kl_realize")
-            first = koff[sys_of[(s, 0)]]
-            _lib.check(self.L.mfb_kl_realize(
-                _ptr(d_phi), _ptr(d_mean), nc, nt,
-                ctypes.c_void_p(d_xi.data_ptr() + 8 * nt), int(plan.n_loc[s]),
-                ctypes.c_void_p(K.data_ptr() + 8 * int(first)), self.sp), "mfb_kl_realize")
-        self.K, self.koff, self.systems = K, koff, systems
-        return K
-
-    # ------------------------------------------------------- (2) bases ----
-    def build_bases(self, threads=None, keep_fields=True):
-        torch, plan = self.torch, self.plan
-        systems = self.systems
+            xi[1:] = grid.local_points[r][:, :nt]
+            self.kl.append((s, len(mean), nt, _dev(phi, f64), _dev(mean, f64), _dev(xi, f64),
+                            int(koff[first[s]])))
+        self.kl_h2d_bytes = sum(8 * (t[3].numel() + t[4].numel() + t[5].numel())
+                                for t in self.kl)
+        self._plan = plan
+        # (2) systems: pools and waves
         pats = plan.patterns
-        nsys = len(systems)
         sys_pat = np.array([s for s, _ in systems], dtype=np.int32)
         nd = plan.ndof[sys_pat].astype(np.int64)
         nf = plan.nfield[sys_pat].astype(np.int64)
@@ -178,121 +152,93 @@ class S3Engine:
         hoff = np.concatenate([[0], np.cumsum(nd)])
         moff = np.concatenate([[0], np.cumsum(nf * nd)])
         fboff = np.concatenate([[0], np.cumsum(nf)])
-        self.blocks = torch.empty(int(boff[-1]), dtype=torch.float64, device="cuda")
-        self.hbar = torch.empty(int(hoff[-1]), dtype=torch.float64, device="cuda")
-        self.M = torch.empty(int(moff[-1]) if keep_fields else 0, dtype=torch.float64,
-                             device="cuda")
-        self.Fb = torch.empty(int(fboff[-1]) if keep_fields else 0, dtype=torch.float64,
-                              device="cuda")
+        self.keep_fields = keep_fields
+        self.blocks = torch.empty(int(boff[-1]), dtype=f64, device="cuda")
+        self.hbar = torch.empty(int(hoff[-1]), dtype=f64, device="cuda")
+        self.M = torch.empty(int(moff[-1]) if keep_fields else 0, dtype=f64, device="cuda")
+        self.Fb = torch.empty(int(fboff[-1]) if keep_fields else 0, dtype=f64, device="cuda")
         self.sys_boff, self.sys_hoff = boff[:-1], hoff[:-1]
         self.sys_moff, self.sys_fboff = moff[:-1], fboff[:-1]
-        self.info = torch.zeros(nsys, dtype=torch.int32, device="cuda")
-        work_d = np.array([pats[s].work_doubles for s, _ in systems], dtype=np.int64)
-        x_d = np.array([pats[s].x_doubles for s, _ in systems], dtype=np.int64)
-        smem = max(p.smem_doubles for p in pats)
-        # waves bounded by the workspace budget
-        per = 8 * (work_d + x_d)
-        start = 0
-        d_pat = _dev(sys_pat, torch.int32)
-        d_koff = _dev(self.koff, torch.int64)
-        d_boff, d_hoff = _dev(boff[:-1], torch.int64), _dev(hoff[:-1], torch.int64)
-        d_moff, d_fboff = _dev(moff[:-1], torch.int64), _dev(fboff[:-1], torch.int64)
-        phys = [plan.problem.layout.physics(s) for s, _ in systems]
-        while start < nsys:
-            end, acc = start, 0
-            while end < nsys and (end == start or (acc + per[end] <= WORK_BUDGET_BYTES
-                                                   and phys[end] == phys[start])):
-                acc += per[end]
-                end += 1
-            cnt = end - start
-            woff = np.concatenate([[0], np.cumsum(work_d[start:end])])
-            xoff = np.concatenate([[0], np.cumsum(x_d[start:end])])
-            work = torch.empty(int(woff[-1]), dtype=torch.float64, device="cuda")
-            X = torch.empty(int(xoff[-1]), dtype=torch.float64, device="cuda")
-            d_woff, d_xoff = _dev(woff[:-1], torch.int64), _dev(xoff[:-1], torch.int64)
-            nt = threads or (512 if max(pats[s].kl for s, _ in systems[start:end]) > 128
-                             else 256)
-            sub = lambda t, elt=8: ctypes.c_void_p(t.data_ptr() + elt * start)
-            if self.timing:
-                e0 = self._ev()
-            _lib.check(self.L.mfb_systems_solve(
-                _ptr(plan.pat_dev), cnt, sub(d_pat, 4), _ptr(self.K), sub(d_koff),
-                _ptr(work), _ptr(d_woff), _ptr(X), _ptr(d_xoff), sub(self.info, 4), nt, smem,
-                self.sp), "mfb_systems_solve")
-            if self.timing:
-                self.solve_events.append((e0, self._ev()))
-                self.solve_flops.append(sum(pats[s].algorithmic_flops for s, _ in
-                                            systems[start:end]))
-            self.launches += 2
-            _lib.check(self.L.mfb_systems_extract(
-                _ptr(plan.pat_dev), cnt, sub(d_pat, 4), _ptr(X), _ptr(d_xoff),
-                _ptr(self.blocks), sub(d_boff), _ptr(self.hbar), sub(d_hoff),
-                _ptr(self.M) if keep_fields else None, sub(d_moff),
-                _ptr(self.Fb) if keep_fields else None, sub(d_fboff), self.sp),
-                "mfb_systems_extract")
-            start = end
-        self.d_sys_moff, self.d_sys_fboff = d_moff, d_fboff
-        # per-sid bases into the pool
-        first = {}
-        for idx, (s, l) in enumerate(systems):
-            first.setdefault(s, idx)
+        self.d_pat = _dev(sys_pat, i32)
+        self.d_koff = _dev(koff, i64)
+        self.d_boff, self.d_hoff = _dev(boff[:-1], i64), _dev(hoff[:-1], i64)
+        self.d_moff, self.d_fboff = _dev(moff[:-1], i64), _dev(fboff[:-1], i64)
+        phys = [lay.physics(s) for s, _ in systems]
+        use_hyb = [ph == "darcy" and self.darcy_kernel == "hybrid" for ph in phys]
+
+        def sub(idx):
+            idx = np.asarray(idx, dtype=np.int64)
+            return {"idx": idx, "pat": _dev(sys_pat[idx], i32), "koff": _dev(koff[idx], i64),
+                    "boff": _dev(boff[:-1][idx], i64), "hoff": _dev(hoff[:-1][idx], i64),
+                    "moff": _dev(moff[:-1][idx], i64), "fboff": _dev(fboff[:-1][idx], i64)}
+
+        # generic banded-LU waves (Stokes, or every system when forced)
+        self.smem = max(p.smem_doubles for p in pats)
+        gen = [i for i in range(nsys) if not use_hyb[i]]
+        work_d = {i: pats[systems[i][0]].work_doubles for i in gen}
+        x_d = {i: pats[systems[i][0]].x_doubles for i in gen}
+        self.waves, wmax, xmax = [], 0, 0
+        pos = 0
+        while pos < len(gen):
+            grp, acc = [], 0
+            while pos < len(gen) and (not grp or (acc + 8 * (work_d[gen[pos]] + x_d[gen[pos]])
+                                                  <= WORK_BUDGET_BYTES
+                                                  and phys[gen[pos]] == phys[grp[0]])):
+                acc += 8 * (work_d[gen[pos]] + x_d[gen[pos]])
+                grp.append(gen[pos])
+                pos += 1
+            woff = np.concatenate([[0], np.cumsum([work_d[i] for i in grp])])
+            xoff = np.concatenate([[0], np.cumsum([x_d[i] for i in grp])])
+            nt = 512 if max(pats[systems[i][0]].kl for i in grp) > 128 else 256
+            w = sub(grp)
+            w["info"] = torch.zeros(len(grp), dtype=i32, device="cuda")
+            w.update(nt=nt, woff=_dev(woff[:-1], i64), xoff=_dev(xoff[:-1], i64),
+                     flops=sum(pats[systems[i][0]].algorithmic_flops for i in grp))
+            self.waves.append(w)
+            wmax, xmax = max(wmax, int(woff[-1])), max(xmax, int(xoff[-1]))
+        # hybrid (SPD condensation) waves for Darcy systems, grouped by panel width
+        hyb = [i for i in range(nsys) if use_hyb[i]]
+        self.hwaves = []
+        lmax = hxmax = 0
+        for panel in (16, 8):
+            idxs = [i for i in hyb if plan.hyb_panel[systems[i][0]] == panel]
+            pos = 0
+            while pos < len(idxs):
+                grp, acc = [], 0
+                while pos < len(idxs):
+                    h = plan.hyb[systems[idxs[pos]][0]]
+                    _, _, _, ld, xd = h.layout_for(panel)
+                    cost = 8 * (ld + xd) if keep_fields else 0
+                    if grp and acc + cost > WORK_BUDGET_BYTES:
+                        break
+                    acc += cost
+                    grp.append(idxs[pos])
+                    pos += 1
+                lays = [plan.hyb[systems[i][0]].layout_for(panel) for i in grp]
+                loff = np.concatenate([[0], np.cumsum([l[3] for l in lays])])
+                hxoff = np.concatenate([[0], np.cumsum([l[4] for l in lays])])
+                w = sub(grp)
+                w["info"] = torch.zeros(len(grp), dtype=i32, device="cuda")
+                w.update(panel=panel, smem_c=max(l[1] for l in lays),
+                         smem_b=max(l[2] for l in lays), loff=_dev(loff[:-1], i64),
+                         xoff=_dev(hxoff[:-1], i64),
+                         flops=sum(plan.hyb[systems[i][0]].algorithmic_flops for i in grp),
+                         survey_flops=sum(pats[systems[i][0]].algorithmic_flops for i in grp))
+                self.hwaves.append(w)
+                lmax, hxmax = max(lmax, int(loff[-1])), max(hxmax, int(hxoff[-1]))
+        self.work = torch.empty(max(wmax, 1), dtype=f64, device="cuda")
+        self.X = torch.empty(max(xmax, 1), dtype=f64, device="cuda")
+        self.Lstore = torch.empty(max(lmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
+        self.HX = torch.empty(max(hxmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
         self.blk_base = np.array([boff[first[s]] for s in range(plan.n_sub)], dtype=np.int64)
         self.h_base = np.array([hoff[first[s]] for s in range(plan.n_sub)], dtype=np.int64)
-        self.sys_first = first
-
-    def check_info(self):
-        info = self.info.cpu().numpy()
-        bad = np.nonzero(info != 0)[0]
-        if len(bad):
-            s, l = self.systems[bad[0]]
-            raise SingularOperatorError(
-                f"subdomain {s} (local realization {l}): singular system "
-                f"(device info {int(info[bad[0]])})")
-
-    # ---------------------------------------------------------- (3) CG ----
-    def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False):
-        torch, plan = self.torch, self.plan
-        n_real = plan.grid.n_real
-        n_pts = n_real - k0 if n_pts is None else n_pts
-        nl = plan.n_lambda
-        hist_cap = max_iter if hist_cap is None else hist_cap
-        lam = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda")
-        iters = torch.empty(n_pts, dtype=torch.int32, device="cuda")
-        status = torch.empty(n_pts, dtype=torch.int32, device="cuda")
-        hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=torch.float64, device="cuda")
-        g = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda") if keep_g else None
-        d_blk, d_h = _dev(self.blk_base, torch.int64), _dev(self.h_base, torch.int64)
-        self.launches += 1
-        _lib.check(self.L.mfb_cg_batched(
-            nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
-            _ptr(plan.d_region), _ptr(d_blk), _ptr(d_h), _ptr(plan.d_local), n_real,
-            _ptr(self.blocks), _ptr(self.hbar), k0, n_pts, float(tol), int(max_iter),
-            _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
-            _ptr(g) if keep_g else None, self.sp), "mfb_cg_batched")
-        return lam, iters, status, hist, g
-
-    # ----------------------------------------------------- (4) moments ----
-    def moments(self, lam):
-        torch, plan = self.torch, self.plan
-        grid = plan.grid
-        nl, n_real = plan.n_lambda, grid.n_real
-        out = {}
-        m = torch.empty(nl, dtype=torch.float64, device="cuda")
-        v = torch.empty_like(m)
-        q = torch.empty_like(m)
-        self.launches += 4
-        _lib.check(self.L.mfb_lambda_moments(nl, n_real, _ptr(lam), _ptr(plan.d_weights),
-                                             _ptr(m), _ptr(v), _ptr(q), self.sp),
-                   "mfb_lambda_moments")
-        # groups = systems; members from the region local-index tables
-        systems = self.systems
-        ng = len(systems)
-        members, gptr = [], [0]
-        order_cache = {}
+        self.d_blk, self.d_h = _dev(self.blk_base, i64), _dev(self.h_base, i64)
+        # (4) moment groups = systems; members from the region local-index tables
+        members, gptr, order_cache = [], [0], {}
         for s, l in systems:
             r = plan.region[s]
             if r < 0:
-                mem = np.arange(n_real)
+                mem = np.arange(grid.n_real)
             else:
                 if r not in order_cache:
                     li = grid.local_indices[r]
@@ -303,49 +249,204 @@ class S3Engine:
                 mem = order[bounds[l]:bounds[l + 1]]
             members.append(mem)
             gptr.append(gptr[-1] + len(mem))
-        grp_sid = np.array([s for s, _ in systems], dtype=np.int32)
-        nd = plan.ndof[grp_sid].astype(np.int64)
         voff = np.concatenate([[0], np.cumsum(nd)])
         coff = np.concatenate([[0], np.cumsum(nd * nd)])
-        d_sid = _dev(grp_sid, torch.int32)
-        d_gptr = _dev(np.array(gptr), torch.int32)
-        d_mem = _dev(np.concatenate(members), torch.int32)
-        d_voff, d_coff = _dev(voff[:-1], torch.int64), _dev(coff[:-1], torch.int64)
-        W = torch.empty(ng, dtype=torch.float64, device="cuda")
-        lstar = torch.empty(int(voff[-1]), dtype=torch.float64, device="cuda")
+        self.d_gptr = _dev(np.array(gptr), i32)
+        self.d_mem = _dev(np.concatenate(members), i32)
+        self.d_voff, self.d_coff = _dev(voff[:-1], i64), _dev(coff[:-1], i64)
+        self.nv, self.nc = int(voff[-1]), int(coff[-1])
+        sid_gptr = np.array([first[s] for s in range(plan.n_sub)] + [nsys], dtype=np.int32)
+        self.d_sgptr = _dev(sid_gptr, i32)
+        self.out_off = np.concatenate([[0], np.cumsum(plan.nfield.astype(np.int64))])
+        self.d_outoff = _dev(self.out_off[:-1], i64)
+        self.wtot = float(np.sum(grid.weights))
+
+
+    def refresh_inputs(self):
+        """Re-upload the sweep's inputs from the host: collocation weights, local
+        index tables and the KL tables (Phi, mean, local points). Returns bytes."""
+        import torch
+        plan, grid = self._plan, self._plan.grid
+        nbytes = 0
+        li = np.stack(grid.local_indices).astype(np.int32) if grid.local_indices else \
+            np.zeros((1, grid.n_real), dtype=np.int32)
+        plan.d_local.copy_(torch.from_numpy(li))
+        plan.d_weights.copy_(torch.from_numpy(np.ascontiguousarray(grid.weights)))
+        nbytes += li.nbytes + grid.weights.nbytes
+        pb = plan.problem
+        for s, nc, nt, d_phi, d_mean, d_xi, first in self.kl:
+            r = pb.layout.blocks[s].kl_region
+            c = pb.meshes[s].centroids
+            phi, mean = pb.perm.mode_table(r, c[:, 0], c[:, 1])
+            xi = np.zeros((1 + int(plan.n_loc[s]), nt))
+            xi[1:] = grid.local_points[r][:, :nt]
+            for d, h in ((d_phi, phi), (d_mean, mean), (d_xi, xi)):
+                d.copy_(torch.from_numpy(np.ascontiguousarray(h)).view(d.shape))
+                nbytes += h.nbytes
+        return nbytes
+
+
+class S3Engine:
+    """Device work of one S3 sweep; methods map 1:1 onto the C ABI calls."""
+
+    def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid"):
+        import torch
+        self.torch = torch
+        self.plan = plan
+        self.L = _lib.lib()
+        self.st = plan.s3_static(keep_fields, darcy_kernel)
+        self.stream = torch.cuda.current_stream() if stream is None else stream
+        self.sp = ctypes.c_void_p(self.stream.cuda_stream)
+        self.launches = 0            # kernels launched through the C ABI
+        self.timing = False          # record CUDA events around the basis solves
+        self.solve_events = []
+        self.solve_flops = []
+
+    def __getattr__(self, name):     # pools live in the static state
+        return getattr(self.__dict__["st"], name)
+
+    def _ev(self):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        return ev
+
+    # ------------------------------------------------------------ (1) KL --
+    def kl_fields(self):
+        """K for every (Darcy sid, loc) system plus the mean-field K0 buffer."""
+        st, plan = self.st, self.plan
+        K = st.K
+        for s, nc, nt, d_phi, d_mean, d_xi, first in st.kl:
+            self.launches += 2
+            _lib.check(self.L.mfb_kl_realize(
+                _ptr(d_phi), _ptr(d_mean), nc, nt, _ptr(d_xi), 1,
+                ctypes.c_void_p(K.data_ptr() + 8 * plan.k0_off[s]), self.sp), "mfb_kl_realize")
+            _lib.check(self.L.mfb_kl_realize(
+                _ptr(d_phi), _ptr(d_mean), nc, nt, ctypes.c_void_p(d_xi.data_ptr() + 8 * nt),
+                int(plan.n_loc[s]), ctypes.c_void_p(K.data_ptr() + 8 * first), self.sp),
+                "mfb_kl_realize")
+        return K
+
+    # ------------------------------------------------------- (2) bases ----
+    def build_bases(self):
+        st, plan = self.st, self.plan
+        P = ctypes.c_void_p
+        for w in st.waves:                      # generic banded LU (Stokes)
+            cnt = len(w["idx"])
+            if self.timing:
+                e0 = self._ev()
+            _lib.check(self.L.mfb_systems_solve(
+                _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
+                _ptr(st.work), _ptr(w["woff"]), _ptr(st.X), _ptr(w["xoff"]), _ptr(w["info"]),
+                w["nt"], st.smem, self.sp), "mfb_systems_solve")
+            if self.timing:
+                self.solve_events.append(("band", e0, self._ev(), w["flops"], w["flops"]))
+            self.launches += 2
+            _lib.check(self.L.mfb_systems_extract(
+                _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.X), _ptr(w["xoff"]),
+                _ptr(st.blocks), _ptr(w["boff"]), _ptr(st.hbar), _ptr(w["hoff"]),
+                _ptr(st.M) if st.keep_fields else None, _ptr(w["moff"]),
+                _ptr(st.Fb) if st.keep_fields else None, _ptr(w["fboff"]), self.sp),
+                "mfb_systems_extract")
+        for w in st.hwaves:                     # hybridised Darcy condensation
+            cnt = len(w["idx"])
+            keep = st.keep_fields
+            if self.timing:
+                e0 = self._ev()
+            _lib.check(self.L.mfb_darcy_condense(
+                _ptr(plan.hyb_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
+                _ptr(st.blocks), _ptr(w["boff"]), _ptr(st.hbar), _ptr(w["hoff"]),
+                _ptr(st.Lstore) if keep else None, _ptr(w["loff"]), _ptr(w["info"]),
+                w["panel"], w["smem_c"], self.sp), "mfb_darcy_condense")
+            if self.timing:
+                self.solve_events.append(("hybrid", e0, self._ev(), w["flops"],
+                                          w["survey_flops"]))
+            self.launches += 1
+            if keep:
+                self.launches += 2
+                _lib.check(self.L.mfb_darcy_backsolve(
+                    _ptr(plan.hyb_dev), cnt, _ptr(w["pat"]), _ptr(st.Lstore), _ptr(w["loff"]),
+                    _ptr(st.HX), _ptr(w["xoff"]), w["panel"], w["smem_b"], self.sp),
+                    "mfb_darcy_backsolve")
+                _lib.check(self.L.mfb_darcy_recover(
+                    _ptr(plan.hyb_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
+                    _ptr(st.HX), _ptr(w["xoff"]), _ptr(st.M), _ptr(w["moff"]), _ptr(st.Fb),
+                    _ptr(w["fboff"]), self.sp), "mfb_darcy_recover")
+
+    def check_info(self):
+        info = np.zeros(len(self.st.systems), dtype=np.int64)
+        for w in self.st.waves + self.st.hwaves:
+            info[w["idx"]] = w["info"].cpu().numpy()
+        bad = np.nonzero(info != 0)[0]
+        if len(bad):
+            s, l = self.st.systems[bad[0]]
+            raise SingularOperatorError(
+                f"subdomain {s} (local realization {l}): singular system "
+                f"(device info {int(info[bad[0]])})")
+
+    # ---------------------------------------------------------- (3) CG ----
+    def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False):
+        torch, plan, st = self.torch, self.plan, self.st
+        n_real = plan.grid.n_real
+        n_pts = n_real - k0 if n_pts is None else n_pts
+        nl = plan.n_lambda
+        hist_cap = max_iter if hist_cap is None else hist_cap
+        lam = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda")
+        iters = torch.empty(n_pts, dtype=torch.int32, device="cuda")
+        status = torch.empty(n_pts, dtype=torch.int32, device="cuda")
+        hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=torch.float64, device="cuda")
+        g = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda") if keep_g else None
+        self.launches += 1
+        _lib.check(self.L.mfb_cg_batched(
+            nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
+            _ptr(plan.d_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(plan.d_local), n_real,
+            _ptr(st.blocks), _ptr(st.hbar), k0, n_pts, float(tol), int(max_iter),
+            _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
+            _ptr(g) if keep_g else None, self.sp), "mfb_cg_batched")
+        return lam, iters, status, hist, g
+
+    # ----------------------------------------------------- (4) moments ----
+    def moments(self, lam):
+        torch, plan, st = self.torch, self.plan, self.st
+        nl, n_real = plan.n_lambda, plan.grid.n_real
+        f64 = torch.float64
+        ng = len(st.systems)
+        m = torch.empty(3 * nl, dtype=f64, device="cuda")
+        self.launches += 4
+        _lib.check(self.L.mfb_lambda_moments(
+            nl, n_real, _ptr(lam), _ptr(plan.d_weights), _ptr(m),
+            ctypes.c_void_p(m.data_ptr() + 8 * nl), ctypes.c_void_p(m.data_ptr() + 16 * nl),
+            self.sp), "mfb_lambda_moments")
+        W = torch.empty(ng, dtype=f64, device="cuda")
+        lstar = torch.empty(st.nv, dtype=f64, device="cuda")
         s_ = torch.empty_like(lstar)
-        C = torch.empty(int(coff[-1]), dtype=torch.float64, device="cuda")
+        C = torch.empty(st.nc, dtype=f64, device="cuda")
         _lib.check(self.L.mfb_group_stats(
-            ng, _ptr(d_sid), _ptr(d_gptr), _ptr(d_mem), _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr),
-            _ptr(plan.d_dof_map), nl, _ptr(lam), _ptr(plan.d_weights), _ptr(d_voff),
-            _ptr(d_coff), _ptr(W), _ptr(lstar), _ptr(s_), _ptr(C), self.sp), "mfb_group_stats")
-        nfb = int(self.Fb.numel())
-        fstar = torch.empty(nfb, dtype=torch.float64, device="cuda")
-        t = torch.empty_like(fstar)
-        qq = torch.empty_like(fstar)
+            ng, _ptr(st.d_pat), _ptr(st.d_gptr), _ptr(st.d_mem), _ptr(plan.d_ndof),
+            _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map), nl, _ptr(lam), _ptr(plan.d_weights),
+            _ptr(st.d_voff), _ptr(st.d_coff), _ptr(W), _ptr(lstar), _ptr(s_), _ptr(C),
+            self.sp), "mfb_group_stats")
+        nfb = int(st.Fb.numel())
+        fstar = torch.empty(3 * nfb, dtype=f64, device="cuda")
+        fp = fstar.data_ptr()
         _lib.check(self.L.mfb_group_fields(
-            ng, _ptr(d_sid), _ptr(plan.d_ndof), _ptr(plan.d_nfield), _ptr(self.M),
-            _ptr(self.d_sys_moff), _ptr(self.Fb), _ptr(self.d_sys_fboff), _ptr(d_voff),
-            _ptr(d_coff), _ptr(lstar), _ptr(s_), _ptr(C), _ptr(fstar), _ptr(t), _ptr(qq),
-            self.sp), "mfb_group_fields")
-        sid_gptr = np.array([self.sys_first[s] for s in range(plan.n_sub)] + [ng],
-                            dtype=np.int32)
-        out_off = np.concatenate([[0], np.cumsum(plan.nfield.astype(np.int64))])
-        mean_f = torch.empty(int(out_off[-1]), dtype=torch.float64, device="cuda")
-        var_f = torch.empty_like(mean_f)
-        wtot = float(np.sum(grid.weights))
-        d_sgptr = _dev(sid_gptr, torch.int32)
-        d_outoff = _dev(out_off[:-1], torch.int64)
+            ng, _ptr(st.d_pat), _ptr(plan.d_ndof), _ptr(plan.d_nfield), _ptr(st.M),
+            _ptr(st.d_moff), _ptr(st.Fb), _ptr(st.d_fboff), _ptr(st.d_voff),
+            _ptr(st.d_coff), _ptr(lstar), _ptr(s_), _ptr(C), ctypes.c_void_p(fp),
+            ctypes.c_void_p(fp + 8 * nfb), ctypes.c_void_p(fp + 16 * nfb), self.sp),
+            "mfb_group_fields")
+        nout = int(st.out_off[-1])
+        mv = torch.empty(2 * nout, dtype=f64, device="cuda")
         _lib.check(self.L.mfb_moments_reduce(
-            plan.n_sub, _ptr(d_sgptr), _ptr(plan.d_nfield),
-            _ptr(self.d_sys_fboff), _ptr(W), _ptr(fstar), _ptr(t), _ptr(qq), wtot,
-            _ptr(d_outoff), _ptr(mean_f), _ptr(var_f), self.sp),
-            "mfb_moments_reduce")
-        mh, vh, qh = m.cpu().numpy(), v.cpu().numpy(), q.cpu().numpy()
-        out["lambda"] = _finalize("lambda", mh, vh, qh)
-        mf, vf = mean_f.cpu().numpy(), var_f.cpu().numpy()
+            plan.n_sub, _ptr(st.d_sgptr), _ptr(plan.d_nfield), _ptr(st.d_fboff), _ptr(W),
+            ctypes.c_void_p(fp), ctypes.c_void_p(fp + 8 * nfb), ctypes.c_void_p(fp + 16 * nfb),
+            st.wtot, _ptr(st.d_outoff), _ptr(mv), ctypes.c_void_p(mv.data_ptr() + 8 * nout),
+            self.sp), "mfb_moments_reduce")
+        lm = m.cpu().numpy()
+        out = {"lambda": _finalize("lambda", lm[:nl], lm[nl:2 * nl], lm[2 * nl:])}
+        mvh = mv.cpu().numpy()
+        mf, vf = mvh[:nout], mvh[nout:]
         for s in range(plan.n_sub):
-            base = out_off[s]
+            base = st.out_off[s]
             for name, start, shape in plan.patterns[s].field_layout:
                 size = int(np.prod(shape))
                 mm = mf[base + start: base + start + size].reshape(shape)
@@ -389,6 +490,7 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     _check_basis_cap(plan.basis_bytes(), basis_cap_mb)
     timings = {"plan": time.perf_counter() - t0}
     eng = S3Engine(plan)
+    timings["h2d_bytes"] = eng.st.refresh_inputs()
     t1 = time.perf_counter()
     eng.kl_fields()
     eng.build_bases()

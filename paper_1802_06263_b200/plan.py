@@ -13,6 +13,7 @@ import numpy as np
 
 from . import _lib
 from .discretization import darcy_pattern, stokes_pattern
+from .hybrid import hybrid_pattern
 
 
 def _dev(a, dtype):
@@ -63,7 +64,10 @@ class DevicePlan:
                                 for s in range(self.n_sub)], dtype=np.int32)
         self.n_loc = np.array([grid.local_counts[r] if r >= 0 else 1 for r in self.region],
                               dtype=np.int64)
+        self.hyb = {s: hybrid_pattern(problem, s) for s in self.darcy}
+        self.hyb_panel = {s: h.choose_panel() for s, h in self.hyb.items()}
         self._upload_patterns()
+        self._upload_hybrid()
         self._upload_tables()
 
     # ---------------------------------------------------------------- upload
@@ -98,6 +102,50 @@ class DevicePlan:
         host = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
         self.pat_dev = host.to("cuda")
 
+    def _upload_hybrid(self):
+        """MfbHybPattern per subdomain (Darcy entries filled; index = sid)."""
+        torch = self.torch
+        i32, f64 = torch.int32, torch.float64
+        structs = (_lib.MfbHybPattern * self.n_sub)()
+        self._keep_h = []
+        for s, h in self.hyb.items():
+            # transpose of G: mortar dof -> (interface edge id, coefficient)
+            gam_edge = np.nonzero(h.edge_kind == 1)[0]
+            order = np.argsort(h.edge_idx[gam_edge])
+            gam_edge = gam_edge[order]
+            rows = np.repeat(gam_edge, np.diff(h.gam_ptr))
+            o = np.argsort(h.gam_d, kind="stable")
+            dof_ptr = np.zeros(h.ndof + 1, dtype=np.int64)
+            np.add.at(dof_ptr, h.gam_d + 1, 1)
+            dof_ptr = np.cumsum(dof_ptr)
+            arrs = {
+                "row_edge": _dev(h.row_edge, i32), "edge_kind": _dev(h.edge_kind, i32),
+                "edge_idx": _dev(h.edge_idx, i32), "edge_cells": _dev(h.edge_cells.ravel(), i32),
+                "edge_slot": _dev(h.edge_slot.ravel(), i32),
+                "edge_noflow": _dev(h.edge_noflow, i32),
+                "cell_edges": _dev(h.cell_edges.ravel(), i32),
+                "gam_ptr": _dev(h.gam_ptr, i32), "gam_d": _dev(h.gam_d, i32),
+                "gam_c": _dev(h.gam_c, f64), "dof_ptr": _dev(dof_ptr, i32),
+                "dof_edge": _dev(rows[o], i32), "dof_coef": _dev(h.gam_c[o], f64),
+                "p_val": _dev(h.p_val, f64), "src_k": _dev(h.src_k.ravel(), f64),
+                "src_c": _dev(h.src_c.ravel(), f64), "cell_f": _dev(h.cell_f.ravel(), f64),
+                "cell_q": _dev(h.cell_q, f64),
+            }
+            self._keep_h.append(arrs)
+            st = structs[s]
+            ws = h.layout_for(self.hyb_panel[s])[0]
+            st.n, st.w, st.ws, st.ndof, st.nfield = h.n, h.w, ws, h.ndof, h.nfield
+            st.n_edges, st.n_cells = len(h.edge_kind), len(h.cell_q)
+            st.has_src = int(h.has_src)
+            st.hx, st.hy, st.nu = h.hx, h.hy, h.nu
+            st.s2 = h.hx * h.hx + h.hy * h.hy
+            for i, v in enumerate(h.Hhat.ravel()):
+                st.Hhat[i] = float(v)
+            for name, t in arrs.items():
+                setattr(st, name, _ptr(t).value or 0)
+        raw = bytes(structs)
+        self.hyb_dev = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to("cuda")
+
     def _upload_tables(self):
         torch = self.torch
         g = self.grid
@@ -118,6 +166,16 @@ class DevicePlan:
         for s in range(self.n_sub):
             out += [(s, l) for l in range(int(self.n_loc[s]))]
         return out
+
+    def s3_static(self, keep_fields=True, darcy_kernel="hybrid"):
+        st = getattr(self, "_s3_static", None)
+        if (st is None or (keep_fields and not st.keep_fields)
+                or st.darcy_kernel != darcy_kernel):
+            from .interface import _S3Static
+            self._s3_static = None
+            st = _S3Static(self, keep_fields, darcy_kernel)
+            self._s3_static = st
+        return st
 
     def basis_bytes(self):
         return [8 * int(self.ndof[s]) ** 2 * int(self.n_loc[s]) for s in range(self.n_sub)]

@@ -149,9 +149,9 @@ def test_cfg5_basis_blocks(gpu):
     grid.local_points = [loc.points.copy() for _ in range(4)]
     grid.local_counts = [729] * 4
     plan = get_plan(problem, grid)
-    eng = S3Engine(plan)
+    eng = S3Engine(plan, keep_fields=False)
     eng.kl_fields()
-    eng.build_bases(keep_fields=False)
+    eng.build_bases()
     eng.check_info()
     blocks = eng.blocks.cpu().numpy()
     for idx, (s, l) in enumerate(eng.systems):

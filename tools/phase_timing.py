@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--tol", type=float, default=1e-11)
     ap.add_argument("--no-cg", action="store_true")
+    ap.add_argument("--darcy", default="hybrid", choices=["hybrid", "band"])
     a = ap.parse_args()
     path = a.config if a.config.endswith(".json") else f"configs/{a.config}.json"
     t = time.time()
@@ -33,7 +34,7 @@ def main():
     print(f"setup {t_setup:.2f}s plan {t_plan:.2f}s n_real {grid.n_real} "
           f"n_lambda {plan.n_lambda} systems {len(plan.s3_systems())}", flush=True)
     for rep in range(a.reps):
-        eng = S3Engine(plan)
+        eng = S3Engine(plan, darcy_kernel=a.darcy)
         eng.timing = True
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
@@ -56,8 +57,11 @@ def main():
             it = iters.cpu().numpy()
             msg += f" | iters mean {it.mean():.1f} max {it.max()} status {np.bincount(status.cpu().numpy())}"
         print(f"rep {rep}: {msg}", flush=True)
-        for (a0, a1), fl in zip(eng.solve_events, eng.solve_flops):
-            print(f"   solve launch {a0.elapsed_time(a1):.2f} ms, {fl / 1e9:.2f} GFLOP algorithmic")
+        for kind, a0, a1, fl, sfl in eng.solve_events:
+            ms = a0.elapsed_time(a1)
+            print(f"   {kind:6s} launch {ms:8.2f} ms, {fl / 1e9:8.2f} GFLOP executed "
+                  f"({fl / ms / 1e9:6.2f} TF/s), survey-algorithmic {sfl / 1e9:8.2f} GFLOP "
+                  f"({sfl / ms / 1e9:6.2f} TF/s)")
 
 
 if __name__ == "__main__":
