@@ -108,6 +108,15 @@ typedef struct MfbHybPattern {
     const int *dof_ptr, *dof_edge;
     const double *dof_coef;
     const double *p_val, *src_k, *src_c, *cell_f, *cell_q;
+    /* assembly term tables (hybrid.py::assembly_tables): window/border row
+     * entries (CSR over rows; dest <= w: band offset, else w+1+border col)
+     * and the initial border block entries (dest = d1*(ndof+1)+d2); every
+     * term is coef*K[cell] (cell >= 0) or coef (cell < 0). */
+    int z_n;
+    const int *asm_ptr, *asm_row, *asm_dest, *asm_tptr, *asm_cell;
+    const double *asm_coef;
+    const int *z_dest, *z_tptr, *z_cell;
+    const double *z_coef;
 } MfbHybPattern;
 
 const char *mfb_version(void);
@@ -207,6 +216,8 @@ int mfb_lambda_moments(int n_lambda, int n_real, const double *lam,
  * the bar jump h. If Lstore != NULL the factor panels are kept for
  * mfb_darcy_backsolve (layout: per panel m*(panel+4) L doubles then
  * panel*Cp rhs doubles, m = w + panel, Cp = ndof+1 rounded up to 8).
+ * `panel` = width | (rows_per_lane << 8) with rows_per_lane >=
+ * ceil((w + width) / 32) (the panel warp keeps its rows in registers).
  * info[s] = -(pivot index + 1) if a pivot is not positive. smem_bytes:
  * 8 * (m*ws + m*Cp + Cp*Cp + m*(panel+4) + panel*Cp) for the widest pattern.
  */

@@ -38,6 +38,9 @@ class MfbHybPattern(ctypes.Structure):
         ("edge_slot", _p), ("edge_noflow", _p), ("cell_edges", _p), ("gam_ptr", _p),
         ("gam_d", _p), ("gam_c", _p), ("dof_ptr", _p), ("dof_edge", _p), ("dof_coef", _p),
         ("p_val", _p), ("src_k", _p), ("src_c", _p), ("cell_f", _p), ("cell_q", _p),
+        ("z_n", _i), ("asm_ptr", _p), ("asm_row", _p), ("asm_dest", _p), ("asm_tptr", _p),
+        ("asm_cell", _p), ("asm_coef", _p), ("z_dest", _p), ("z_tptr", _p), ("z_cell", _p),
+        ("z_coef", _p),
     ]
 
 

@@ -40,39 +40,32 @@ __device__ __forceinline__ double gcoef(const MfbHybPattern &P, int gi, int d) {
     return 0.0;
 }
 
-// one thread assembles one window row r: lower band of H_II and border
-__device__ void assemble_row(const MfbHybPattern &P, const double *K, int r, double *W,
-                             double *Pb, int m, int ws, int Cp) {
-    const int w = P.w, nd = P.ndof;
-    double *wrow = W + (r % m) * ws;
-    double *prow = Pb + (r % m) * Cp;
-    for (int t = 0; t < ws; ++t) wrow[t] = 0.0;
-    for (int t = 0; t < Cp; ++t) prow[t] = 0.0;
-    const int e = P.row_edge[r];
-    for (int side = 0; side < 2; ++side) {
-        const int T = P.edge_cells[2 * e + side];
-        if (T < 0) continue;
-        const int a = P.edge_slot[2 * e + side];
-        const double k = K[T];
-        for (int b = 0; b < 4; ++b) {
-            const int e2 = P.cell_edges[4 * T + b];
-            const double h = k * P.Hhat[4 * a + b];
-            const int kind = P.edge_kind[e2], id = P.edge_idx[e2];
-            if (kind == 0) {
-                if (id <= r && r - id <= w) wrow[id - r + w] += h;
-            } else if (kind == 1) {
-                for (int t = P.gam_ptr[id]; t < P.gam_ptr[id + 1]; ++t)
-                    prow[P.gam_d[t]] += h * P.gam_c[t];
-            } else {
-                prow[nd] -= h * P.p_val[id];
-            }
-        }
-        if (P.has_src) prow[nd] += k * P.src_k[4 * T + a] + P.src_c[4 * T + a];
+__device__ __forceinline__ double term_sum(const int *tptr, const int *cell,
+                                           const double *coef, int e, const double *K) {
+    double v = 0.0;
+    for (int t = tptr[e]; t < tptr[e + 1]; ++t) {
+        const int c = cell[t];
+        v += c >= 0 ? coef[t] * K[c] : coef[t];
+    }
+    return v;
+}
+
+// scatter the term-table entries of rows [r0, r1) into the window (slots must
+// be zero); each entry has a unique destination, so threads never collide
+__device__ void assemble_entries(const MfbHybPattern &P, const double *K, int r0, int r1,
+                                 int t0, int nt, double *W, double *Pb, int m, int ws, int Cp) {
+    const int w = P.w;
+    const int e0 = P.asm_ptr[r0], e1 = P.asm_ptr[r1];
+    for (int e = e0 + t0; e < e1; e += nt) {
+        const int r = P.asm_row[e], d = P.asm_dest[e];
+        const double v = term_sum(P.asm_tptr, P.asm_cell, P.asm_coef, e, K);
+        if (d <= w) W[(r % m) * ws + d] = v;
+        else Pb[(r % m) * Cp + (d - w - 1)] = v;
     }
 }
 
-template <int BP>
-__global__ void __launch_bounds__(HYB_NT)
+template <int BP, int RL>
+__global__ void __launch_bounds__(HYB_NT, (BP == 16 ? 2 : 1))
 condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ sys_pat,
                 const double *__restrict__ Kbuf, const long long *__restrict__ sys_koff,
                 double *__restrict__ blocks, const long long *__restrict__ sys_boff,
@@ -96,31 +89,16 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     const int g = lane >> 2, q4 = lane & 3;
     if (tid == 0) s_bad = 0;
     for (int t = tid; t < Cp * Cp; t += HYB_NT) S[t] = 0.0;
+    // initial border block Z and the first window rows (term tables, thread per entry)
+    for (int t = tid; t < m * ws; t += HYB_NT) W[t] = 0.0;
+    for (int t = tid; t < m * Cp; t += HYB_NT) Pb[t] = 0.0;
     __syncthreads();
-    // initial Schur block Z (thread per entry; sums in a fixed order)
-    for (int t = tid; t < nd * (nd + 1); t += HYB_NT) {
-        const int d1 = t / (nd + 1), d2 = t % (nd + 1);
-        double z = 0.0;
-        for (int u = P.dof_ptr[d1]; u < P.dof_ptr[d1 + 1]; ++u) {
-            const int e1 = P.dof_edge[u];
-            const double c1 = P.dof_coef[u];
-            const int T = P.edge_cells[2 * e1], a = P.edge_slot[2 * e1];
-            const double k = K[T];
-            for (int b = 0; b < 4; ++b) {
-                const int e2 = P.cell_edges[4 * T + b];
-                const int kind = P.edge_kind[e2], id = P.edge_idx[e2];
-                const double h = k * P.Hhat[4 * a + b];
-                if (d2 < nd) {
-                    if (kind == 1) z += c1 * h * gcoef(P, id, d2);
-                } else if (kind == 2) {
-                    z -= c1 * h * P.p_val[id];
-                }
-            }
-            if (d2 == nd && P.has_src) z += c1 * (k * P.src_k[4 * T + a] + P.src_c[4 * T + a]);
-        }
-        S[d1 * Cp + d2] = z;
+    for (int e = tid; e < P.z_n; e += HYB_NT) {
+        const int d1 = P.z_dest[e] / (nd + 1), d2 = P.z_dest[e] % (nd + 1);
+        S[d1 * Cp + d2] = term_sum(P.z_tptr, P.z_cell, P.z_coef, e, K);
     }
-    for (int r = tid; r < min(n, m); r += HYB_NT) assemble_row(P, K, r, W, Pb, m, ws, Cp);
+    assemble_entries(P, K, 0, min(n, m), tid, HYB_NT, W, Pb, m, ws, Cp);
+
     __syncthreads();
 
     const int n_pan = (n + BP - 1) / BP;
@@ -142,34 +120,77 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
         }
         __syncthreads();
         if (wid == 0) {
-            // panel Cholesky + forward substitution of the border rows (one warp)
-            for (int p = 0; p < nb; ++p) {
-                double d = Lb[p * LS + p];
-                if (!(d > 0.0)) {
-                    if (lane == 0) { s_bad = 1; info[s] = -(k + p + 1); }
-                    break;
+            // panel Cholesky (left-looking, register resident) + forward
+            // substitution of the border rows, one warp: lane l owns panel
+            // rows l, l+32, ... and border columns l, l+32
+            double a[RL][BP];                           // rows per lane: nrow <= 32*RL
+#pragma unroll
+            for (int r = 0; r < RL; ++r)
+#pragma unroll
+                for (int q = 0; q < BP; ++q) {
+                    const int i = lane + 32 * r;
+                    a[r][q] = i < nrow ? Lb[i * LS + q] : 0.0;
                 }
-                d = sqrt(d);
-                __syncwarp();
-                for (int i = p + 1 + lane; i < nrow; i += 32) Lb[i * LS + p] /= d;
-                for (int c = lane; c < Cp; c += 32) Yb[p * Cp + c] /= d;
-                if (lane == 0) Lb[p * LS + p] = d;
-                __syncwarp();
-                for (int i = p + 1 + lane; i < nrow; i += 32) {
-                    const double lip = Lb[i * LS + p];
-                    const int qe = min(nb - 1, i);
-                    for (int q = p + 1; q <= qe; ++q) Lb[i * LS + q] -= lip * Lb[q * LS + p];
+            bool bad = false;
+#pragma unroll
+            for (int p = 0; p < BP; ++p) {
+                if (p >= nb) break;
+                // broadcast row p of L (columns < p) from its owner lane
+                double lp[BP];
+                const int own = p & 31, slot = p >> 5;
+#pragma unroll
+                for (int q = 0; q < BP; ++q) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int r = 0; r < RL; ++r)
+                        if (r == slot) v = a[r][q];
+                    lp[q] = q < p ? __shfl_sync(0xffffffffu, v, own) : 0.0;
+                }
+                double vp = 0.0;
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int i = lane + 32 * r;
+                    double v = a[r][p];
+#pragma unroll
+                    for (int q = 0; q < BP; ++q) v -= a[r][q] * lp[q];
+                    a[r][p] = v;
+                    if (i == p) vp = v;
+                }
+                const double dd = __shfl_sync(0xffffffffu, vp, own);
+                if (!(dd > 0.0)) { bad = true; break; }
+                const double d = sqrt(dd);
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int i = lane + 32 * r;
+                    if (i > p) a[r][p] /= d;
+                    else if (i == p) a[r][p] = d;
                 }
                 for (int c = lane; c < Cp; c += 32) {
-                    const double yp = Yb[p * Cp + c];
-                    for (int q = p + 1; q < nb; ++q) Yb[q * Cp + c] -= Lb[q * LS + p] * yp;
+                    double t0 = Yb[p * Cp + c];
+                    for (int q = 0; q < p; ++q) t0 -= lp[q] * Yb[q * Cp + c];
+                    Yb[p * Cp + c] = t0 / d;
                 }
-                __syncwarp();
+            }
+            if (bad) {
+                if (lane == 0) { s_bad = 1; info[s] = -(k + 1); }
+            } else {
+#pragma unroll
+                for (int r = 0; r < RL; ++r)
+#pragma unroll
+                    for (int q = 0; q < BP; ++q) {
+                        const int i = lane + 32 * r;
+                        if (i < nrow) Lb[i * LS + q] = (q <= i) ? a[r][q] : 0.0;
+                    }
             }
         } else {
-            // rows entering the window take the freed slots of this panel
-            for (int r = k + m + (tid - 32); r < min(n, k + m + BP); r += HYB_NT - 32)
-                assemble_row(P, K, r, W, Pb, m, ws, Cp);
+            // rows entering the window take the freed slots of this panel:
+            // zero them, sync the assembly warps, scatter the term-table entries
+            const int r0 = k + m, r1 = min(n, k + m + BP);
+            const int at = tid - 32, an = HYB_NT - 32;
+            for (int t = at; t < (r1 - r0) * ws; t += an) W[((r0 + t / ws) % m) * ws + t % ws] = 0.0;
+            for (int t = at; t < (r1 - r0) * Cp; t += an) Pb[((r0 + t / Cp) % m) * Cp + t % Cp] = 0.0;
+            asm volatile("bar.sync 1, %0;" ::"r"(HYB_NT - 32));
+            if (r1 > r0) assemble_entries(P, K, r0, r1, at, an, W, Pb, m, ws, Cp);
         }
         __syncthreads();
         if (s_bad) return;
@@ -371,6 +392,22 @@ recover_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ s
 
 }  // namespace
 
+template <int BP, int RL>
+static int launch_condense(int n_sys, size_t smem, cudaStream_t st, const MfbHybPattern *pats,
+                           const int *sys_pat, const double *Kbuf, const long long *sys_koff,
+                           double *blocks, const long long *sys_boff, double *hbar,
+                           const long long *sys_hoff, double *Lstore, const long long *sys_loff,
+                           int *info) {
+    if (cudaFuncSetAttribute(condense_kernel<BP, RL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return MFB_ERR_SMEM;
+    condense_kernel<BP, RL><<<n_sys, HYB_NT, smem, st>>>(pats, sys_pat, Kbuf, sys_koff, blocks,
+                                                         sys_boff, hbar, sys_hoff, Lstore,
+                                                         sys_loff, info);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
 extern "C" int mfb_darcy_condense(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
                                   const double *Kbuf, const long long *sys_koff, double *blocks,
                                   const long long *sys_boff, double *hbar,
@@ -379,23 +416,18 @@ extern "C" int mfb_darcy_condense(const MfbHybPattern *pats, int n_sys, const in
                                   int smem_bytes, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
     cudaStream_t st = mfb_stream(stream);
-    if (panel == 16) {
-        if (cudaFuncSetAttribute(condense_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes) != cudaSuccess)
-            return MFB_ERR_SMEM;
-        condense_kernel<16><<<n_sys, HYB_NT, smem_bytes, st>>>(
-            pats, sys_pat, Kbuf, sys_koff, blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
-    } else if (panel == 8) {
-        if (cudaFuncSetAttribute(condense_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes) != cudaSuccess)
-            return MFB_ERR_SMEM;
-        condense_kernel<8><<<n_sys, HYB_NT, smem_bytes, st>>>(
-            pats, sys_pat, Kbuf, sys_koff, blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
-    } else {
-        return MFB_ERR_ARG;
-    }
-    MFB_CHECK_LAUNCH();
-    return MFB_OK;
+    // panel = BP | (rows-per-lane << 8): the panel warp holds nrow <= 32*RL rows
+    const int bp = panel & 255, rl = panel >> 8;
+#define MFB_CONDENSE(B, R)                                                                    \
+    if (bp == B && rl <= R)                                                                   \
+        return launch_condense<B, R>(n_sys, smem_bytes, st, pats, sys_pat, Kbuf, sys_koff,    \
+                                     blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
+    MFB_CONDENSE(16, 2)
+    MFB_CONDENSE(16, 3)
+    MFB_CONDENSE(8, 5)
+    MFB_CONDENSE(8, 8)
+#undef MFB_CONDENSE
+    return MFB_ERR_ARG;
 }
 
 extern "C" int mfb_darcy_backsolve(const MfbHybPattern *pats, int n_sys, const int *sys_pat,

@@ -327,3 +327,82 @@ def recover_fields(hp, K, X):
         out[ne + nc + 2 * c + 1] = 0.5 * (u[2] + u[3])
         out[ne + 3 * nc + c] = p
     return out[:, nd], -out[:, :nd]
+
+
+def assembly_tables(hp):
+    """Term tables the device uses to assemble window rows and the border block.
+
+    Row table (CSR over unknown rows r): entries with a destination
+    `dest` = c - r + w for H_II[r][c] (c <= r, inside the band) or
+    w + 1 + d for border column d (d = ndof is the bar column); each entry
+    is a short list of terms coef * K[cell] (cell >= 0) or coef (cell = -1),
+    summed in list order. Z table: entries d1 * (ndof+1) + d2 of the initial
+    border block with terms of the same form.
+    """
+    nd = hp.ndof
+    w = hp.w
+    rows = {}          # r -> {dest: [(cell, coef)]}
+    zent = {}          # (d1, d2) -> [(cell, coef)]
+
+    def gvec(e):
+        gi = hp.edge_idx[e]
+        sl = slice(hp.gam_ptr[gi], hp.gam_ptr[gi + 1])
+        return list(zip(hp.gam_d[sl].tolist(), hp.gam_c[sl].tolist()))
+
+    for c in range(len(hp.cell_q)):
+        E = hp.cell_edges[c]
+        for a in range(4):
+            ea, ka = int(E[a]), hp.edge_kind[E[a]]
+            if ka == KIND_I:
+                r = int(hp.edge_idx[ea])
+                ent = rows.setdefault(r, {})
+                for b in range(4):
+                    eb, kb = int(E[b]), hp.edge_kind[E[b]]
+                    h = float(hp.Hhat[a, b])
+                    if kb == KIND_I:
+                        col = int(hp.edge_idx[eb])
+                        if col <= r:
+                            ent.setdefault(col - r + w, []).append((c, h))
+                    elif kb == KIND_GAMMA:
+                        for d, gc in gvec(eb):
+                            ent.setdefault(w + 1 + d, []).append((c, h * gc))
+                    else:
+                        ent.setdefault(w + 1 + nd, []).append(
+                            (c, -h * float(hp.p_val[hp.edge_idx[eb]])))
+                if hp.has_src:
+                    ent.setdefault(w + 1 + nd, []).append((c, float(hp.src_k[c, a])))
+                    ent[w + 1 + nd].append((-1, float(hp.src_c[c, a])))
+            elif ka == KIND_GAMMA:
+                for d1, g1 in gvec(ea):
+                    for b in range(4):
+                        eb, kb = int(E[b]), hp.edge_kind[E[b]]
+                        h = float(hp.Hhat[a, b])
+                        if kb == KIND_GAMMA:
+                            for d2, g2 in gvec(eb):
+                                zent.setdefault((d1, d2), []).append((c, g1 * h * g2))
+                        elif kb == KIND_P:
+                            zent.setdefault((d1, nd), []).append(
+                                (c, -g1 * h * float(hp.p_val[hp.edge_idx[eb]])))
+                    if hp.has_src:
+                        zent.setdefault((d1, nd), []).append((c, g1 * float(hp.src_k[c, a])))
+                        zent[(d1, nd)].append((-1, g1 * float(hp.src_c[c, a])))
+
+    ptr, dest, tptr, tcell, tcoef = [0], [], [0], [], []
+    for r in range(hp.n):
+        for dd in sorted(rows.get(r, {})):
+            dest.append(dd)
+            for cell, coef in rows[r][dd]:
+                tcell.append(cell)
+                tcoef.append(coef)
+            tptr.append(len(tcell))
+        ptr.append(len(dest))
+    zdest, ztptr, zcell, zcoef = [], [0], [], []
+    for (d1, d2) in sorted(zent):
+        zdest.append(d1 * (nd + 1) + d2)
+        for cell, coef in zent[(d1, d2)]:
+            zcell.append(cell)
+            zcoef.append(coef)
+        ztptr.append(len(zcell))
+    return {k: np.asarray(v) for k, v in dict(
+        asm_ptr=ptr, asm_dest=dest, asm_tptr=tptr, asm_cell=tcell, asm_coef=tcoef,
+        z_dest=zdest, z_tptr=ztptr, z_cell=zcell, z_coef=zcoef).items()}

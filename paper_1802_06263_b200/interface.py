@@ -219,7 +219,8 @@ class _S3Static:
                 hxoff = np.concatenate([[0], np.cumsum([l[4] for l in lays])])
                 w = sub(grp)
                 w["info"] = torch.zeros(len(grp), dtype=i32, device="cuda")
-                w.update(panel=panel, smem_c=max(l[1] for l in lays),
+                wmax_ = max(plan.hyb[systems[i][0]].w for i in grp)
+                w.update(panel=panel, rl=-(-(wmax_ + panel) // 32), smem_c=max(l[1] for l in lays),
                          smem_b=max(l[2] for l in lays), loff=_dev(loff[:-1], i64),
                          xoff=_dev(hxoff[:-1], i64),
                          flops=sum(plan.hyb[systems[i][0]].algorithmic_flops for i in grp),
@@ -356,7 +357,7 @@ class S3Engine:
                 _ptr(plan.hyb_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
                 _ptr(st.blocks), _ptr(w["boff"]), _ptr(st.hbar), _ptr(w["hoff"]),
                 _ptr(st.Lstore) if keep else None, _ptr(w["loff"]), _ptr(w["info"]),
-                w["panel"], w["smem_c"], self.sp), "mfb_darcy_condense")
+                w["panel"] | (w["rl"] << 8), w["smem_c"], self.sp), "mfb_darcy_condense")
             if self.timing:
                 self.solve_events.append(("hybrid", e0, self._ev(), w["flops"],
                                           w["survey_flops"]))

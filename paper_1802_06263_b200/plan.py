@@ -13,7 +13,7 @@ import numpy as np
 
 from . import _lib
 from .discretization import darcy_pattern, stokes_pattern
-from .hybrid import hybrid_pattern
+from .hybrid import assembly_tables, hybrid_pattern
 
 
 def _dev(a, dtype):
@@ -131,12 +131,21 @@ class DevicePlan:
                 "src_c": _dev(h.src_c.ravel(), f64), "cell_f": _dev(h.cell_f.ravel(), f64),
                 "cell_q": _dev(h.cell_q, f64),
             }
+            T = assembly_tables(h)
+            asm_row = np.repeat(np.arange(h.n), np.diff(T["asm_ptr"]))
+            arrs.update({
+                "asm_ptr": _dev(T["asm_ptr"], i32), "asm_row": _dev(asm_row, i32),
+                "asm_dest": _dev(T["asm_dest"], i32), "asm_tptr": _dev(T["asm_tptr"], i32),
+                "asm_cell": _dev(T["asm_cell"], i32), "asm_coef": _dev(T["asm_coef"], f64),
+                "z_dest": _dev(T["z_dest"], i32), "z_tptr": _dev(T["z_tptr"], i32),
+                "z_cell": _dev(T["z_cell"], i32), "z_coef": _dev(T["z_coef"], f64)})
             self._keep_h.append(arrs)
             st = structs[s]
             ws = h.layout_for(self.hyb_panel[s])[0]
             st.n, st.w, st.ws, st.ndof, st.nfield = h.n, h.w, ws, h.ndof, h.nfield
             st.n_edges, st.n_cells = len(h.edge_kind), len(h.cell_q)
             st.has_src = int(h.has_src)
+            st.z_n = int(len(T["z_dest"]))
             st.hx, st.hy, st.nu = h.hx, h.hy, h.nu
             st.s2 = h.hx * h.hx + h.hy * h.hy
             for i, v in enumerate(h.Hhat.ravel()):
