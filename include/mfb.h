@@ -211,13 +211,11 @@ int mfb_lambda_moments(int n_lambda, int n_real, const double *lam,
 
 /*
  * Darcy flux basis by static condensation of the SPD hybridised system in
- * shared memory (band Cholesky, panel width `panel` = 8 or 16, trailing
+ * shared memory (band Cholesky, panel width `panel` = 8, trailing
  * updates on DMMA): per system B (column-major into blocks + sys_boff) and
  * the bar jump h. If Lstore != NULL the factor panels are kept for
  * mfb_darcy_backsolve (layout: per panel m*(panel+4) L doubles then
  * panel*Cp rhs doubles, m = w + panel, Cp = ndof+1 rounded up to 8).
- * `panel` = width | (rows_per_lane << 8) with rows_per_lane >=
- * ceil((w + width) / 32) (the panel warp keeps its rows in registers).
  * info[s] = -(pivot index + 1) if a pivot is not positive. smem_bytes:
  * 8 * (m*ws + m*Cp + Cp*Cp + m*(panel+4) + panel*Cp) for the widest pattern.
  */
@@ -243,6 +241,10 @@ int mfb_darcy_recover(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
 /* Self test of the FP64 tensor-core (DMMA m8n8k4) fragment layout the
  * elimination kernels rely on; writes max |error| to *err (device). */
 int mfb_selftest_dmma(double *err, void *stream);
+
+/* Phase cycle counters of the condense kernel (builds with -DMFB_PROFILE
+ * only; returns 1 otherwise). Host pointer, 16 counters. */
+int mfb_debug_prof(unsigned long long *out);
 
 #ifdef __cplusplus
 }

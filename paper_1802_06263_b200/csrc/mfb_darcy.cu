@@ -21,6 +21,21 @@
 // form X = H_II^-1 V and mfb_darcy_recover the cell fields.
 #include "mfb_common.cuh"
 
+#ifdef MFB_PROFILE
+__device__ unsigned long long g_prof[16];
+#define PROF_MARK(i)                                                              \
+    do {                                                                          \
+        if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) {         \
+            long long _c = clock64();                                             \
+            int _slot = (i) + (threadIdx.x == 32 ? 8 : 0);                        \
+            if ((i) > 0) atomicAdd(&g_prof[_slot], (unsigned long long)(_c - s_t0[threadIdx.x >> 5])); \
+            s_t0[threadIdx.x >> 5] = _c;                                          \
+        }                                                                         \
+    } while (0)
+#else
+#define PROF_MARK(i) do {} while (0)
+#endif
+
 namespace {
 
 constexpr int HYB_NT = 256;
@@ -64,8 +79,8 @@ __device__ void assemble_entries(const MfbHybPattern &P, const double *K, int r0
     }
 }
 
-template <int BP, int RL>
-__global__ void __launch_bounds__(HYB_NT, (BP == 16 ? 2 : 1))
+template <int BP>
+__global__ void __launch_bounds__(HYB_NT, 2)
 condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ sys_pat,
                 const double *__restrict__ Kbuf, const long long *__restrict__ sys_koff,
                 double *__restrict__ blocks, const long long *__restrict__ sys_boff,
@@ -75,6 +90,10 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     constexpr int LS = BP + 4;
     extern __shared__ double sm[];
     __shared__ int s_bad;
+    __shared__ double s_inv[8];
+#ifdef MFB_PROFILE
+    __shared__ long long s_t0[8];
+#endif
     const int s = blockIdx.x;
     const MfbHybPattern &P = pats[sys_pat[s]];
     const double *K = Kbuf + sys_koff[s];
@@ -104,6 +123,7 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     const int n_pan = (n + BP - 1) / BP;
     const long long pstride = (long long)m * LS + (long long)BP * Cp;
     for (int pi = 0; pi < n_pan; ++pi) {
+        PROF_MARK(0);
         const int k = pi * BP;
         const int nb = min(BP, n - k);
         const int rend = min(n, k + BP + w);
@@ -119,68 +139,69 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
             Yb[t] = p < nb ? Pb[((k + p) % m) * Cp + c] : 0.0;
         }
         __syncthreads();
-        if (wid == 0) {
-            // panel Cholesky (left-looking, register resident) + forward
-            // substitution of the border rows, one warp: lane l owns panel
-            // rows l, l+32, ... and border columns l, l+32
-            double a[RL][BP];                           // rows per lane: nrow <= 32*RL
+        PROF_MARK(1);
+        if (tid == 0) {
+            // 8x8 diagonal block: Cholesky in registers (missing pivots of a
+            // short last panel are identity rows)
+            double a[8][8];
 #pragma unroll
-            for (int r = 0; r < RL; ++r)
+            for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int q = 0; q < BP; ++q) {
-                    const int i = lane + 32 * r;
-                    a[r][q] = i < nrow ? Lb[i * LS + q] : 0.0;
-                }
-            bool bad = false;
+                for (int q = 0; q < 8; ++q)
+                    a[i][q] = (i < nb && q < nb) ? Lb[i * LS + q] : (i == q ? 1.0 : 0.0);
+            bool ok = true;
 #pragma unroll
-            for (int p = 0; p < BP; ++p) {
-                if (p >= nb) break;
-                // broadcast row p of L (columns < p) from its owner lane
-                double lp[BP];
-                const int own = p & 31, slot = p >> 5;
+            for (int p = 0; p < 8; ++p) {
+                double v = a[p][p];
 #pragma unroll
-                for (int q = 0; q < BP; ++q) {
-                    double v = 0.0;
+                for (int q = 0; q < p; ++q) v -= a[p][q] * a[p][q];
+                ok = ok && (v > 0.0);
+                const double d = sqrt(v);
+                a[p][p] = d;
+                const double inv = 1.0 / d;
 #pragma unroll
-                    for (int r = 0; r < RL; ++r)
-                        if (r == slot) v = a[r][q];
-                    lp[q] = q < p ? __shfl_sync(0xffffffffu, v, own) : 0.0;
-                }
-                double vp = 0.0;
+                for (int i = p + 1; i < 8; ++i) {
+                    double x = a[i][p];
 #pragma unroll
-                for (int r = 0; r < RL; ++r) {
-                    const int i = lane + 32 * r;
-                    double v = a[r][p];
-#pragma unroll
-                    for (int q = 0; q < BP; ++q) v -= a[r][q] * lp[q];
-                    a[r][p] = v;
-                    if (i == p) vp = v;
-                }
-                const double dd = __shfl_sync(0xffffffffu, vp, own);
-                if (!(dd > 0.0)) { bad = true; break; }
-                const double d = sqrt(dd);
-#pragma unroll
-                for (int r = 0; r < RL; ++r) {
-                    const int i = lane + 32 * r;
-                    if (i > p) a[r][p] /= d;
-                    else if (i == p) a[r][p] = d;
-                }
-                for (int c = lane; c < Cp; c += 32) {
-                    double t0 = Yb[p * Cp + c];
-                    for (int q = 0; q < p; ++q) t0 -= lp[q] * Yb[q * Cp + c];
-                    Yb[p * Cp + c] = t0 / d;
+                    for (int q = 0; q < p; ++q) x -= a[i][q] * a[p][q];
+                    a[i][p] = x * inv;
                 }
             }
-            if (bad) {
-                if (lane == 0) { s_bad = 1; info[s] = -(k + 1); }
-            } else {
+            if (!ok) { s_bad = 1; info[s] = -(k + 1); }
 #pragma unroll
-                for (int r = 0; r < RL; ++r)
+            for (int i = 0; i < 8; ++i) {
 #pragma unroll
-                    for (int q = 0; q < BP; ++q) {
-                        const int i = lane + 32 * r;
-                        if (i < nrow) Lb[i * LS + q] = (q <= i) ? a[r][q] : 0.0;
-                    }
+                for (int q = 0; q < 8; ++q)
+                    if (i < nb) Lb[i * LS + q] = (q <= i && q < nb) ? a[i][q] : 0.0;
+                s_inv[i] = 1.0 / a[i][i];
+            }
+        }
+        if (wid == 0) {
+            __syncwarp();
+            // L21 = A21 L11^-T (lane per row), Yb = L11^-1 Yb (lane per column)
+            for (int i = nb + lane; i < nrow; i += 32) {
+                double x[BP];
+#pragma unroll
+                for (int q = 0; q < BP; ++q) {
+                    double v = q < nb ? Lb[i * LS + q] : 0.0;
+#pragma unroll
+                    for (int qq = 0; qq < q; ++qq) v -= x[qq] * Lb[q * LS + qq];
+                    x[q] = q < nb ? v * s_inv[q] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < BP; ++q) Lb[i * LS + q] = x[q];
+            }
+            for (int c = lane; c < Cp; c += 32) {
+                double y[BP];
+#pragma unroll
+                for (int q = 0; q < BP; ++q) {
+                    double v = q < nb ? Yb[q * Cp + c] : 0.0;
+#pragma unroll
+                    for (int qq = 0; qq < q; ++qq) v -= Lb[q * LS + qq] * y[qq];
+                    y[q] = q < nb ? v * s_inv[q] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < BP; ++q) Yb[q * Cp + c] = y[q];
             }
         } else {
             // rows entering the window take the freed slots of this panel:
@@ -192,8 +213,11 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
             asm volatile("bar.sync 1, %0;" ::"r"(HYB_NT - 32));
             if (r1 > r0) assemble_entries(P, K, r0, r1, at, an, W, Pb, m, ws, Cp);
         }
+        PROF_MARK(5);
         __syncthreads();
+        PROF_MARK(2);
         if (s_bad) return;
+        PROF_MARK(3);
         if (Lstore) {
             double *dst = Lstore + sys_loff[s] + (long long)pi * pstride;
             for (int t = tid; t < nrow * LS; t += HYB_NT) dst[t] = Lb[t];
@@ -260,6 +284,7 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
             }
         }
         __syncthreads();
+        PROF_MARK(4);
     }
     for (int t = tid; t < nd * nd; t += HYB_NT) {
         const int r = t % nd, c = t / nd;
@@ -392,22 +417,6 @@ recover_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ s
 
 }  // namespace
 
-template <int BP, int RL>
-static int launch_condense(int n_sys, size_t smem, cudaStream_t st, const MfbHybPattern *pats,
-                           const int *sys_pat, const double *Kbuf, const long long *sys_koff,
-                           double *blocks, const long long *sys_boff, double *hbar,
-                           const long long *sys_hoff, double *Lstore, const long long *sys_loff,
-                           int *info) {
-    if (cudaFuncSetAttribute(condense_kernel<BP, RL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return MFB_ERR_SMEM;
-    condense_kernel<BP, RL><<<n_sys, HYB_NT, smem, st>>>(pats, sys_pat, Kbuf, sys_koff, blocks,
-                                                         sys_boff, hbar, sys_hoff, Lstore,
-                                                         sys_loff, info);
-    MFB_CHECK_LAUNCH();
-    return MFB_OK;
-}
-
 extern "C" int mfb_darcy_condense(const MfbHybPattern *pats, int n_sys, const int *sys_pat,
                                   const double *Kbuf, const long long *sys_koff, double *blocks,
                                   const long long *sys_boff, double *hbar,
@@ -415,19 +424,23 @@ extern "C" int mfb_darcy_condense(const MfbHybPattern *pats, int n_sys, const in
                                   const long long *sys_loff, int *info, int panel,
                                   int smem_bytes, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
-    cudaStream_t st = mfb_stream(stream);
-    // panel = BP | (rows-per-lane << 8): the panel warp holds nrow <= 32*RL rows
-    const int bp = panel & 255, rl = panel >> 8;
-#define MFB_CONDENSE(B, R)                                                                    \
-    if (bp == B && rl <= R)                                                                   \
-        return launch_condense<B, R>(n_sys, smem_bytes, st, pats, sys_pat, Kbuf, sys_koff,    \
-                                     blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
-    MFB_CONDENSE(16, 2)
-    MFB_CONDENSE(16, 3)
-    MFB_CONDENSE(8, 5)
-    MFB_CONDENSE(8, 8)
-#undef MFB_CONDENSE
-    return MFB_ERR_ARG;
+    if ((panel & 255) != 8) return MFB_ERR_ARG;
+    if (cudaFuncSetAttribute(condense_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_bytes) != cudaSuccess)
+        return MFB_ERR_SMEM;
+    condense_kernel<8><<<n_sys, HYB_NT, smem_bytes, mfb_stream(stream)>>>(
+        pats, sys_pat, Kbuf, sys_koff, blocks, sys_boff, hbar, sys_hoff, Lstore, sys_loff, info);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_debug_prof(unsigned long long *out) {
+#ifdef MFB_PROFILE
+    return cudaMemcpyFromSymbol(out, g_prof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 2;
+#else
+    (void)out;
+    return 1;
+#endif
 }
 
 extern "C" int mfb_darcy_backsolve(const MfbHybPattern *pats, int n_sys, const int *sys_pat,

@@ -106,7 +106,7 @@ class HybPattern:
         return ws, smem_c, smem_b, l_doubles, self.n * Cp
 
     def choose_panel(self):
-        for panel in (16, 8):
+        for panel in (8,):
             if self.layout_for(panel)[1] <= SMEM_LIMIT:
                 return panel
         raise ValueError(f"Darcy subdomain {self.sid}: band {self.w} too wide for shared memory")
