@@ -19,6 +19,20 @@
 // every update element costs one global read-modify-write.
 #include "mfb_common.cuh"
 
+#ifdef MFB_PROFILE
+__device__ unsigned long long g_bprof[16];
+#define BPROF(i)                                                                  \
+    do {                                                                          \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
+            long long _c = clock64();                                             \
+            if ((i) > 0) atomicAdd(&g_bprof[(i)], (unsigned long long)(_c - s_bt0)); \
+            s_bt0 = _c;                                                           \
+        }                                                                         \
+    } while (0)
+#else
+#define BPROF(i) do {} while (0)
+#endif
+
 namespace {
 
 constexpr int MAX_NB = 8;
@@ -48,14 +62,17 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     extern __shared__ double smem[];
     __shared__ double red_v[NW];
     __shared__ int red_i[NW];
-    __shared__ int s_piv;
     __shared__ int s_ipiv[NB];
     __shared__ int s_low[NB];
     __shared__ int s_nlow;
     __shared__ double s_u11[NB * NB];
+    __shared__ double s_linv[NB * NB];
     __shared__ double s_bord[MAX_NB * MAX_NCY];
     __shared__ double s_z[MAX_NB * MAX_NCY];
     __shared__ int s_flag;
+#ifdef MFB_PROFILE
+    __shared__ long long s_bt0;
+#endif
 
     const int s = blockIdx.x;
     const MfbPattern P = pats[sys_pat[s]];
@@ -68,7 +85,8 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     double *Y = AB + (long long)ldab * n;
     double *Pnl = smem;                          // (kl + NB) x PST   panel L | U11
     double *U12s = Pnl + (kl + NB) * PST;        // NB x UST          U12 of the panel
-    double *Ytop = U12s + NB * UST;              // NB x ncy          rhs rows of the panel
+    double *Tmp = U12s + NB * UST;               // NB x UST          staged A12
+    double *Ytop = Tmp + NB * UST;               // NB x ncy          rhs rows of the panel
     int *s_perm = reinterpret_cast<int *>(Ytop + NB * ncy);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
@@ -101,8 +119,11 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     }
     __syncthreads();
 
+    if (tid == 0) s_flag = 0;
+    __syncthreads();
     // ---- 2. blocked banded LU with partial pivoting (gbtrf) --------------
     for (int j0 = 0; j0 < n; j0 += NB) {
+        BPROF(0);
         const int pnb = min(NB, n - j0);
         const int r1 = min(n, j0 + pnb + kl);
         const int nr = r1 - j0;
@@ -117,50 +138,59 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                                    ? AB[bidx(r, col, kl, ku, ldab)] : 0.0;
         }
         __syncthreads();
-        for (int c = 0; c < pnb; ++c) {
+        BPROF(1);
+        if (tid < 128) {
+            // panel LU with partial pivoting on 4 warps (named barrier 2); the
+            // pivot candidate of column c+1 is found while column c is applied
+            const int pw = tid >> 5;
             double best = -1.0;
-            int bi = c;
-            for (int i = c + tid; i < nr; i += NT) {
-                const double a = fabs(Pnl[i * PST + c]);
+            int bi = 0;
+            for (int i = tid; i < nr; i += 128) {
+                const double a = fabs(Pnl[i * PST]);
                 if (a > best) { best = a; bi = i; }
             }
+            for (int c = 0; c < pnb; ++c) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_down_sync(0xffffffffu, best, o);
-                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-            }
-            if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
-            __syncthreads();
-            if (tid == 0) {
-                double bv = red_v[0];
-                int bx = red_i[0];
-                for (int w = 1; w < NW; ++w)
-                    if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bx)) { bv = red_v[w]; bx = red_i[w]; }
-                s_piv = bx;
-                s_ipiv[c] = bx;
-            }
-            __syncthreads();
-            const int p = s_piv;
-            if (Pnl[p * PST + c] == 0.0) {
-                if (tid == 0) info[s] = j0 + c + 1;
-                return;
-            }
-            if (p != c)
-                for (int cc = tid; cc < NB; cc += NT) {
-                    const double t0 = Pnl[c * PST + cc];
-                    Pnl[c * PST + cc] = Pnl[p * PST + cc];
-                    Pnl[p * PST + cc] = t0;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_down_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
                 }
-            __syncthreads();
-            const double piv = Pnl[c * PST + c];
-            for (int i = c + 1 + tid; i < nr; i += NT) {
-                const double l = Pnl[i * PST + c] / piv;
-                Pnl[i * PST + c] = l;
-                for (int cc = c + 1; cc < pnb; ++cc) Pnl[i * PST + cc] -= l * Pnl[c * PST + cc];
+                if (lane == 0) { red_v[pw] = best; red_i[pw] = bi; }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                double bv = red_v[0];
+                int p = red_i[0];
+#pragma unroll
+                for (int w = 1; w < 4; ++w)
+                    if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < p)) { bv = red_v[w]; p = red_i[w]; }
+                if (!(bv > 0.0)) {
+                    if (tid == 0) { info[s] = j0 + c + 1; s_flag = -1; }
+                    break;
+                }
+                if (tid == 0) s_ipiv[c] = p;
+                if (p != c && tid < NB) {
+                    const double t0 = Pnl[c * PST + tid];
+                    Pnl[c * PST + tid] = Pnl[p * PST + tid];
+                    Pnl[p * PST + tid] = t0;
+                }
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                const double inv = 1.0 / Pnl[c * PST + c];
+                best = -1.0;
+                bi = c + 1;
+                for (int i = c + 1 + tid; i < nr; i += 128) {
+                    const double l = Pnl[i * PST + c] * inv;
+                    Pnl[i * PST + c] = l;
+                    for (int cc = c + 1; cc < pnb; ++cc) Pnl[i * PST + cc] -= l * Pnl[c * PST + cc];
+                    if (c + 1 < pnb) {
+                        const double a = fabs(Pnl[i * PST + c + 1]);
+                        if (a > best) { best = a; bi = i; }
+                    }
+                }
             }
-            __syncthreads();
         }
+        __syncthreads();
+        BPROF(2);
+        if (s_flag < 0) return;
         // net row permutation of the panel's swaps
         if (tid == 0) {
             for (int i = 0; i < nr; ++i) s_perm[i] = i;
@@ -179,53 +209,69 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             s_nlow = nl;
         }
         __syncthreads();
+        BPROF(3);
         for (int t = tid; t < nr * pnb; t += NT) {
             const int i = t % nr, c = t / nr;
             const int r = j0 + i, col = j0 + c;
             if (r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = Pnl[i * PST + c];
         }
-        // phase A: trailing columns -- permute, U12 = L11^-1 A12 (thread per column)
+        // phase A: stage the permuted top rows of every trailing column (Tmp)
+        // and the moved lower rows (U12s used as staging); all reads first
         const int nlow = s_nlow;
         const int ncpad = (nc + 7) & ~7;
-        for (int t = tid; t < ncpad; t += NT) {
-            const int col = c0 + t;
-            double u[NB], low[NB];
-            if (t < nc) {
+        for (int t = tid; t < NB * ncpad; t += NT) {
+            const int q = t / ncpad, cc = t % ncpad, col = c0 + cc;
+            const int src = j0 + (q < pnb ? s_perm[q] : 0);
+            const bool vt = q < pnb && cc < nc && col - src <= kl + ku && src - col <= kl;
+            const int srl = j0 + (q < nlow ? s_perm[s_low[q]] : 0);
+            const bool vl = q < nlow && cc < nc && col - srl <= kl + ku && srl - col <= kl;
+            const double x = __ldcg(AB + (vt ? bidx(src, col, kl, ku, ldab) : 0));
+            const double y = __ldcg(AB + (vl ? bidx(srl, col, kl, ku, ldab) : 0));
+            Tmp[q * UST + cc] = vt ? x : 0.0;
+            U12s[q * UST + cc] = vl ? y : 0.0;
+        }
+        if (tid < NB) {
+            // column tid of L11^-1 (unit lower triangular)
+            double x[NB];
 #pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    u[q] = 0.0;
-                    if (q < pnb) {
-                        const int src = j0 + s_perm[q];
-                        if (col - src <= kl + ku && src - col <= kl) u[q] = AB[bidx(src, col, kl, ku, ldab)];
-                    }
-                }
+            for (int q = 0; q < NB; ++q) {
+                double v = (q == tid) ? 1.0 : 0.0;
 #pragma unroll
-                for (int z = 0; z < NB; ++z) {
-                    low[z] = 0.0;
-                    if (z < nlow) {
-                        const int src = j0 + s_perm[s_low[z]];
-                        if (col - src <= kl + ku && src - col <= kl) low[z] = AB[bidx(src, col, kl, ku, ldab)];
-                    }
-                }
-#pragma unroll
-                for (int z = 0; z < NB; ++z)
-                    if (z < nlow && (j0 + s_low[z]) - col <= kl) AB[bidx(j0 + s_low[z], col, kl, ku, ldab)] = low[z];
-#pragma unroll
-                for (int q = 1; q < NB; ++q) {
-                    double v = u[q];
-#pragma unroll
-                    for (int qq = 0; qq < q; ++qq) v -= Pnl[q * PST + qq] * u[qq];
-                    u[q] = v;
-                }
-#pragma unroll
-                for (int q = 0; q < NB; ++q)
-                    if (q < pnb && col - (j0 + q) <= kl + ku) AB[bidx(j0 + q, col, kl, ku, ldab)] = u[q];
-            } else {
-#pragma unroll
-                for (int q = 0; q < NB; ++q) u[q] = 0.0;
+                for (int qq = 0; qq < q; ++qq) v -= (q < pnb ? Pnl[q * PST + qq] : 0.0) * x[qq];
+                x[q] = v;
             }
 #pragma unroll
-            for (int q = 0; q < NB; ++q) U12s[q * UST + t] = q < pnb ? u[q] : 0.0;
+            for (int q = 0; q < NB; ++q) s_linv[q * NB + tid] = x[q];
+        }
+        __syncthreads();
+        for (int t = tid; t < nlow * nc; t += NT) {
+            const int z = t / nc, cc = t % nc, col = c0 + cc;
+            const int row = j0 + s_low[z];
+            if (row - col <= kl) AB[bidx(row, col, kl, ku, ldab)] = U12s[z * UST + cc];
+        }
+        __syncthreads();
+        // U12 = L11^-1 A12 on DMMA; written to the band (top rows) and to U12s
+        {
+            const int g = lane >> 2, q4 = lane & 3;
+            const int tcn = ncpad >> 3;
+            for (int t = wid; t < 2 * tcn; t += NW) {
+                const int ti = t & 1, tj = t >> 1;
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int k0 = 0; k0 < NB; k0 += 4) {
+                    const double a = s_linv[(ti * 8 + g) * NB + k0 + q4];
+                    const double b = Tmp[(k0 + q4) * UST + tj * 8 + g];
+                    dmma884(d0, d1, a, b);
+                }
+                const int q = ti * 8 + g, cc = tj * 8 + 2 * q4;
+                U12s[q * UST + cc] = q < pnb ? d0 : 0.0;
+                U12s[q * UST + cc + 1] = q < pnb ? d1 : 0.0;
+                const int row = j0 + q;
+                if (q < pnb && cc < nc && c0 + cc - row <= kl + ku)
+                    AB[bidx(row, c0 + cc, kl, ku, ldab)] = d0;
+                if (q < pnb && cc + 1 < nc && c0 + cc + 1 - row <= kl + ku)
+                    AB[bidx(row, c0 + cc + 1, kl, ku, ldab)] = d1;
+            }
         }
         // phase A': right-hand sides -- permute + forward substitution (thread per column)
         for (int cy = tid; cy < ncy; cy += NT) {
@@ -255,7 +301,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         __syncthreads();
         // phase B: A22 -= L21 U12 on FP64 tensor cores (DMMA 8x8x4 tiles).
         // A warp owns a column tile: its U12 fragments stay in registers while
-        // it walks down the row tiles, prefetching the next C tile.
+        // it walks down the row tiles, four tiles in flight at a time.
         {
             const int mrows = nr - pnb;
             const int tr = (mrows + 7) >> 3, tcn = ncpad >> 3;
@@ -265,26 +311,36 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
 #pragma unroll
                 for (int kk = 0; kk < NB / 4; ++kk) bf[kk] = U12s[(4 * kk + q4) * UST + tj * 8 + g];
                 const int ca = c0 + tj * 8 + 2 * q4, cb = ca + 1;
-                auto load_c = [&](int ti, double &x0, double &x1) {
-                    const int row = j0 + pnb + ti * 8 + g;
-                    x0 = (row < r1 && ca < c1 && row - ca <= kl) ? AB[bidx(row, ca, kl, ku, ldab)] : 0.0;
-                    x1 = (row < r1 && cb < c1 && row - cb <= kl) ? AB[bidx(row, cb, kl, ku, ldab)] : 0.0;
-                };
-                double n0 = 0.0, n1 = 0.0;
-                if (tr > 0) load_c(0, n0, n1);
-                for (int ti = 0; ti < tr; ++ti) {
-                    double d0 = n0, d1 = n1;
-                    if (ti + 1 < tr) load_c(ti + 1, n0, n1);
-                    const int prow = pnb + ti * 8 + g;
-                    const bool ra = prow < nr;
+                // band column pointers: element (row, col) = colp[row]
+                double *pa = AB + (long long)ca * ldab + (kl + ku - ca);
+                double *pb = pa + (ldab - 1);
+                const int lima = ca < c1 ? min(r1, ca + kl + 1) : 0;
+                const int limb = cb < c1 ? min(r1, cb + kl + 1) : 0;
+                const int rbase = j0 + pnb + g;
+                for (int tg = 0; tg < tr; tg += 4) {
+                    double d0[4], d1[4];
 #pragma unroll
-                    for (int kk = 0; kk < NB / 4; ++kk) {
-                        const double a = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
-                        dmma884(d0, d1, a, bf[kk]);
+                    for (int h = 0; h < 4; ++h) {
+                        const int row = rbase + (tg + h) * 8;
+                        d0[h] = row < lima ? pa[row] : 0.0;
+                        d1[h] = row < limb ? pb[row] : 0.0;
                     }
-                    const int row = j0 + prow;
-                    if (row < r1 && ca < c1 && row - ca <= kl) AB[bidx(row, ca, kl, ku, ldab)] = d0;
-                    if (row < r1 && cb < c1 && row - cb <= kl) AB[bidx(row, cb, kl, ku, ldab)] = d1;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int prow = pnb + (tg + h) * 8 + g;
+                        const bool ra = prow < nr;
+#pragma unroll
+                        for (int kk = 0; kk < NB / 4; ++kk) {
+                            const double a = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
+                            dmma884(d0[h], d1[h], a, bf[kk]);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int row = rbase + (tg + h) * 8;
+                        if (row < lima) pa[row] = d0[h];
+                        if (row < limb) pb[row] = d1[h];
+                    }
                 }
             }
         }
@@ -317,6 +373,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             }
         }
         __syncthreads();
+        BPROF(5);
     }
 
     // ---- 3. blocked column-oriented back substitution with U ---------------
@@ -379,6 +436,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         }
         __syncthreads();
     }
+    BPROF(7);
 
     // ---- 4. border ------------------------------------------------------
     double *X = Xout + sys_xoff[s];
@@ -551,6 +609,15 @@ extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *s
     }
     MFB_CHECK_LAUNCH();
     return MFB_OK;
+}
+
+extern "C" int mfb_debug_bprof(unsigned long long *out) {
+#ifdef MFB_PROFILE
+    return cudaMemcpyFromSymbol(out, g_bprof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 2;
+#else
+    (void)out;
+    return 1;
+#endif
 }
 
 extern "C" int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,

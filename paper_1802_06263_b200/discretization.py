@@ -98,9 +98,9 @@ class Pattern:
 
     @property
     def smem_doubles(self):
-        # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 16 x (kl + ku + 8),
+        # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 + staging 2 x 16 x (kl + ku + 8),
         # rhs rows 16 x (nb + ndof + 1), (kl + 16) ints of row permutation
-        return ((self.kl + 16) * 17 + 16 * (self.kl + self.ku + 8)
+        return ((self.kl + 16) * 17 + 2 * 16 * (self.kl + self.ku + 8)
                 + 16 * (self.nb + self.ndof + 1) + (self.kl + 16) // 2 + 1)
 
 
