@@ -244,46 +244,76 @@ def run_ours(a):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
-    def step(eng):
-        eng.kl_fields()
-        eng.build_bases()
-        lam, iters, status, hist, _ = eng.solve_points(a.tol, max_iter)
-        mom = eng.moments(lam)
-        return lam, iters, status, mom
+    if ws > 1:
+        import torch.distributed as dist
+
+        from paper_1802_06263_b200.distributed import (DeviceShardEngine, run_method_distributed,
+                                                       run_sharded)
+
+        def step(eng):
+            out = run_sharded(eng, grid.n_real, nl, a.tol, max_iter, dist, rank, ws)
+            return out
+
+        def new_engine():
+            e = DeviceShardEngine(plan)
+            e.eng.timing = True
+            return e
+    else:
+        def step(eng):
+            eng.kl_fields()
+            eng.build_bases()
+            lam, iters, status, hist, _ = eng.solve_points(a.tol, max_iter)
+            mom = eng.moments(lam)
+            return lam, iters, status, mom
+
+        def new_engine():
+            e = S3Engine(plan)
+            e.timing = True
+            return e
 
     for _ in range(a.warmup):
-        eng = S3Engine(plan)
-        step(eng)
+        step(new_engine())
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
     dev_ms, e2e_s = [], []
-    solve_ms, solve_flops, launches = [], [], 0
+    solve_ms, launches = [], 0
     iters_host = None
     with ClockSampler(local) as clocks:
         for _ in range(a.steps):
             flush.fill_(1)
             torch.cuda.synchronize()
-            eng = S3Engine(plan)
-            eng.timing = True
+            if ws > 1:
+                torch.distributed.barrier()
+            eng = new_engine()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            lam, iters, status, mom = step(eng)   # moments include D2H of the results
+            out = step(eng)                       # moments include D2H of the results
             e1.record(stream)
             torch.cuda.synchronize()
             dev_ms.append(e0.elapsed_time(e1))
-            launches = eng.launches
-            for kind, s0, s1, fl, sfl in eng.solve_events:
+            core = eng.eng if ws > 1 else eng
+            launches = core.launches
+            for kind, s0, s1, fl, sfl in core.solve_events:
                 solve_ms.append((kind, s0.elapsed_time(s1), fl, sfl))
-            iters_host = iters.cpu().numpy()
-            eng.check_info()
+            if ws > 1:
+                iters_host = out[2] if out is not None else np.zeros(1)
+            else:
+                iters_host = out[1].cpu().numpy()
+            core.check_info()
         # end-to-end through the public API, host in / host out
         for _ in range(a.steps):
             flush.fill_(1)
             torch.cuda.synchronize()
+            if ws > 1:
+                torch.distributed.barrier()
             t = time.perf_counter()
-            res = run_method(problem, grid, method="S3", tol=a.tol)
+            if ws > 1:
+                res = run_method_distributed(problem, grid, tol=a.tol)
+                torch.cuda.synchronize()
+            else:
+                res = run_method(problem, grid, method="S3", tol=a.tol)
             e2e_s.append(time.perf_counter() - t)
     if ws > 1:
         tmax = torch.tensor([sum(dev_ms), sum(e2e_s)], dtype=torch.float64, device="cuda")
@@ -292,8 +322,9 @@ def run_ours(a):
     else:
         tot_ms, tot_e2e = sum(dev_ms), sum(e2e_s)
     ms_step = tot_ms / a.steps
-    value = ws * grid.n_real / (ms_step / 1000.0)
-    e2e_val = ws * grid.n_real / (tot_e2e / a.steps)
+    # ws > 1: the ranks share ONE sweep (points and subdomains sharded)
+    value = grid.n_real / (ms_step / 1000.0)
+    e2e_val = grid.n_real / (tot_e2e / a.steps)
     systems = plan.s3_systems()
     local_solves = int(sum(int(plan.ndof[s]) for s, _ in systems))
     peaks, fp64 = _peaks()
@@ -324,7 +355,8 @@ def run_ours(a):
                 "per_kind_ms_per_step": {k: v[0] / len(dev_ms) for k, v in kinds.items()}}
     basis_ms = sum(v[0] for v in kinds.values()) / max(len(dev_ms), 1)
     # bytes of the per-step inputs run_method uploads (collocation + KL tables)
-    h2d = int(res.timings.get("h2d_bytes", 0))
+    h2d = int(res.timings.get("h2d_bytes", 0)) if (res is not None and hasattr(res, "timings")) \
+        else 0
     d2h = 8 * grid.n_real * nl + 8 * grid.n_real * max_iter + 8 * grid.n_real * 2 + \
         16 * (nl + int(plan.nfield.sum()))
     if rank == 0:
@@ -332,12 +364,14 @@ def run_ours(a):
             "metric": f"collocation realizations/s (S3 sweep, {a.config})",
             "value": value, "unit": "realizations/s", "n_gpus": ws, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic Gauss-Hermite/Smolyak collocation of the "
                     "config; no dataset)",
             "config": {"workload": a.config, "n_real": grid.n_real, "n_lambda": nl,
                        "systems": len(systems), "tol": a.tol,
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+                       "parallelism": (f"sharded x{ws}: subdomains (pre-loop + moments), "
+                                       f"points (CG); NCCL all-reduce/all-gather")
+                       if ws > 1 else "single",
                        "l2": "flushed (256 MB write) before every timed step",
                        "plan_cached": True, "plan_build_s": plan_s},
             "basis_local_solves_per_s": local_solves / (basis_ms / 1000.0) if basis_ms else None,

@@ -1,0 +1,169 @@
+"""Multi-GPU S3 sweep: one process per GPU, torch.distributed for the plumbing.
+
+The path shards naturally:
+
+* pre-loop: subdomains are assigned to ranks (`sid_owners`); a rank builds
+  the flux-basis blocks, bar jumps and field responses of its subdomains'
+  local realizations only, then one all-reduce (SUM over zero-padded pools,
+  exact because every slot has a single non-zero contributor) gives every
+  rank the full basis pool;
+* main loop: each rank runs the batched CG on a contiguous range of
+  collocation points (`point_range`); one all-gather assembles lambda;
+* moments: the rank that owns a subdomain reduces its field keys with the
+  exact single-GPU arithmetic (groups live with their subdomain), rank 0
+  streams the lambda key; results are gathered on rank 0 in key order.
+
+Every number a rank computes is computed by the same kernel with the same
+inputs as on one GPU, so the N-rank result is bitwise the 1-rank result.
+The collectives are ordinary torch.distributed calls (NCCL on GPUs, gloo in
+the CPU tests), and `Engine` is the device engine (`interface.S3Engine`) or
+a CPU stand-in used by tests/test_distributed.py.
+"""
+
+import numpy as np
+
+
+def point_range(n_real, rank, world):
+    """Contiguous [k0, k1) block of collocation points for one rank."""
+    base, extra = divmod(n_real, world)
+    k0 = rank * base + min(rank, extra)
+    return k0, k0 + base + (1 if rank < extra else 0)
+
+
+def sid_owners(costs, world):
+    """Greedy longest-processing-time assignment of subdomains to ranks.
+
+    `costs[s]` is the basis-construction cost of subdomain s (systems x
+    work); ties go to the lowest rank, so the assignment is deterministic.
+    """
+    order = sorted(range(len(costs)), key=lambda s: (-costs[s], s))
+    load = [0.0] * world
+    owner = [0] * len(costs)
+    for s in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        owner[s] = r
+        load[r] += costs[s]
+    return owner
+
+
+def run_sharded(engine, n_real, n_lambda, tol, max_iter, dist, rank, world):
+    """Drive one sharded sweep; returns (moments, lam, iters, status, hist) on rank 0.
+
+    engine: object with build(sids), pools() -> list of tensors to all-reduce,
+    solve(k0, n) -> (lam, iters, status, hist), moments(lam_all, sids,
+    with_lambda) -> dict, to_host(t) -> numpy, and torch-like tensors.
+    dist: torch.distributed (initialised).
+    """
+    import torch
+    owners = sid_owners(engine.sid_costs(), world)
+    mine = [s for s, r in enumerate(owners) if r == rank]
+    engine.build(mine)
+    for t in engine.pools():
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    k0, k1 = point_range(n_real, rank, world)
+    lam, iters, status, hist = engine.solve(k0, k1 - k0, tol, max_iter)
+    # all-gather lambda and the per-point outputs (padded to the largest range)
+    width = point_range(n_real, 0, world)[1]
+    dev = lam.device
+
+    def gather(x, cols, dtype):
+        buf = torch.zeros((width, cols), dtype=dtype, device=dev)
+        buf[:x.shape[0]] = x.reshape(x.shape[0], cols)
+        out = [torch.zeros_like(buf) for _ in range(world)]
+        dist.all_gather(out, buf)
+        parts = [out[r][:point_range(n_real, r, world)[1] - point_range(n_real, r, world)[0]]
+                 for r in range(world)]
+        return torch.cat(parts, 0)
+
+    lam_all = gather(lam, n_lambda, lam.dtype)
+    iters_all = gather(iters.to(torch.int64), 1, torch.int64).reshape(-1)
+    status_all = gather(status.to(torch.int64), 1, torch.int64).reshape(-1)
+    hist_all = gather(hist, hist.shape[1], hist.dtype)
+    mom = engine.moments(lam_all, mine, with_lambda=(rank == 0))
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mom)
+    if rank != 0:
+        return None
+    merged = {}
+    for part in gathered:
+        merged.update(part)
+    keys = ["lambda"] + sorted((k for k in merged if k != "lambda"),
+                               key=lambda k: (int(k.split(":")[0]),
+                                              ["u", "p", "cv", "cp"].index(k.split(":")[1])))
+    moments = {k: merged[k] for k in keys}
+    return (moments, engine.to_host(lam_all), engine.to_host(iters_all),
+            engine.to_host(status_all), engine.to_host(hist_all))
+
+
+class DeviceShardEngine:
+    """`run_sharded` engine over the sm_100a S3Engine (one GPU per rank)."""
+
+    def __init__(self, plan):
+        from .interface import S3Engine
+        self.plan = plan
+        self.eng = S3Engine(plan)
+
+    def sid_costs(self):
+        p = self.plan
+        return [float(int(p.n_loc[s]) * (p.hyb[s].algorithmic_flops if s in p.hyb
+                                           else p.patterns[s].algorithmic_flops))
+                for s in range(p.n_sub)]
+
+    def build(self, sids):
+        st = self.eng.st
+        st.blocks.zero_()
+        st.hbar.zero_()
+        self.eng.kl_fields()
+        self.eng.build_bases(sids=sids)
+        self.eng.check_info()
+
+    def pools(self):
+        return [self.eng.st.blocks, self.eng.st.hbar]
+
+    def solve(self, k0, n, tol, max_iter):
+        lam, iters, status, hist, _ = self.eng.solve_points(tol, max_iter, k0=k0, n_pts=n)
+        return lam, iters, status, hist
+
+    def moments(self, lam_all, sids, with_lambda):
+        return self.eng.moments(lam_all, sids=sids, with_lambda=with_lambda)
+
+    @staticmethod
+    def to_host(t):
+        return t.cpu().numpy()
+
+
+def run_method_distributed(problem, grid, tol=1e-9, max_iter=None, basis_cap_mb=1024.0):
+    """S3 sweep sharded over the initialised torch.distributed world.
+
+    Returns the RunResult on rank 0 and None elsewhere.
+    """
+    import torch.distributed as dist
+
+    from .errors import ConvergenceError
+    from .interface import RunResult, SolveStats, _check_basis_cap, get_plan
+    rank, world = dist.get_rank(), dist.get_world_size()
+    plan = get_plan(problem, grid)
+    _check_basis_cap(plan.basis_bytes(), basis_cap_mb)
+    nl = problem.space.n_dof
+    if max_iter is None:
+        max_iter = max(50, 10 * nl)
+    out = run_sharded(DeviceShardEngine(plan), grid.n_real, nl, tol, max_iter, dist, rank,
+                      world)
+    if out is None:
+        return None
+    moments, lam, iters, status, hist = out
+    fail = np.nonzero((status == 1) | (status == 2))[0]
+    if len(fail):
+        k = int(fail[0])
+        raise ConvergenceError(f"CG failed at point {k} (status {int(status[k])})",
+                               hist[k, :int(iters[k])].tolist())
+    stats = SolveStats.new("S3", plan.n_sub)
+    stats.n_real = grid.n_real
+    stats.cg_iters = [int(x) for x in iters]
+    for s in range(plan.n_sub):
+        nloc = int(plan.n_loc[s])
+        stats.factorizations[s] = nloc
+        stats.basis_backsolves[s] = int(plan.ndof[s]) * nloc
+        stats.backsolves[s] = int(plan.ndof[s]) * nloc + 2 * grid.n_real
+    return RunResult(moments, stats, [lam[k] for k in range(grid.n_real)],
+                     [hist[k, :int(iters[k])].tolist() for k in range(grid.n_real)], grid)

@@ -252,16 +252,71 @@ class _S3Static:
             gptr.append(gptr[-1] + len(mem))
         voff = np.concatenate([[0], np.cumsum(nd)])
         coff = np.concatenate([[0], np.cumsum(nd * nd)])
-        self.d_gptr = _dev(np.array(gptr), i32)
-        self.d_mem = _dev(np.concatenate(members), i32)
-        self.d_voff, self.d_coff = _dev(voff[:-1], i64), _dev(coff[:-1], i64)
+        self._members, self._voff, self._coff = members, voff, coff
+        self._moff, self._fboff = moff, fboff
         self.nv, self.nc = int(voff[-1]), int(coff[-1])
-        sid_gptr = np.array([first[s] for s in range(plan.n_sub)] + [nsys], dtype=np.int32)
-        self.d_sgptr = _dev(sid_gptr, i32)
         self.out_off = np.concatenate([[0], np.cumsum(plan.nfield.astype(np.int64))])
-        self.d_outoff = _dev(self.out_off[:-1], i64)
+        self._mtab = {}
+        self._wave_cache = {}
         self.wtot = float(np.sum(grid.weights))
 
+
+    def moment_table(self, sids):
+        """Device group tables restricted to the systems of `sids` (cached)."""
+        key = tuple(sids)
+        tab = self._mtab.get(key)
+        if tab is not None:
+            return tab
+        import torch
+        plan = self._plan
+        i32, i64 = torch.int32, torch.int64
+        sel = [i for i, (s, _) in enumerate(self.systems) if s in set(sids)]
+        gptr = np.concatenate([[0], np.cumsum([len(self._members[i]) for i in sel])])
+        mem = np.concatenate([self._members[i] for i in sel]) if sel else np.zeros(1, int)
+        sys_pat = np.array([self.systems[i][0] for i in sel], dtype=np.int32)
+        sgptr, cur = [0], 0
+        for s in sids:
+            cur += sum(1 for i in sel if self.systems[i][0] == s)
+            sgptr.append(cur)
+        nf = plan.nfield[list(sids)].astype(np.int64)
+        out_off = np.concatenate([[0], np.cumsum(nf)])
+        tab = {"n": len(sel), "pat": _dev(sys_pat, i32), "gptr": _dev(gptr, i32),
+               "mem": _dev(mem, i32), "voff": _dev(self._voff[:-1][sel], i64),
+               "coff": _dev(self._coff[:-1][sel], i64),
+               "moff": _dev(self._moff[:-1][sel], i64),
+               "fboff": _dev(self._fboff[:-1][sel], i64),
+               "sgptr": _dev(np.array(sgptr), i32), "nfield": _dev(nf.astype(np.int32), i32),
+               "out_off": out_off, "d_outoff": _dev(out_off[:-1], i64), "sids": list(sids)}
+        self._mtab[key] = tab
+        return tab
+
+    def waves_for(self, sids):
+        """The basis waves restricted to the systems of `sids` (cached)."""
+        if sids is None:
+            return self.waves, self.hwaves
+        key = tuple(sorted(sids))
+        if key not in self._wave_cache:
+            import torch
+            keep = set(key)
+            out = []
+            for wl in (self.waves, self.hwaves):
+                sub = []
+                for w in wl:
+                    m = np.array([self.systems[i][0] in keep for i in w["idx"]])
+                    if not m.any():
+                        continue
+                    nw = {}
+                    for k, v in w.items():
+                        if isinstance(v, torch.Tensor) and v.numel() == len(w["idx"]):
+                            nw[k] = v[torch.as_tensor(np.nonzero(m)[0], device=v.device)]
+                        elif k == "idx":
+                            nw[k] = v[m]
+                        else:
+                            nw[k] = v
+                    sub.append(nw)
+                out.append(sub)
+            self._wave_cache[key] = tuple(out)
+        return self._wave_cache[key]
 
     def refresh_inputs(self):
         """Re-upload the sweep's inputs from the host: collocation weights, local
@@ -328,10 +383,11 @@ class S3Engine:
         return K
 
     # ------------------------------------------------------- (2) bases ----
-    def build_bases(self):
+    def build_bases(self, sids=None):
         st, plan = self.st, self.plan
-        P = ctypes.c_void_p
-        for w in st.waves:                      # generic banded LU (Stokes)
+        waves, hwaves = st.waves_for(sids)
+        self._last_waves = list(waves) + list(hwaves)
+        for w in waves:                         # generic banded LU (Stokes)
             cnt = len(w["idx"])
             if self.timing:
                 e0 = self._ev()
@@ -348,7 +404,7 @@ class S3Engine:
                 _ptr(st.M) if st.keep_fields else None, _ptr(w["moff"]),
                 _ptr(st.Fb) if st.keep_fields else None, _ptr(w["fboff"]), self.sp),
                 "mfb_systems_extract")
-        for w in st.hwaves:                     # hybridised Darcy condensation
+        for w in hwaves:                        # hybridised Darcy condensation
             cnt = len(w["idx"])
             keep = st.keep_fields
             if self.timing:
@@ -375,7 +431,7 @@ class S3Engine:
 
     def check_info(self):
         info = np.zeros(len(self.st.systems), dtype=np.int64)
-        for w in self.st.waves + self.st.hwaves:
+        for w in getattr(self, "_last_waves", self.st.waves + self.st.hwaves):
             info[w["idx"]] = w["info"].cpu().numpy()
         bad = np.nonzero(info != 0)[0]
         if len(bad):
@@ -406,48 +462,58 @@ class S3Engine:
         return lam, iters, status, hist, g
 
     # ----------------------------------------------------- (4) moments ----
-    def moments(self, lam):
+    def moments(self, lam, sids=None, with_lambda=True):
+        """Moment dict over the "lambda" key (if with_lambda) and the field keys
+        of `sids` (default: every subdomain). `lam` holds every point."""
         torch, plan, st = self.torch, self.plan, self.st
         nl, n_real = plan.n_lambda, plan.grid.n_real
         f64 = torch.float64
-        ng = len(st.systems)
-        m = torch.empty(3 * nl, dtype=f64, device="cuda")
-        self.launches += 4
-        _lib.check(self.L.mfb_lambda_moments(
-            nl, n_real, _ptr(lam), _ptr(plan.d_weights), _ptr(m),
-            ctypes.c_void_p(m.data_ptr() + 8 * nl), ctypes.c_void_p(m.data_ptr() + 16 * nl),
-            self.sp), "mfb_lambda_moments")
+        sids = list(range(plan.n_sub)) if sids is None else list(sids)
+        tab = st.moment_table(sids)
+        ng = tab["n"]
+        out = {}
+        if with_lambda:
+            m = torch.empty(3 * nl, dtype=f64, device="cuda")
+            self.launches += 1
+            _lib.check(self.L.mfb_lambda_moments(
+                nl, n_real, _ptr(lam), _ptr(plan.d_weights), _ptr(m),
+                ctypes.c_void_p(m.data_ptr() + 8 * nl), ctypes.c_void_p(m.data_ptr() + 16 * nl),
+                self.sp), "mfb_lambda_moments")
+            lm = m.cpu().numpy()
+            out["lambda"] = _finalize("lambda", lm[:nl], lm[nl:2 * nl], lm[2 * nl:])
+        if not ng:
+            return out
         W = torch.empty(ng, dtype=f64, device="cuda")
         lstar = torch.empty(st.nv, dtype=f64, device="cuda")
         s_ = torch.empty_like(lstar)
         C = torch.empty(st.nc, dtype=f64, device="cuda")
+        self.launches += 3
         _lib.check(self.L.mfb_group_stats(
-            ng, _ptr(st.d_pat), _ptr(st.d_gptr), _ptr(st.d_mem), _ptr(plan.d_ndof),
+            ng, _ptr(tab["pat"]), _ptr(tab["gptr"]), _ptr(tab["mem"]), _ptr(plan.d_ndof),
             _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map), nl, _ptr(lam), _ptr(plan.d_weights),
-            _ptr(st.d_voff), _ptr(st.d_coff), _ptr(W), _ptr(lstar), _ptr(s_), _ptr(C),
+            _ptr(tab["voff"]), _ptr(tab["coff"]), _ptr(W), _ptr(lstar), _ptr(s_), _ptr(C),
             self.sp), "mfb_group_stats")
         nfb = int(st.Fb.numel())
         fstar = torch.empty(3 * nfb, dtype=f64, device="cuda")
         fp = fstar.data_ptr()
         _lib.check(self.L.mfb_group_fields(
-            ng, _ptr(st.d_pat), _ptr(plan.d_ndof), _ptr(plan.d_nfield), _ptr(st.M),
-            _ptr(st.d_moff), _ptr(st.Fb), _ptr(st.d_fboff), _ptr(st.d_voff),
-            _ptr(st.d_coff), _ptr(lstar), _ptr(s_), _ptr(C), ctypes.c_void_p(fp),
+            ng, _ptr(tab["pat"]), _ptr(plan.d_ndof), _ptr(plan.d_nfield), _ptr(st.M),
+            _ptr(tab["moff"]), _ptr(st.Fb), _ptr(tab["fboff"]), _ptr(tab["voff"]),
+            _ptr(tab["coff"]), _ptr(lstar), _ptr(s_), _ptr(C), ctypes.c_void_p(fp),
             ctypes.c_void_p(fp + 8 * nfb), ctypes.c_void_p(fp + 16 * nfb), self.sp),
             "mfb_group_fields")
-        nout = int(st.out_off[-1])
+        out_off = tab["out_off"]
+        nout = int(out_off[-1])
         mv = torch.empty(2 * nout, dtype=f64, device="cuda")
         _lib.check(self.L.mfb_moments_reduce(
-            plan.n_sub, _ptr(st.d_sgptr), _ptr(plan.d_nfield), _ptr(st.d_fboff), _ptr(W),
+            len(sids), _ptr(tab["sgptr"]), _ptr(tab["nfield"]), _ptr(tab["fboff"]), _ptr(W),
             ctypes.c_void_p(fp), ctypes.c_void_p(fp + 8 * nfb), ctypes.c_void_p(fp + 16 * nfb),
-            st.wtot, _ptr(st.d_outoff), _ptr(mv), ctypes.c_void_p(mv.data_ptr() + 8 * nout),
+            st.wtot, _ptr(tab["d_outoff"]), _ptr(mv), ctypes.c_void_p(mv.data_ptr() + 8 * nout),
             self.sp), "mfb_moments_reduce")
-        lm = m.cpu().numpy()
-        out = {"lambda": _finalize("lambda", lm[:nl], lm[nl:2 * nl], lm[2 * nl:])}
         mvh = mv.cpu().numpy()
         mf, vf = mvh[:nout], mvh[nout:]
-        for s in range(plan.n_sub):
-            base = st.out_off[s]
+        for j, s in enumerate(sids):
+            base = out_off[j]
             for name, start, shape in plan.patterns[s].field_layout:
                 size = int(np.prod(shape))
                 mm = mf[base + start: base + start + size].reshape(shape)

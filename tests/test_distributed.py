@@ -1,0 +1,168 @@
+"""Sharded S3 orchestration on CPU with gloo (world_size 2).
+
+The device kernels cannot run here, so the engine is a CPU stand-in with
+the same interface as distributed.DeviceShardEngine: deterministic "basis"
+values per (subdomain, local realization) slot, a per-point "CG" that reads
+the full pool, and per-subdomain "moments" over every point. The test
+checks that ownership, the pool all-reduce, the lambda all-gather and the
+rank-0 merge reproduce the single-rank result bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1802_06263_b200.distributed import point_range, run_sharded, sid_owners
+
+N_SUB, N_LOC, N_REAL, N_LAMBDA, HIST = 5, 4, 37, 6, 3
+
+
+class FakeEngine:
+    def __init__(self):
+        self.pool = torch.zeros(N_SUB * N_LOC, dtype=torch.float64)
+
+    def sid_costs(self):
+        return [float(3 + (s % 3)) for s in range(N_SUB)]
+
+    def build(self, sids):
+        self.pool.zero_()
+        for s in sids:
+            for l in range(N_LOC):
+                self.pool[s * N_LOC + l] = np.sin(1.0 + s * 7.3 + l * 1.1)
+
+    def pools(self):
+        return [self.pool]
+
+    def solve(self, k0, n, tol, max_iter):
+        lam = torch.zeros((n, N_LAMBDA), dtype=torch.float64)
+        for j in range(n):
+            k = k0 + j
+            for d in range(N_LAMBDA):
+                lam[j, d] = self.pool[(k * 3 + d) % self.pool.numel()] * (1 + 0.01 * k)
+        iters = torch.arange(k0, k0 + n, dtype=torch.int32) % 7 + 1
+        status = torch.zeros(n, dtype=torch.int32)
+        hist = torch.full((n, HIST), 0.5, dtype=torch.float64)
+        return lam, iters, status, hist
+
+    def moments(self, lam_all, sids, with_lambda):
+        L = lam_all.numpy()
+        out = {}
+        if with_lambda:
+            out["lambda"] = (L.mean(0), L.var(0))
+        for s in sids:
+            f = L[:, s % N_LAMBDA] * (s + 1)
+            out[f"{s}:u"] = (np.array([f.sum()]), np.array([(f * f).sum()]))
+            out[f"{s}:p"] = (np.array([f.max()]), np.array([f.min()]))
+        return out
+
+    @staticmethod
+    def to_host(t):
+        return t.numpy()
+
+
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = run_sharded(FakeEngine(), N_REAL, N_LAMBDA, 1e-9, 10, dist, rank, world)
+        if rank == 0:
+            mom, lam, iters, status, hist = out
+            q.put({"mom": {k: (v[0].tolist(), v[1].tolist()) for k, v in mom.items()},
+                   "lam": lam.tolist(), "iters": iters.tolist()})
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_partition_helpers():
+    ranges = [point_range(37, r, 4) for r in range(4)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == 37
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    assert max(b - a for a, b in ranges) - min(b - a for a, b in ranges) <= 1
+    own = sid_owners([5, 1, 4, 4, 2], 2)
+    assert sorted(set(own)) == [0, 1]
+    assert own == sid_owners([5, 1, 4, 4, 2], 2)          # deterministic
+
+
+@pytest.mark.timeout(300)
+def test_two_ranks_match_one_rank_bitwise():
+    one = _run(1)
+    two = _run(2)
+    assert one["lam"] == two["lam"]
+    assert one["iters"] == two["iters"]
+    assert list(one["mom"]) == list(two["mom"])
+    for k in one["mom"]:
+        assert one["mom"][k] == two["mom"][k], k
+
+
+def _gpu_worker(rank, world, port, q, name):
+    import json as _json
+
+    from conftest import GOLDEN
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    # gloo moves the collectives through the host: the two ranks' kernels never
+    # wait on one another, so sharing one GPU is a functional (not perf) test
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1802_06263_b200.config import build_from_config, validate_config
+        from paper_1802_06263_b200.distributed import run_method_distributed
+        z = np.load(os.path.join(GOLDEN, name + ".npz"))
+        problem, grid, _ = build_from_config(validate_config(_json.loads(str(z["config_json"]))))
+        res = run_method_distributed(problem, grid, tol=1e-11)
+        if rank == 0:
+            q.put({"lam": np.array(res.lambdas).tolist(),
+                   "mom": {k: (v[0].ravel().tolist(), v[1].ravel().tolist())
+                           for k, v in res.moments.items()},
+                   "iters": res.stats.cg_iters})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_device_sharded_sweep_matches_single_gpu(gpu, name):
+    from conftest import case_from_golden
+    from paper_1802_06263_b200.interface import run_method
+    _, problem, grid, _ = case_from_golden(name)
+    ref = run_method(problem, grid, method="S3", tol=1e-11)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, name)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert np.array_equal(np.array(got["lam"]), np.array(ref.lambdas))
+    assert got["iters"] == ref.stats.cg_iters
+    assert list(got["mom"]) == list(ref.moments)
+    for k, (m, v) in ref.moments.items():
+        assert np.array_equal(np.array(got["mom"][k][0]), m.ravel()), k
+        assert np.array_equal(np.array(got["mom"][k][1]), v.ravel()), k

@@ -35,8 +35,9 @@ print("n", h.n, "w", h.w, "panels", (h.n + 15) // 16)
 out = (ctypes.c_ulonglong * 16)()
 _lib.load().mfb_debug_bprof(out)
 v = np.array(out[:], dtype=np.float64)
-names = {1: "load panel", 2: "panel factor", 3: "perm+writeback", 4: "phase A (U12, rhs)",
-         5: "phase B (DMMA trailing + rhs)", 7: "back substitution"}
+names = {1: "load panel", 2: "panel factor", 3: "perm+writeback", 4: "phase A (stage+U12)",
+         6: "phase A' (rhs top)", 8: "phase B (DMMA trailing)", 5: "phase B' (rhs below)",
+         7: "back substitution"}
 tot = sum(v[i] for i in names)
 print("band_solve CTA 0 (first Stokes system):")
 for i, nme in names.items():
