@@ -44,9 +44,25 @@ __device__ __forceinline__ long long bidx(int i, int k, int kl, int ku, int ldab
 }
 
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+#ifdef MFB_NO_DMMA
+    // debug: the same 8x8x4 product with scalar FMAs (fragment exchange by shuffles)
+    const int lane = threadIdx.x & 31, g = lane >> 2, q4 = lane & 3;
+    double s0 = d0, s1 = d1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double ak = __shfl_sync(0xffffffffu, a, g * 4 + k);
+        const double b0 = __shfl_sync(0xffffffffu, b, (2 * q4) * 4 + k);
+        const double b1 = __shfl_sync(0xffffffffu, b, (2 * q4 + 1) * 4 + k);
+        s0 = fma(ak, b0, s0);
+        s1 = fma(ak, b1, s1);
+    }
+    d0 = s0;
+    d1 = s1;
+#else
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
+#endif
 }
 
 template <int NT>
@@ -66,9 +82,6 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     __shared__ int s_low[NB];
     __shared__ int s_nlow;
     __shared__ double s_u11[NB * NB];
-    __shared__ double s_linv[NB * NB];
-    __shared__ double s_bord[MAX_NB * MAX_NCY];
-    __shared__ double s_z[MAX_NB * MAX_NCY];
     __shared__ int s_flag;
 #ifdef MFB_PROFILE
     __shared__ long long s_bt0;
@@ -79,14 +92,15 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     const double *K = Kbuf + sys_koff[s];
     const int n = P.n, kl = P.kl, ku = P.ku, ldab = P.ldab, nb = P.nb;
     const int nrhs = P.ndof + 1;
-    const int ncy = nb + nrhs;
+    const int ncy = nrhs;              // rhs block: N_dof mortar columns + bar
     const int UST = kl + ku + 8;
     double *AB = work + sys_woff[s];
     double *Y = AB + (long long)ldab * n;
     double *Pnl = smem;                          // (kl + NB) x PST   panel L | U11
     double *U12s = Pnl + (kl + NB) * PST;        // NB x UST          U12 of the panel
     double *Tmp = U12s + NB * UST;               // NB x UST          staged A12
-    double *Ytop = Tmp + NB * UST;               // NB x ncy          rhs rows of the panel
+    const int TMPN = max(NB * UST, 3 * MAX_NB * MAX_NCY);   // also kernel-projection scratch
+    double *Ytop = Tmp + TMPN;                   // NB x ncy          rhs rows of the panel
     int *s_perm = reinterpret_cast<int *>(Ytop + NB * ncy);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
@@ -100,14 +114,12 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             v += mfb_term(P.t_kind[t], P.t_c[t], K, P.t_k[t]);
         AB[bidx(P.e_row[e], P.e_col[e], kl, ku, ldab)] = v;
     }
-    for (long long t = tid; t < (long long)n * nb; t += NT)
-        Y[(t / nb) * ncy + (t % nb)] = P.E[t];
     for (int d = 0; d < P.ndof; ++d)
         for (int q = P.q_ptr[d] + tid; q < P.q_ptr[d + 1]; q += NT) {
             int r = P.q_row[q];
-            if (r < n) Y[(long long)r * ncy + nb + d] = P.q_val[q];
+            if (r < n) Y[(long long)r * ncy + d] = P.q_val[q];
         }
-    for (int i = tid; i < n; i += NT) Y[(long long)i * ncy + nb + P.ndof] = P.bar_const[i];
+    for (int i = tid; i < n; i += NT) Y[(long long)i * ncy + P.ndof] = P.bar_const[i];
     __syncthreads();
     for (int b = tid; b < P.n_bar_rows; b += NT) {
         int r = P.b_row[b];
@@ -115,10 +127,65 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         double v = 0.0;
         for (int t = P.b_tptr[b]; t < P.b_tptr[b + 1]; ++t)
             v += mfb_term(P.bt_kind[t], P.bt_c[t], K, P.bt_k[t]);
-        Y[(long long)r * ncy + nb + P.ndof] += v;
+        Y[(long long)r * ncy + P.ndof] += v;
     }
     __syncthreads();
 
+    // ---- 1b. rigid-body kernel (Stokes, nb > 0): make the rhs compatible --
+    // The reference pins the kernel with Lagrange rows C (stokes.py:276-298):
+    // K x + C^T mu = r, C x = 0. With the nb pinned dofs J removed, K_II is
+    // regular; mu = (C C^T)^-1 C r, then K_II x~ = (r - C^T mu)_I, x~_J = 0,
+    // and x = x~ - C^T (C C^T)^-1 C x~ (section 4). E = C_I^T, G = [C_J; (CC^T)^-1].
+    const int lane0 = tid & 31, wid0 = tid >> 5;
+    if (nb > 0) {
+        double *s_cr = Tmp;                      // nb x nrhs  (C r, then mu)
+        for (int pr = wid0; pr < nb * nrhs; pr += NT / 32) {
+            const int a = pr / nrhs, c = pr % nrhs;
+            double acc = 0.0;
+            for (int i = lane0; i < n; i += 32) acc += P.E[(long long)i * nb + a] * Y[(long long)i * ncy + c];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+            if (lane0 == 0) s_cr[pr] = acc;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // pinned rows of r: Q entries with row >= n, bar_const and bar terms
+            double *rj = Tmp + MAX_NB * MAX_NCY;
+            for (int t = 0; t < nb * nrhs; ++t) rj[t] = 0.0;
+            for (int d = 0; d < P.ndof; ++d)
+                for (int q = P.q_ptr[d]; q < P.q_ptr[d + 1]; ++q)
+                    if (P.q_row[q] >= n) rj[(P.q_row[q] - n) * nrhs + d] += P.q_val[q];
+            for (int b = 0; b < nb; ++b) rj[b * nrhs + P.ndof] += P.bar_const[n + b];
+            for (int bb = 0; bb < P.n_bar_rows; ++bb) {
+                const int r = P.b_row[bb];
+                if (r < n) continue;
+                double v = 0.0;
+                for (int t = P.b_tptr[bb]; t < P.b_tptr[bb + 1]; ++t)
+                    v += mfb_term(P.bt_kind[t], P.bt_c[t], K, P.bt_k[t]);
+                rj[(r - n) * nrhs + P.ndof] += v;
+            }
+            double *cr = Tmp + 2 * MAX_NB * MAX_NCY;
+            for (int a = 0; a < nb; ++a)
+                for (int c = 0; c < nrhs; ++c) {
+                    double v = s_cr[a * nrhs + c];
+                    for (int b = 0; b < nb; ++b) v += P.G[a * nb + b] * rj[b * nrhs + c];
+                    cr[a * nrhs + c] = v;
+                }
+            for (int a = 0; a < nb; ++a)
+                for (int c = 0; c < nrhs; ++c) {
+                    double v = 0.0;
+                    for (int b = 0; b < nb; ++b) v += P.G[(nb + a) * nb + b] * cr[b * nrhs + c];
+                    s_cr[a * nrhs + c] = v;              // mu
+                }
+        }
+        __syncthreads();
+        for (long long t = tid; t < (long long)n * nrhs; t += NT) {
+            const int i = (int)(t / nrhs), c = (int)(t % nrhs);
+            double v = Y[(long long)i * ncy + c];
+            for (int a = 0; a < nb; ++a) v -= P.E[(long long)i * nb + a] * s_cr[a * nrhs + c];
+            Y[(long long)i * ncy + c] = v;
+        }
+    }
     if (tid == 0) s_flag = 0;
     __syncthreads();
     // ---- 2. blocked banded LU with partial pivoting (gbtrf) --------------
@@ -230,19 +297,6 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             Tmp[q * UST + cc] = vt ? x : 0.0;
             U12s[q * UST + cc] = vl ? y : 0.0;
         }
-        if (tid < NB) {
-            // column tid of L11^-1 (unit lower triangular)
-            double x[NB];
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                double v = (q == tid) ? 1.0 : 0.0;
-#pragma unroll
-                for (int qq = 0; qq < q; ++qq) v -= (q < pnb ? Pnl[q * PST + qq] : 0.0) * x[qq];
-                x[q] = v;
-            }
-#pragma unroll
-            for (int q = 0; q < NB; ++q) s_linv[q * NB + tid] = x[q];
-        }
         __syncthreads();
         for (int t = tid; t < nlow * nc; t += NT) {
             const int z = t / nc, cc = t % nc, col = c0 + cc;
@@ -250,27 +304,25 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             if (row - col <= kl) AB[bidx(row, col, kl, ku, ldab)] = U12s[z * UST + cc];
         }
         __syncthreads();
-        // U12 = L11^-1 A12 on DMMA; written to the band (top rows) and to U12s
-        {
-            const int g = lane >> 2, q4 = lane & 3;
-            const int tcn = ncpad >> 3;
-            for (int t = wid; t < 2 * tcn; t += NW) {
-                const int ti = t & 1, tj = t >> 1;
-                double d0 = 0.0, d1 = 0.0;
+        // U12 = L11^-1 A12 by forward substitution (thread per column, as gbtrf's
+        // dtrsm): written to the band (top rows) and to U12s
+        for (int cc = tid; cc < ncpad; cc += NT) {
+            double u[NB];
 #pragma unroll
-                for (int k0 = 0; k0 < NB; k0 += 4) {
-                    const double a = s_linv[(ti * 8 + g) * NB + k0 + q4];
-                    const double b = Tmp[(k0 + q4) * UST + tj * 8 + g];
-                    dmma884(d0, d1, a, b);
-                }
-                const int q = ti * 8 + g, cc = tj * 8 + 2 * q4;
-                U12s[q * UST + cc] = q < pnb ? d0 : 0.0;
-                U12s[q * UST + cc + 1] = q < pnb ? d1 : 0.0;
+            for (int q = 0; q < NB; ++q) u[q] = Tmp[q * UST + cc];
+#pragma unroll
+            for (int q = 1; q < NB; ++q) {
+                double v = u[q];
+#pragma unroll
+                for (int qq = 0; qq < q; ++qq) v -= Pnl[q * PST + qq] * u[qq];
+                u[q] = q < pnb ? v : 0.0;
+            }
+            const int col = c0 + cc;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                U12s[q * UST + cc] = q < pnb ? u[q] : 0.0;
                 const int row = j0 + q;
-                if (q < pnb && cc < nc && c0 + cc - row <= kl + ku)
-                    AB[bidx(row, c0 + cc, kl, ku, ldab)] = d0;
-                if (q < pnb && cc + 1 < nc && c0 + cc + 1 - row <= kl + ku)
-                    AB[bidx(row, c0 + cc + 1, kl, ku, ldab)] = d1;
+                if (q < pnb && cc < nc && col - row <= kl + ku) AB[bidx(row, col, kl, ku, ldab)] = u[q];
             }
         }
         // phase A': right-hand sides -- permute + forward substitution (thread per column)
@@ -438,86 +490,38 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     }
     BPROF(7);
 
-    // ---- 4. border ------------------------------------------------------
+    // ---- 4. project out the rigid-body kernel (nb > 0) --------------------
     double *X = Xout + sys_xoff[s];
     if (nb > 0) {
-        const int lane = tid & 31, wid = tid >> 5;
-        for (int pr = wid; pr < nb * ncy; pr += NT / 32) {
-            const int a = pr / ncy, col = pr % ncy;
+        double *s_cx = Tmp;                      // nb x nrhs: C x~, then alpha
+        for (int pr = wid0; pr < nb * nrhs; pr += NT / 32) {
+            const int a = pr / nrhs, c = pr % nrhs;
             double acc = 0.0;
-            for (int i = lane; i < n; i += 32)
-                acc += P.E[(long long)i * nb + a] * Y[(long long)i * ncy + col];
+            for (int i = lane0; i < n; i += 32) acc += P.E[(long long)i * nb + a] * Y[(long long)i * ncy + c];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-            if (lane == 0) s_bord[pr] = acc;
+            if (lane0 == 0) s_cx[MAX_NB * MAX_NCY + pr] = acc;
         }
         __syncthreads();
-        if (tid == 0) {
-            // Sigma (nb x nb) in s_bord[a*ncy + b], rhs (nb x nrhs) in s_z
-            for (int a = 0; a < nb; ++a) {
-                for (int b = 0; b < nb; ++b)
-                    s_bord[a * ncy + b] = P.G[a * nb + b] - s_bord[a * ncy + b];
-                for (int c = 0; c < nrhs; ++c) s_z[a * nrhs + c] = -s_bord[a * ncy + nb + c];
-                s_z[a * nrhs + P.ndof] += P.bar_const[n + a];
-            }
-            for (int d = 0; d < P.ndof; ++d)
-                for (int q = P.q_ptr[d]; q < P.q_ptr[d + 1]; ++q)
-                    if (P.q_row[q] >= n) s_z[(P.q_row[q] - n) * nrhs + d] += P.q_val[q];
-            for (int b = 0; b < P.n_bar_rows; ++b) {
-                int r = P.b_row[b];
-                if (r < n) continue;
-                double v = 0.0;
-                for (int t = P.b_tptr[b]; t < P.b_tptr[b + 1]; ++t)
-                    v += mfb_term(P.bt_kind[t], P.bt_c[t], K, P.bt_k[t]);
-                s_z[(r - n) * nrhs + P.ndof] += v;
-            }
-            // Gaussian elimination with partial pivoting on Sigma
-            int ok = 1;
-            for (int c = 0; c < nb && ok; ++c) {
-                int pr = c;
-                for (int r = c + 1; r < nb; ++r)
-                    if (fabs(s_bord[r * ncy + c]) > fabs(s_bord[pr * ncy + c])) pr = r;
-                if (s_bord[pr * ncy + c] == 0.0) { ok = 0; break; }
-                if (pr != c) {
-                    for (int b = 0; b < nb; ++b) {
-                        double t0 = s_bord[c * ncy + b];
-                        s_bord[c * ncy + b] = s_bord[pr * ncy + b];
-                        s_bord[pr * ncy + b] = t0;
-                    }
-                    for (int b = 0; b < nrhs; ++b) {
-                        double t0 = s_z[c * nrhs + b];
-                        s_z[c * nrhs + b] = s_z[pr * nrhs + b];
-                        s_z[pr * nrhs + b] = t0;
-                    }
-                }
-                for (int r = c + 1; r < nb; ++r) {
-                    double l = s_bord[r * ncy + c] / s_bord[c * ncy + c];
-                    for (int b = c; b < nb; ++b) s_bord[r * ncy + b] -= l * s_bord[c * ncy + b];
-                    for (int b = 0; b < nrhs; ++b) s_z[r * nrhs + b] -= l * s_z[c * nrhs + b];
-                }
-            }
-            if (ok) {
-                for (int c = nb - 1; c >= 0; --c)
-                    for (int b = 0; b < nrhs; ++b) {
-                        double v = s_z[c * nrhs + b];
-                        for (int r = c + 1; r < nb; ++r) v -= s_bord[c * ncy + r] * s_z[r * nrhs + b];
-                        s_z[c * nrhs + b] = v / s_bord[c * ncy + c];
-                    }
-            }
-            s_flag = ok;
+        if (tid < nb * nrhs) {
+            const int a = tid / nrhs, c = tid % nrhs;
+            double v = 0.0;
+            for (int b = 0; b < nb; ++b) v += P.G[(nb + a) * nb + b] * s_cx[MAX_NB * MAX_NCY + b * nrhs + c];
+            s_cx[a * nrhs + c] = v;
         }
         __syncthreads();
-        if (!s_flag) {
-            if (tid == 0) info[s] = -1;
-            return;
-        }
         for (long long t = tid; t < (long long)n * nrhs; t += NT) {
             const int i = (int)(t / nrhs), c = (int)(t % nrhs);
-            double v = Y[(long long)i * ncy + nb + c];
-            for (int a = 0; a < nb; ++a) v -= Y[(long long)i * ncy + a] * s_z[a * nrhs + c];
+            double v = Y[(long long)i * ncy + c];
+            for (int a = 0; a < nb; ++a) v -= P.E[(long long)i * nb + a] * s_cx[a * nrhs + c];
             X[t] = v;
         }
-        for (int t = tid; t < nb * nrhs; t += NT) X[(long long)n * nrhs + t] = s_z[t];
+        for (int t = tid; t < nb * nrhs; t += NT) {
+            const int b = t / nrhs, c = t % nrhs;
+            double v = 0.0;
+            for (int a = 0; a < nb; ++a) v -= P.G[a * nb + b] * s_cx[a * nrhs + c];
+            X[(long long)n * nrhs + t] = v;
+        }
     } else {
         for (long long t = tid; t < (long long)n * nrhs; t += NT) X[t] = Y[t];
     }

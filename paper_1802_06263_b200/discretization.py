@@ -84,7 +84,7 @@ class Pattern:
 
     @property
     def work_doubles(self):
-        return self.ldab * self.n + self.n * (self.nb + self.ndof + 1)
+        return self.ldab * self.n + self.n * (self.ndof + 1)
 
     @property
     def x_doubles(self):
@@ -100,8 +100,9 @@ class Pattern:
     def smem_doubles(self):
         # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 + staging 2 x 16 x (kl + ku + 8),
         # rhs rows 16 x (nb + ndof + 1), (kl + 16) ints of row permutation
-        return ((self.kl + 16) * 17 + 2 * 16 * (self.kl + self.ku + 8)
-                + 16 * (self.nb + self.ndof + 1) + (self.kl + 16) // 2 + 1)
+        return ((self.kl + 16) * 17 + 16 * (self.kl + self.ku + 8)
+                + max(16 * (self.kl + self.ku + 8), 3 * 8 * 160)
+                + 16 * (self.ndof + 1) + (self.kl + 16) // 2 + 1)
 
 
 class _TermTable:
@@ -498,7 +499,7 @@ def stokes_pattern(problem, sid, k0_offsets, K0_host):
                 p_idx[(ly // 2) * (mesh.nx + 1) + lx // 2] = nxt
                 nxt += 1
     n = nxt
-    nb = 2 * kdim
+    nb = kdim
     for a, d in enumerate(J_dofs):
         vel_idx[d] = n + a                      # border numbering
     sysidx_u = vel_idx
@@ -520,31 +521,21 @@ def stokes_pattern(problem, sid, k0_offsets, K0_host):
     kl = int(np.max(e_row - e_col))
     ku = int(np.max(e_col - e_row))
 
-    # border: E (n x nb), G (nb x nb); constant because J avoids BJS dofs
+    # rigid-body constraints C (rows over the free velocity dofs): interior part
+    # E = C_I^T (n x k), pinned part C_J (k x k) and (C C^T)^-1 (k x k) stacked
+    # in G; the device solves the pinned system for a compatible rhs and
+    # projects (see band_solve_kernel, section 4)
     E = np.zeros((n, nb))
-    G = np.zeros((nb, nb))
+    G = np.zeros((2 * nb, nb))
     if kdim:
-        Aconst = A_full.tocsc()
-        for a, d in enumerate(J_dofs):
-            col = Aconst[:, d].toarray().ravel()
-            for dd in np.nonzero(col)[0]:
-                if vel_idx[dd] >= 0 and vel_idx[dd] < n:
-                    E[vel_idx[dd], a] += col[dd]
-                elif vel_idx[dd] >= n:
-                    G[vel_idx[dd] - n, a] += col[dd]
-            bcol = np.zeros(npr)
-            sel = pcl == d
-            np.add.at(bcol, prw[sel], pval[sel])
-            for pp in np.nonzero(bcol)[0]:
-                E[p_idx[pp], a] += bcol[pp]
         for r in range(kdim):
             crow = np.zeros(nud)
             crow[free] = C[r]
             inter = (vel_idx >= 0) & (vel_idx < n)
-            E[vel_idx[inter], kdim + r] = crow[inter]
+            E[vel_idx[inter], r] = crow[inter]
             for a, d in enumerate(J_dofs):
-                G[a, kdim + r] = crow[d]
-                G[kdim + r, a] = crow[d]
+                G[r, a] = crow[d]
+        G[kdim:, :] = np.linalg.inv(C @ C.T)
 
     # Q and the readout of lifted data on the traces
     pos, ndof = _local_mortar_positions(problem, sid)

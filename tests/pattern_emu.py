@@ -15,15 +15,12 @@ def term_values(kind, c, k, K):
 
 
 def dense_system(pat, K):
+    """Interior matrix K_II (n x n) and the rhs block over rows I and J."""
     n, nb = pat.n, pat.nb
-    A = np.zeros((n + nb, n + nb))
+    A = np.zeros((n, n))
     vals = np.add.reduceat(term_values(pat.t_kind, pat.t_c, pat.t_k, K), pat.e_tptr[:-1]) \
         if len(pat.e_row) else np.zeros(0)
     A[pat.e_row, pat.e_col] = vals
-    if nb:
-        A[:n, n:] = pat.E
-        A[n:, :n] = pat.E.T
-        A[n:, n:] = pat.G
     rhs = np.zeros((n + nb, pat.ndof + 1))
     for d in range(pat.ndof):
         sl = slice(pat.q_ptr[d], pat.q_ptr[d + 1])
@@ -36,8 +33,21 @@ def dense_system(pat, K):
 
 
 def solve(pat, K):
+    """Mirror of band_solve_kernel: compatible rhs, pinned solve, projection."""
     A, rhs = dense_system(pat, K)
-    X = np.linalg.solve(A, rhs)
+    n, nb = pat.n, pat.nb
+    if nb:
+        Cf = np.zeros((nb, n + nb))
+        Cf[:, :n] = pat.E.T
+        Cf[:, n:] = pat.G[:nb]
+        Ci = pat.G[nb:]
+        mu = Ci @ (Cf @ rhs)
+        rt = rhs - Cf.T @ mu
+        Xt = np.zeros_like(rhs)
+        Xt[:n] = np.linalg.solve(A, rt[:n])
+        X = Xt - Cf.T @ (Ci @ (Cf @ Xt))
+    else:
+        X = np.linalg.solve(A, rhs)
     nd = pat.ndof
     Q = np.zeros((pat.n + pat.nb, nd))
     for d in range(nd):
