@@ -133,14 +133,17 @@ int mfb_kl_realize(const double *phi, const double *mean, int n_cells, int n_ter
  * sys_woff[s] holds ldab*n band + n*(nb+ndof+1) doubles; the solution
  * X (n+nb rows x ndof+1 columns, row-major) goes to X + sys_xoff[s].
  * info[s]: 0 ok, j+1 zero pivot at band column j, -1 singular border.
- * threads: 128/256/512/1024 per system; smem_doubles >= max over the
- * patterns used of (2*kl + ku + 3 + nb + ndof + 1).
+ * threads: 128/256/512 per CTA; smem_doubles: Pattern.smem_doubles of
+ * the widest pattern. group: CTAs per system (>1: cooperative launch of
+ * n_sys*group CTAs that split the trailing and rhs columns; `bar` is a
+ * device scratch of n_sys counters, zeroed by the call).
  */
 int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *sys_pat,
                       const double *Kbuf, const long long *sys_koff,
                       double *work, const long long *sys_woff,
                       double *X, const long long *sys_xoff, int *info,
-                      int threads, int smem_doubles, void *stream);
+                      int threads, int smem_doubles, int group, unsigned int *bar,
+                      void *stream);
 
 /*
  * From X: basis block Bt (column-major ndof x ndof, i.e. Bt[c*ndof+r] =

@@ -48,7 +48,7 @@ _SIGS = {
     "mfb_version": ([], ctypes.c_char_p),
     "mfb_strerror": ([_i], ctypes.c_char_p),
     "mfb_kl_realize": ([_p, _p, _i, _i, _p, _i, _p, _p], _i),
-    "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p], _i),
+    "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p], _i),
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
                         _p, _p, _p, _p, _i, _p, _p], _i),

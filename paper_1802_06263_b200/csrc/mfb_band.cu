@@ -65,13 +65,35 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 #endif
 }
 
+// Barrier among the C CTAs that share one system (co-resident: cooperative
+// launch). Writes before it are published at GPU scope; reads of data other
+// CTAs wrote go through L2 (__ldcg) because L1 is not coherent.
+__device__ __forceinline__ void group_sync(unsigned int *ctr, int C, unsigned int &target) {
+    __syncthreads();
+    if (C > 1) {
+        if (threadIdx.x == 0) {
+            target += C;
+            __threadfence();
+            atomicAdd(ctr, 1u);
+            unsigned int v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                if (v >= target) break;
+                __nanosleep(32);
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT)
 band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ sys_pat,
                   const double *__restrict__ Kbuf, const long long *__restrict__ sys_koff,
                   double *__restrict__ work, const long long *__restrict__ sys_woff,
                   double *__restrict__ Xout, const long long *__restrict__ sys_xoff,
-                  int *__restrict__ info) {
+                  int *__restrict__ info, int C, unsigned int *__restrict__ bar) {
     constexpr int NB = BAND_NB;
     constexpr int PST = NB + 1;          // odd stride: lane-varying rows hit distinct banks
     constexpr int NW = NT / 32;
@@ -87,7 +109,11 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     __shared__ long long s_bt0;
 #endif
 
-    const int s = blockIdx.x;
+    // C CTAs cooperate on system s: rank owns the trailing-column tiles and
+    // rhs-column tiles t with t % C == rank; the panel is factored redundantly
+    const int s = blockIdx.x / C, rank = blockIdx.x % C;
+    unsigned int bar_target = 0;
+    unsigned int *ctr = bar + s;
     const MfbPattern P = pats[sys_pat[s]];
     const double *K = Kbuf + sys_koff[s];
     const int n = P.n, kl = P.kl, ku = P.ku, ldab = P.ldab, nb = P.nb;
@@ -106,22 +132,23 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
 
     // ---- 1. assembly ---------------------------------------------------
     const long long nab = (long long)ldab * n, ny = (long long)n * ncy;
-    for (long long t = tid; t < nab + ny; t += NT) AB[t] = 0.0;
-    __syncthreads();
-    for (int e = tid; e < P.n_entries; e += NT) {
+    const int gt = rank * NT + tid, GS = C * NT;
+    for (long long t = gt; t < nab + ny; t += GS) AB[t] = 0.0;
+    group_sync(ctr, C, bar_target);
+    for (int e = gt; e < P.n_entries; e += GS) {
         double v = 0.0;
         for (int t = P.e_tptr[e]; t < P.e_tptr[e + 1]; ++t)
             v += mfb_term(P.t_kind[t], P.t_c[t], K, P.t_k[t]);
         AB[bidx(P.e_row[e], P.e_col[e], kl, ku, ldab)] = v;
     }
     for (int d = 0; d < P.ndof; ++d)
-        for (int q = P.q_ptr[d] + tid; q < P.q_ptr[d + 1]; q += NT) {
+        for (int q = P.q_ptr[d] + gt; q < P.q_ptr[d + 1]; q += GS) {
             int r = P.q_row[q];
             if (r < n) Y[(long long)r * ncy + d] = P.q_val[q];
         }
-    for (int i = tid; i < n; i += NT) Y[(long long)i * ncy + P.ndof] = P.bar_const[i];
-    __syncthreads();
-    for (int b = tid; b < P.n_bar_rows; b += NT) {
+    for (int i = gt; i < n; i += GS) Y[(long long)i * ncy + P.ndof] = P.bar_const[i];
+    group_sync(ctr, C, bar_target);
+    for (int b = gt; b < P.n_bar_rows; b += GS) {
         int r = P.b_row[b];
         if (r >= n) continue;
         double v = 0.0;
@@ -129,7 +156,8 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             v += mfb_term(P.bt_kind[t], P.bt_c[t], K, P.bt_k[t]);
         Y[(long long)r * ncy + P.ndof] += v;
     }
-    __syncthreads();
+    group_sync(ctr, C, bar_target);
+#define OWN(tile) (((tile) % C) == rank)
 
     // ---- 1b. rigid-body kernel (Stokes, nb > 0): make the rhs compatible --
     // The reference pins the kernel with Lagrange rows C (stokes.py:276-298):
@@ -141,6 +169,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         double *s_cr = Tmp;                      // nb x nrhs  (C r, then mu)
         for (int pr = wid0; pr < nb * nrhs; pr += NT / 32) {
             const int a = pr / nrhs, c = pr % nrhs;
+            if (!OWN(c >> 3)) continue;
             double acc = 0.0;
             for (int i = lane0; i < n; i += 32) acc += P.E[(long long)i * nb + a] * Y[(long long)i * ncy + c];
 #pragma unroll
@@ -181,6 +210,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         __syncthreads();
         for (long long t = tid; t < (long long)n * nrhs; t += NT) {
             const int i = (int)(t / nrhs), c = (int)(t % nrhs);
+            if (!OWN(c >> 3)) continue;
             double v = Y[(long long)i * ncy + c];
             for (int a = 0; a < nb; ++a) v -= P.E[(long long)i * nb + a] * s_cr[a * nrhs + c];
             Y[(long long)i * ncy + c] = v;
@@ -202,9 +232,10 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             const int i = t % nr, c = t / nr;
             const int r = j0 + i, col = j0 + c;
             Pnl[i * PST + c] = (c < pnb && r - col <= kl && col - r <= kl + ku)
-                                   ? AB[bidx(r, col, kl, ku, ldab)] : 0.0;
+                                   ? __ldcg(AB + bidx(r, col, kl, ku, ldab)) : 0.0;
         }
-        __syncthreads();
+        // every CTA must hold the panel before rank 0 writes its factors back
+        group_sync(ctr, C, bar_target);
         BPROF(1);
         if (tid < 128) {
             // panel LU with partial pivoting on 4 warps (named barrier 2); the
@@ -231,7 +262,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 for (int w = 1; w < 4; ++w)
                     if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < p)) { bv = red_v[w]; p = red_i[w]; }
                 if (!(bv > 0.0)) {
-                    if (tid == 0) { info[s] = j0 + c + 1; s_flag = -1; }
+                    if (tid == 0) { if (rank == 0) info[s] = j0 + c + 1; s_flag = -1; }
                     break;
                 }
                 if (tid == 0) s_ipiv[c] = p;
@@ -277,17 +308,19 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         }
         __syncthreads();
         BPROF(3);
-        for (int t = tid; t < nr * pnb; t += NT) {
-            const int i = t % nr, c = t / nr;
-            const int r = j0 + i, col = j0 + c;
-            if (r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = Pnl[i * PST + c];
-        }
+        if (rank == 0)
+            for (int t = tid; t < nr * pnb; t += NT) {
+                const int i = t % nr, c = t / nr;
+                const int r = j0 + i, col = j0 + c;
+                if (r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = Pnl[i * PST + c];
+            }
         // phase A: stage the permuted top rows of every trailing column (Tmp)
         // and the moved lower rows (U12s used as staging); all reads first
         const int nlow = s_nlow;
         const int ncpad = (nc + 7) & ~7;
         for (int t = tid; t < NB * ncpad; t += NT) {
             const int q = t / ncpad, cc = t % ncpad, col = c0 + cc;
+            if (!OWN((c0 >> 3) + (cc >> 3))) continue;
             const int src = j0 + (q < pnb ? s_perm[q] : 0);
             const bool vt = q < pnb && cc < nc && col - src <= kl + ku && src - col <= kl;
             const int srl = j0 + (q < nlow ? s_perm[s_low[q]] : 0);
@@ -300,6 +333,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         __syncthreads();
         for (int t = tid; t < nlow * nc; t += NT) {
             const int z = t / nc, cc = t % nc, col = c0 + cc;
+            if (!OWN((c0 >> 3) + (cc >> 3))) continue;
             const int row = j0 + s_low[z];
             if (row - col <= kl) AB[bidx(row, col, kl, ku, ldab)] = U12s[z * UST + cc];
         }
@@ -307,6 +341,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         // U12 = L11^-1 A12 by forward substitution (thread per column, as gbtrf's
         // dtrsm): written to the band (top rows) and to U12s
         for (int cc = tid; cc < ncpad; cc += NT) {
+            if (!OWN((c0 >> 3) + (cc >> 3))) continue;
             double u[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) u[q] = Tmp[q * UST + cc];
@@ -327,6 +362,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         }
         // phase A': right-hand sides -- permute + forward substitution (thread per column)
         for (int cy = tid; cy < ncy; cy += NT) {
+            if (!OWN(cy >> 3)) continue;
             double u[NB], low[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q)
@@ -358,7 +394,11 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             const int mrows = nr - pnb;
             const int tr = (mrows + 7) >> 3, tcn = ncpad >> 3;
             const int g = lane >> 2, q4 = lane & 3;
-            for (int tj = wid; tj < tcn; tj += NW) {
+            // absolute tile ownership: a column keeps its owner across panels,
+            // so its (L1-cached) reads only ever see the owner's own writes
+            const int tbase = c0 >> 3;
+            const int tj0 = ((rank - tbase) % C + C) % C;
+            for (int tj = tj0 + C * wid; tj < tcn; tj += C * NW) {
                 double bf[NB / 4];
 #pragma unroll
                 for (int kk = 0; kk < NB / 4; ++kk) bf[kk] = U12s[(4 * kk + q4) * UST + tj * 8 + g];
@@ -409,7 +449,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
 #pragma unroll
                 for (int kk = 0; kk < NB / 4; ++kk) af[kk] = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
                 const long long row = j0 + prow;
-                for (int tc = 0; tc < tcy; ++tc) {
+                for (int tc = rank; tc < tcy; tc += C) {
                     const int ca = tc * 8 + 2 * q4, cb = ca + 1;
                     double d0 = (ra && ca < ncy) ? Y[row * ncy + ca] : 0.0;
                     double d1 = (ra && cb < ncy) ? Y[row * ncy + cb] : 0.0;
@@ -424,7 +464,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 }
             }
         }
-        __syncthreads();
+        group_sync(ctr, C, bar_target);
         BPROF(5);
     }
 
@@ -434,10 +474,11 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         const int pnb = min(NB, n - j0);
         for (int t = tid; t < NB * NB; t += NT) {
             const int r = t / NB, c = t % NB;
-            s_u11[t] = (r < pnb && c < pnb && c >= r) ? AB[bidx(j0 + r, j0 + c, kl, ku, ldab)] : 0.0;
+            s_u11[t] = (r < pnb && c < pnb && c >= r) ? __ldcg(AB + bidx(j0 + r, j0 + c, kl, ku, ldab)) : 0.0;
         }
         __syncthreads();
         for (int cy = tid; cy < ncy; cy += NT) {
+            if (!OWN(cy >> 3)) continue;
             double x[NB];
 #pragma unroll
             for (int r = NB - 1; r >= 0; --r) {
@@ -469,9 +510,9 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 for (int kk = 0; kk < NB / 4; ++kk) {
                     const int k = 4 * kk + q4;
                     af[kk] = (ri && k < pnb && (j0 + k) - i <= kl + ku)
-                                 ? -AB[bidx(i, j0 + k, kl, ku, ldab)] : 0.0;
+                                 ? -__ldcg(AB + bidx(i, j0 + k, kl, ku, ldab)) : 0.0;
                 }
-                for (int tc = 0; tc < tcy; ++tc) {
+                for (int tc = rank; tc < tcy; tc += C) {
                     const int ca = tc * 8 + 2 * q4, cb = ca + 1;
                     double d0 = (ri && ca < ncy) ? Y[(long long)i * ncy + ca] : 0.0;
                     double d1 = (ri && cb < ncy) ? Y[(long long)i * ncy + cb] : 0.0;
@@ -496,6 +537,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         double *s_cx = Tmp;                      // nb x nrhs: C x~, then alpha
         for (int pr = wid0; pr < nb * nrhs; pr += NT / 32) {
             const int a = pr / nrhs, c = pr % nrhs;
+            if (!OWN(c >> 3)) continue;
             double acc = 0.0;
             for (int i = lane0; i < n; i += 32) acc += P.E[(long long)i * nb + a] * Y[(long long)i * ncy + c];
 #pragma unroll
@@ -512,20 +554,24 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         __syncthreads();
         for (long long t = tid; t < (long long)n * nrhs; t += NT) {
             const int i = (int)(t / nrhs), c = (int)(t % nrhs);
+            if (!OWN(c >> 3)) continue;
             double v = Y[(long long)i * ncy + c];
             for (int a = 0; a < nb; ++a) v -= P.E[(long long)i * nb + a] * s_cx[a * nrhs + c];
             X[t] = v;
         }
         for (int t = tid; t < nb * nrhs; t += NT) {
             const int b = t / nrhs, c = t % nrhs;
+            if (!OWN(c >> 3)) continue;
             double v = 0.0;
             for (int a = 0; a < nb; ++a) v -= P.G[a * nb + b] * s_cx[a * nrhs + c];
             X[(long long)n * nrhs + t] = v;
         }
     } else {
-        for (long long t = tid; t < (long long)n * nrhs; t += NT) X[t] = Y[t];
+        for (long long t = tid; t < (long long)n * nrhs; t += NT)
+            if (OWN((int)(t % nrhs) >> 3)) X[t] = Y[t];
     }
-    if (tid == 0) info[s] = 0;
+    if (tid == 0 && rank == 0) info[s] = 0;
+#undef OWN
 }
 
 template <int NT>
@@ -569,50 +615,51 @@ extract_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ sys_
 
 }  // namespace
 
+template <int NT>
+static int launch_band(int n_sys, int C, size_t smem, cudaStream_t st, const MfbPattern *pats,
+                       const int *sys_pat, const double *Kbuf, const long long *sys_koff,
+                       double *work, const long long *sys_woff, double *X,
+                       const long long *sys_xoff, int *info, unsigned int *bar) {
+    if (cudaFuncSetAttribute(band_solve_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return MFB_ERR_SMEM;
+    if (C == 1) {
+        band_solve_kernel<NT><<<n_sys, NT, smem, st>>>(pats, sys_pat, Kbuf, sys_koff, work,
+                                                       sys_woff, X, sys_xoff, info, C, bar);
+    } else {
+        // the C CTAs of a system wait on one another: cooperative launch
+        // guarantees they are co-resident
+        if (cudaMemsetAsync(bar, 0, sizeof(unsigned int) * n_sys, st) != cudaSuccess)
+            return MFB_ERR_LAUNCH;
+        void *args[] = {(void *)&pats, (void *)&sys_pat, (void *)&Kbuf, (void *)&sys_koff,
+                        (void *)&work, (void *)&sys_woff, (void *)&X, (void *)&sys_xoff,
+                        (void *)&info, (void *)&C, (void *)&bar};
+        if (cudaLaunchCooperativeKernel((const void *)band_solve_kernel<NT>, dim3(n_sys * C),
+                                        dim3(NT), args, smem, st) != cudaSuccess)
+            return MFB_ERR_LAUNCH;
+    }
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
 extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *sys_pat,
                                  const double *Kbuf, const long long *sys_koff,
                                  double *work, const long long *sys_woff, double *X,
                                  const long long *sys_xoff, int *info, int threads,
-                                 int smem_doubles, void *stream) {
+                                 int smem_doubles, int group, unsigned int *bar, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
-    // dynamic smem: see Pattern.smem_doubles (discretization.py)
-    const int nt = threads;
-    size_t smem = (size_t)smem_doubles * sizeof(double);
+    if (group < 1 || (group > 1 && bar == nullptr)) return MFB_ERR_ARG;
+    const size_t smem = (size_t)smem_doubles * sizeof(double);
     cudaStream_t st = mfb_stream(stream);
-    switch (nt) {
-        case 128:
-            if (cudaFuncSetAttribute(band_solve_kernel<128>,
-                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-                return MFB_ERR_SMEM;
-            band_solve_kernel<128><<<n_sys, 128, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
-                                                             work, sys_woff, X, sys_xoff, info);
-            break;
-        case 256:
-            if (cudaFuncSetAttribute(band_solve_kernel<256>,
-                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-                return MFB_ERR_SMEM;
-            band_solve_kernel<256><<<n_sys, 256, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
-                                                             work, sys_woff, X, sys_xoff, info);
-            break;
-        case 512:
-            if (cudaFuncSetAttribute(band_solve_kernel<512>,
-                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-                return MFB_ERR_SMEM;
-            band_solve_kernel<512><<<n_sys, 512, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
-                                                             work, sys_woff, X, sys_xoff, info);
-            break;
-        case 1024:
-            if (cudaFuncSetAttribute(band_solve_kernel<1024>,
-                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-                return MFB_ERR_SMEM;
-            band_solve_kernel<1024><<<n_sys, 1024, smem, st>>>(pats, sys_pat, Kbuf, sys_koff,
-                                                               work, sys_woff, X, sys_xoff, info);
-            break;
-        default:
-            return MFB_ERR_ARG;
+    switch (threads) {
+        case 128: return launch_band<128>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
+                                          work, sys_woff, X, sys_xoff, info, bar);
+        case 256: return launch_band<256>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
+                                          work, sys_woff, X, sys_xoff, info, bar);
+        case 512: return launch_band<512>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
+                                          work, sys_woff, X, sys_xoff, info, bar);
+        default: return MFB_ERR_ARG;
     }
-    MFB_CHECK_LAUNCH();
-    return MFB_OK;
 }
 
 extern "C" int mfb_debug_bprof(unsigned long long *out) {

@@ -35,6 +35,8 @@ log = logging.getLogger(__name__)
 METHODS = ("S1", "S2", "S3")
 _PLAN_CACHE = {}
 WORK_BUDGET_BYTES = 8 << 30
+N_SMS = 148                 # B200
+BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 
 
 @dataclass
@@ -192,7 +194,10 @@ class _S3Static:
             nt = 512 if max(pats[systems[i][0]].kl for i in grp) > 128 else 256
             w = sub(grp)
             w["info"] = torch.zeros(len(grp), dtype=i32, device="cuda")
-            w.update(nt=nt, woff=_dev(woff[:-1], i64), xoff=_dev(xoff[:-1], i64),
+            # CTAs per system: fill the SMs when systems are few (one CTA per SM
+            # when the band needs most of the shared memory)
+            grpsz = max(1, min(BAND_GROUP_MAX, N_SMS // max(len(grp), 1)))
+            w.update(nt=nt, group=grpsz, woff=_dev(woff[:-1], i64), xoff=_dev(xoff[:-1], i64),
                      flops=sum(pats[systems[i][0]].algorithmic_flops for i in grp))
             self.waves.append(w)
             wmax, xmax = max(wmax, int(woff[-1])), max(xmax, int(xoff[-1]))
@@ -228,6 +233,7 @@ class _S3Static:
                 self.hwaves.append(w)
                 lmax, hxmax = max(lmax, int(loff[-1])), max(hxmax, int(hxoff[-1]))
         self.work = torch.empty(max(wmax, 1), dtype=f64, device="cuda")
+        self.bar = torch.zeros(max(len(systems), 1), dtype=torch.int32, device="cuda")
         self.X = torch.empty(max(xmax, 1), dtype=f64, device="cuda")
         self.Lstore = torch.empty(max(lmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
         self.HX = torch.empty(max(hxmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
@@ -394,7 +400,7 @@ class S3Engine:
             _lib.check(self.L.mfb_systems_solve(
                 _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
                 _ptr(st.work), _ptr(w["woff"]), _ptr(st.X), _ptr(w["xoff"]), _ptr(w["info"]),
-                w["nt"], st.smem, self.sp), "mfb_systems_solve")
+                w["nt"], st.smem, w["group"], _ptr(st.bar), self.sp), "mfb_systems_solve")
             if self.timing:
                 self.solve_events.append(("band", e0, self._ev(), w["flops"], w["flops"]))
             self.launches += 2
