@@ -161,3 +161,27 @@ def test_cfg5_basis_blocks(gpu):
             B = blocks[eng.sys_boff[idx]: eng.sys_boff[idx] + nd * nd].reshape(nd, nd).T
             err = np.max(np.abs(B - z[key])) / np.max(np.abs(z[key]))
             assert err <= 1e-10, (key, err)
+
+
+def test_cfg4_basis_blocks(gpu):
+    """cfg4 (16x8 subdomains, 8 regions, 289 local realizations): sampled blocks."""
+    z = golden("cfg4")
+    from conftest import ROOT, case_from_config
+    from paper_1802_06263_b200.interface import S3Engine, get_plan
+    _, problem, grid, _ = case_from_config(f"{ROOT}/configs/cfg4.json")
+    plan = get_plan(problem, grid)
+    eng = S3Engine(plan, keep_fields=False)
+    eng.kl_fields()
+    eng.build_bases()
+    eng.check_info()
+    blocks = eng.blocks.cpu().numpy()
+    checked = 0
+    for idx, (s, l) in enumerate(eng.systems):
+        key = f"B__{s}__{l}"
+        if key in z:
+            nd = int(plan.ndof[s])
+            B = blocks[eng.sys_boff[idx]: eng.sys_boff[idx] + nd * nd].reshape(nd, nd).T
+            err = np.max(np.abs(B - z[key])) / np.max(np.abs(z[key]))
+            assert err <= 1e-10, (key, err)
+            checked += 1
+    assert checked >= 6
