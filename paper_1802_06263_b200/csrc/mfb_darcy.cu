@@ -128,15 +128,20 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
         const int nb = min(BP, n - k);
         const int rend = min(n, k + BP + w);
         const int nrow = rend - k;
+        const int kslot = k % m;                  // window slot of row k
         for (int t = tid; t < nrow * BP; t += HYB_NT) {
             const int i = t / BP, p = t % BP;
+            int sl = kslot + i;
+            if (sl >= m) sl -= m;
             double v = 0.0;
-            if (p < nb && i >= p && i - p <= w) v = W[((k + i) % m) * ws + (p - i + w)];
+            if (p < nb && i >= p && i - p <= w) v = W[sl * ws + (p - i + w)];
             Lb[i * LS + p] = v;
         }
         for (int t = tid; t < BP * Cp; t += HYB_NT) {
-            const int p = t / Cp, c = t % Cp;
-            Yb[t] = p < nb ? Pb[((k + p) % m) * Cp + c] : 0.0;
+            const int p = t / Cp, c = t - p * Cp;
+            int sl = kslot + p;
+            if (sl >= m) sl -= m;
+            Yb[t] = p < nb ? Pb[sl * Cp + c] : 0.0;
         }
         __syncthreads();
         PROF_MARK(1);
@@ -208,8 +213,12 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
             // zero them, sync the assembly warps, scatter the term-table entries
             const int r0 = k + m, r1 = min(n, k + m + BP);
             const int at = tid - 32, an = HYB_NT - 32;
-            for (int t = at; t < (r1 - r0) * ws; t += an) W[((r0 + t / ws) % m) * ws + t % ws] = 0.0;
-            for (int t = at; t < (r1 - r0) * Cp; t += an) Pb[((r0 + t / Cp) % m) * Cp + t % Cp] = 0.0;
+            for (int q = 0; q < r1 - r0; ++q) {
+                int sl = kslot + q;                   // new row r0+q reuses the slot of k+q
+                if (sl >= m) sl -= m;
+                for (int t = at; t < ws; t += an) W[sl * ws + t] = 0.0;
+                for (int t = at; t < Cp; t += an) Pb[sl * Cp + t] = 0.0;
+            }
             asm volatile("bar.sync 1, %0;" ::"r"(HYB_NT - 32));
             if (r1 > r0) assemble_entries(P, K, r0, r1, at, an, W, Pb, m, ws, Cp);
         }
@@ -223,64 +232,63 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
             for (int t = tid; t < nrow * LS; t += HYB_NT) dst[t] = Lb[t];
             for (int t = tid; t < BP * Cp; t += HYB_NT) dst[(long long)m * LS + t] = Yb[t];
         }
-        // trailing updates on DMMA: window (lower band), border panel, Schur block
+        // trailing updates on DMMA: window (lower band), border panel, Schur
+        // block. A warp owns whole row tiles (its A fragments stay in registers
+        // across the row's window and border tiles); row tiles are dealt in
+        // snake order so the triangular work is balanced across warps.
         const int R = nrow - nb;
         const int tr = (R + 7) >> 3, tc = Cp >> 3;
-        const int nd_t = tr * (tr + 1) / 2, ne_t = tr * tc, nf_t = tc * tc;
-        for (int t = wid; t < nd_t + ne_t + nf_t; t += HYB_NW) {
-            if (t < nd_t) {
-                int ti = 0;
-                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-                const int tj = t - ti * (ti + 1) / 2;
+        int rbase = kslot + nb;
+        if (rbase >= m) rbase -= m;
+        for (int it = wid; it < tr + tc; it += HYB_NW) {
+            if (it < tr) {
+                const int ti = (it & 1) ? (tr - 1 - (it >> 1)) : (it >> 1);
                 const int ii = ti * 8 + g;
-                const int ja = tj * 8 + 2 * q4, jb = ja + 1;
-                const bool va = ii < R && ja <= ii, vb = ii < R && jb <= ii;
-                const int rr = (k + nb + ii) % m;
-                double d0 = va ? W[rr * ws + (ja - ii + w)] : 0.0;
-                double d1 = vb ? W[rr * ws + (jb - ii + w)] : 0.0;
-                const int ra = nb + ti * 8 + g, rb = nb + tj * 8 + g;
-#pragma unroll
-                for (int k0 = 0; k0 < BP; k0 += 4) {
-                    const double a = ra < nrow ? -Lb[ra * LS + k0 + q4] : 0.0;
-                    const double b = rb < nrow ? Lb[rb * LS + k0 + q4] : 0.0;
-                    dmma(d0, d1, a, b);
+                const int ra = nb + ii;
+                const double a0 = ra < nrow ? -Lb[ra * LS + q4] : 0.0;
+                const double a1 = ra < nrow ? -Lb[ra * LS + 4 + q4] : 0.0;
+                int rr = rbase + ii;
+                if (rr >= m) rr -= m;
+                const bool rv = ii < R;
+                double *rowW = W + (rv ? rr : 0) * ws + (w - ii);
+                double *rowP = Pb + (rv ? rr : 0) * Cp;
+                for (int tj = 0; tj <= ti; ++tj) {
+                    const int rb = nb + tj * 8 + g;
+                    const double b0 = rb < nrow ? Lb[rb * LS + q4] : 0.0;
+                    const double b1 = rb < nrow ? Lb[rb * LS + 4 + q4] : 0.0;
+                    const int ja = tj * 8 + 2 * q4;
+                    const bool va = rv && ja <= ii, vb = rv && ja + 1 <= ii;
+                    double d0 = va ? rowW[ja] : 0.0;
+                    double d1 = vb ? rowW[ja + 1] : 0.0;
+                    dmma(d0, d1, a0, b0);
+                    dmma(d0, d1, a1, b1);
+                    if (va) rowW[ja] = d0;
+                    if (vb) rowW[ja + 1] = d1;
                 }
-                if (va) W[rr * ws + (ja - ii + w)] = d0;
-                if (vb) W[rr * ws + (jb - ii + w)] = d1;
-            } else if (t < nd_t + ne_t) {
-                const int u = t - nd_t;
-                const int ti = u / tc, tcol = u % tc;
-                const int ii = ti * 8 + g;
-                const int ca = tcol * 8 + 2 * q4;
-                const bool v = ii < R;
-                const int rr = (k + nb + ii) % m;
-                double d0 = v ? Pb[rr * Cp + ca] : 0.0;
-                double d1 = v ? Pb[rr * Cp + ca + 1] : 0.0;
-                const int ra = nb + ti * 8 + g;
-#pragma unroll
-                for (int k0 = 0; k0 < BP; k0 += 4) {
-                    const double a = ra < nrow ? -Lb[ra * LS + k0 + q4] : 0.0;
-                    const double b = Yb[(k0 + q4) * Cp + tcol * 8 + g];
-                    dmma(d0, d1, a, b);
-                }
-                if (v) {
-                    Pb[rr * Cp + ca] = d0;
-                    Pb[rr * Cp + ca + 1] = d1;
+                for (int tcol = 0; tcol < tc; ++tcol) {
+                    const int ca = tcol * 8 + 2 * q4;
+                    double d0 = rv ? rowP[ca] : 0.0;
+                    double d1 = rv ? rowP[ca + 1] : 0.0;
+                    dmma(d0, d1, a0, Yb[q4 * Cp + tcol * 8 + g]);
+                    dmma(d0, d1, a1, Yb[(4 + q4) * Cp + tcol * 8 + g]);
+                    if (rv) {
+                        rowP[ca] = d0;
+                        rowP[ca + 1] = d1;
+                    }
                 }
             } else {
-                const int u = t - nd_t - ne_t;
-                const int t1 = u / tc, t2 = u % tc;
-                const int ca = t2 * 8 + 2 * q4;
-                double d0 = S[(t1 * 8 + g) * Cp + ca];
-                double d1 = S[(t1 * 8 + g) * Cp + ca + 1];
-#pragma unroll
-                for (int k0 = 0; k0 < BP; k0 += 4) {
-                    const double a = -Yb[(k0 + q4) * Cp + t1 * 8 + g];
-                    const double b = Yb[(k0 + q4) * Cp + t2 * 8 + g];
-                    dmma(d0, d1, a, b);
+                const int t1 = it - tr;
+                const double a0 = -Yb[q4 * Cp + t1 * 8 + g];
+                const double a1 = -Yb[(4 + q4) * Cp + t1 * 8 + g];
+                double *rowS = S + (t1 * 8 + g) * Cp;
+                for (int t2 = 0; t2 < tc; ++t2) {
+                    const int ca = t2 * 8 + 2 * q4;
+                    double d0 = rowS[ca], d1 = rowS[ca + 1];
+                    dmma(d0, d1, a0, Yb[q4 * Cp + t2 * 8 + g]);
+                    dmma(d0, d1, a1, Yb[(4 + q4) * Cp + t2 * 8 + g]);
+                    rowS[ca] = d0;
+                    rowS[ca + 1] = d1;
                 }
-                S[(t1 * 8 + g) * Cp + ca] = d0;
-                S[(t1 * 8 + g) * Cp + ca + 1] = d1;
             }
         }
         __syncthreads();

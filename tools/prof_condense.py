@@ -16,8 +16,13 @@ from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 problem, grid, _ = load_config(f"configs/{cfg}.json")
+if cfg == "cfg5":
+    from paper_1802_06263_b200.collocation import build_tensor_grid
+    loc = build_tensor_grid([3] * 6)
+    grid.local_points = [loc.points.copy() for _ in problem.perm.regions]
+    grid.local_counts = [loc.n_real] * len(problem.perm.regions)
 plan = get_plan(problem, grid)
-eng = S3Engine(plan)
+eng = S3Engine(plan, keep_fields=(cfg != "cfg5"))
 eng.kl_fields()
 eng.build_bases()
 torch.cuda.synchronize()
@@ -30,7 +35,7 @@ tot = v[1] + v[5] + v[2] + v[3] + v[4]
 for i, nme in names.items():
     print(f"{nme:22s} {v[i] / 1e6:10.3f} Mcycles  {100 * v[i] / tot:5.1f}%")
 h = plan.hyb[plan.darcy[0]]
-print("n", h.n, "w", h.w, "panels", (h.n + 15) // 16)
+print("n", h.n, "w", h.w, "panels", (h.n + 7) // 8)
 
 out = (ctypes.c_ulonglong * 16)()
 _lib.load().mfb_debug_bprof(out)
