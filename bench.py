@@ -341,16 +341,20 @@ def run_ours(a):
     roof = None
     if dom:
         t_ms, fl, sfl, cnt = kinds[dom]
-        achieved = fl / (t_ms / 1000.0) / 1e12
+        # achieved = SURVEY 8(d) algorithmic flops (F = 2 n w^2 + 4 n w N_dof of the banded
+        # mixed system) / kernel time; the flops the kernel actually executes are reported
+        # beside it (the hybrid condensation executes ~1/6 of the survey count)
+        achieved = sfl / (t_ms / 1000.0) / 1e12
         roof = {"kernel": {"band": "band_solve_kernel (Stokes: assembly + banded LU + multi-RHS)",
                            "hybrid": "condense_kernel (Darcy: SPD static condensation)"}[dom],
                 "bound": "fp64 (DMMA)", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
                 "peak_source": "profiles/fp64_peak.json (our DMMA microbenchmark; "
                                "MEASURED_PEAKS.json has no FP64 figure)",
-                "flops_per_launch": fl / cnt, "launch_ms": t_ms / cnt,
+                "algorithmic_flops_per_launch": sfl / cnt, "executed_flops_per_launch": fl / cnt, "launch_ms": t_ms / cnt,
                 "share_of_step": t_ms / tot_ms if tot_ms else None,
-                "survey_algorithmic_tflops": sfl / (t_ms / 1000.0) / 1e12,
+                "executed_tflops": fl / (t_ms / 1000.0) / 1e12,
+                "executed_frac": (fl / (t_ms / 1000.0) / 1e12) / peak if peak else None,
                 "traffic": None,
                 "per_kind_ms_per_step": {k: v[0] / len(dev_ms) for k, v in kinds.items()}}
     basis_ms = sum(v[0] for v in kinds.values()) / max(len(dev_ms), 1)

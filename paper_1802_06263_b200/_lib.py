@@ -61,6 +61,7 @@ _SIGS = {
     "mfb_selftest_dmma": ([_p, _p], _i),
     "mfb_debug_prof": ([_p], _i),
     "mfb_debug_bprof": ([_p], _i),
+    "mfb_debug_timeline": ([_p], _i),
     "mfb_darcy_condense": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p], _i),
     "mfb_darcy_backsolve": ([_p, _i, _p, _p, _p, _p, _p, _i, _i, _p], _i),
     "mfb_darcy_recover": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),

@@ -21,6 +21,16 @@
 
 #ifdef MFB_PROFILE
 __device__ unsigned long long g_bprof[16];
+__device__ unsigned long long g_tl[4][4096];     // system 0 timeline (globaltimer ns)
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(which, k)                                                              \
+    do {                                                                          \
+        if (s == 0 && threadIdx.x == 0 && (k) < 4096) g_tl[which][k] = gtime();   \
+    } while (0)
 #define BPROF(i)                                                                  \
     do {                                                                          \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
@@ -29,8 +39,24 @@ __device__ unsigned long long g_bprof[16];
             s_bt0 = _c;                                                           \
         }                                                                         \
     } while (0)
+#define FPROF(i)                                                                  \
+    do {                                                                          \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                \
+            long long _c = clock64();                                             \
+            if ((i) > 0) atomicAdd(&g_bprof[(i)], (unsigned long long)(_c - f_t0)); \
+            f_t0 = _c;                                                            \
+        }                                                                         \
+    } while (0)
 #else
 #define BPROF(i) do {} while (0)
+#define FPROF(i) do {} while (0)
+#define TL(which, k) do {} while (0)
+#endif
+#ifdef MFB_FTS
+__device__ long long g_fts[16 * 8];
+#define FTS(c, k) do { if (threadIdx.x == 0) s_fts[(c) * 8 + (k)] = clock64(); } while (0)
+#else
+#define FTS(c, k) do {} while (0)
 #endif
 
 namespace {
@@ -38,6 +64,7 @@ namespace {
 constexpr int MAX_NB = 8;
 constexpr int MAX_NCY = 160;
 constexpr int BAND_NB = 16;
+constexpr int BAND_GROUP_MAX = 16;   // CTAs per system; panel slots = group + 1 <= 17
 
 __device__ __forceinline__ long long bidx(int i, int k, int kl, int ku, int ldab) {
     return (long long)k * ldab + (kl + ku + i - k);
@@ -87,6 +114,247 @@ __device__ __forceinline__ void group_sync(unsigned int *ctr, int C, unsigned in
     }
 }
 
+__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Factor panel kp (columns kp*NB.., rows down to the band edge) with partial
+// pivoting, held in registers: thread t owns panel rows t, t+NT, .. (RPT of
+// them); only the warps holding rows take part (named barrier 1).
+//
+// FP64 ALU latency on sm_100 is ~90 cycles, so the column loop is built to
+// keep divisions off its dependency chain. Elimination is division-free
+// (scaled, Bareiss-like): with pivot P~ and pivot row u~ of step c,
+//     a~(i,j) <- sigma * (a~(i,j) * P~ - a~(i,c) * u~(j)),   sigma = 2^-e(P~),
+// so every remaining row carries the same scale S_c (S_{c+1} = sigma S_c P~,
+// 1 <= S grows < 2x per step); pivot choice is unchanged because all rows
+// share the scale. Afterwards L(i,c) = a~(i,c) / P~_c and U(c,j) = a~(c,j) / S_c
+// with 2*NB reciprocals computed once. Per column: warp argmax of a packed
+// (|a|, -row) key by redux, each warp posts its candidate row and the thread
+// holding row c posts that row (buffers alternate by column parity), one
+// barrier, tree max over the warps, swap, update.
+// The factors go to the band (the owner's own columns), to the publication
+// slot (L rows, ipiv, fail) and 1/U(c,c) to udinv; then `ready` is released
+// to kp+1. Returns 0, or j+1 for a zero pivot at band column j.
+template <int NT, int RPT>
+__device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int kl, int ku,
+                                           int ldab, int kp, double *__restrict__ slot,
+                                           double *__restrict__ udinv, unsigned int *ready,
+                                           double *s_cand, double *s_rowc, double *s_fin,
+                                           unsigned long long *red_k, int *s_fail) {
+    constexpr int NB = BAND_NB, NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int j0 = kp * NB, pnb = min(NB, n - j0);
+    const int nr = min(n, j0 + pnb + kl) - j0;
+    const int nwf = RPT == 1 ? (nr + 31) >> 5 : NW;
+    int fail = 0;
+    int piv[NB];
+    double a[RPT][NB];
+#ifdef MFB_PROFILE
+    long long f_t0 = 0;
+#endif
+    FPROF(0);
+    if (wid < nwf) {
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr) {
+            const int i = tid + rr * NT, r = j0 + i;
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+                const int col = j0 + c;
+                a[rr][c] = (i < nr && c < pnb && r - col <= kl && col - r <= kl + ku)
+                               ? __ldcg(AB + bidx(r, col, kl, ku, ldab)) : 0.0;
+            }
+        }
+        if (tid == 0) {
+            double t = 0;
+            for (int c = 0; c < NB; ++c) t += a[0][c];
+            if (t == 12345.678) piv[0] = 1;
+        }
+        FPROF(12);
+#ifdef MFB_FTS
+        __shared__ long long s_fts[16 * 8];
+#endif
+        double S = 1.0;                          // running row scale (thread 0)
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+            piv[c] = c;
+            if (c >= pnb) continue;
+            const int par = c & 1;
+            FTS(c, 0);
+            // key: |a(i,c)| bits (non-negative doubles order like their bit
+            // patterns; the low 10 mantissa bits give way to 1023 - i, so
+            // near-ties within 2^-42 go to the first row), 0 = no candidate
+            unsigned long long key = 0ull;
+#pragma unroll
+            for (int rr = 0; rr < RPT; ++rr) {
+                const int i = tid + rr * NT;
+                const unsigned long long k2 =
+                    ((unsigned long long)__double_as_longlong(a[rr][c]) & 0x7FFFFFFFFFFFFC00ull) |
+                    (unsigned long long)(1023 - i);
+                if (i >= c && i < nr && k2 > key) key = k2;
+            }
+            {   // warp max: redux on the high word, then on the low word among
+                // the lanes holding the high maximum
+                const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+                const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+                key = ((unsigned long long)mh << 32) | ml;
+            }
+            const int bi = 1023 - (int)(key & 1023ull);
+            FTS(c, 1);
+            double *cand = s_cand + (par * NW + wid) * NB;
+            double *rowc = s_rowc + par * NB;
+#pragma unroll
+            for (int rr = 0; rr < RPT; ++rr) {
+                const int i = tid + rr * NT;
+                if (key != 0ull && i == bi) {
+#pragma unroll
+                    for (int cc = 0; cc < NB; ++cc) cand[cc] = a[rr][cc];
+                }
+                if (i == c) {
+#pragma unroll
+                    for (int cc = 0; cc < NB; ++cc) rowc[cc] = a[rr][cc];
+                }
+            }
+            if (lane == 0) red_k[par * NW + wid] = key;
+            FTS(c, 2);
+            asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
+            unsigned long long kw[NW];
+#pragma unroll
+            for (int w = 0; w < NW; ++w) kw[w] = w < nwf ? red_k[par * NW + w] : 0ull;
+#pragma unroll
+            for (int h = 1; h < NW; h <<= 1)          // tree max
+#pragma unroll
+                for (int w = 0; w + h < NW; w += 2 * h) kw[w] = kw[w + h] > kw[w] ? kw[w + h] : kw[w];
+            const unsigned long long kb = kw[0];
+            FTS(c, 3);
+            if ((kb & ~1023ull) == 0ull) { fail = j0 + c + 1; break; }   // uniform over the warps
+            const int p = 1023 - (int)(kb & 1023ull);
+            piv[c] = p;
+            const int wb = (p & (NT - 1)) >> 5;
+            const double *prow = s_cand + (par * NW + wb) * NB;
+            const double P = prow[c];
+            // P' = sigma P~ in [1, 2) and sigma = 2^-e, from the bits (exact)
+            const long long pbits = __double_as_longlong(P);
+            const int ef = (int)((pbits >> 52) & 0x7ff);
+            const bool nrm = ef > 0 && ef < 0x7ff;
+            const double Pp = nrm ? __longlong_as_double((pbits & (long long)0x800FFFFFFFFFFFFFull) |
+                                                         0x3FF0000000000000ll) : P;
+            const double sg = nrm ? __longlong_as_double((long long)(2046 - ef) << 52) : 1.0;
+            FTS(c, 4);
+            if (tid == 0) {
+                s_fin[c] = P;
+                s_fin[NB + c] = S;
+                S = sg * S * P;
+            }
+#pragma unroll
+            for (int rr = 0; rr < RPT; ++rr) {
+                const int i = tid + rr * NT;
+                if (i == c) {                 // whole rows swap: L columns too (getf2)
+#pragma unroll
+                    for (int cc = 0; cc < NB; ++cc) a[rr][cc] = prow[cc];
+                } else if (i == p) {
+#pragma unroll
+                    for (int cc = 0; cc < NB; ++cc) a[rr][cc] = rowc[cc];
+                }
+                if (i > c && i < nr) {
+                    const double t = sg * a[rr][c];
+#pragma unroll
+                    for (int cc = c + 1; cc < NB; ++cc) a[rr][cc] = fma(-t, prow[cc], a[rr][cc] * Pp);
+                }
+            }
+            FTS(c, 5);
+        }
+#ifdef MFB_FTS
+        if (tid == 0) for (int q = 0; q < 16 * 8; ++q) g_fts[q] = s_fts[q];
+#endif
+        FPROF(13);
+        // 1/P~_c and 1/S_c once, then unscale: L = a~ / P~, U row c = a~ / S_c
+        asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
+        if (tid < 2 * NB && (tid & (NB - 1)) < pnb && !fail) s_fin[2 * NB + tid] = 1.0 / s_fin[tid];
+        asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
+        if (!fail) {
+#pragma unroll
+            for (int rr = 0; rr < RPT; ++rr) {
+                const int i = tid + rr * NT;
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    if (c < pnb && c < i) a[rr][c] *= s_fin[2 * NB + c];
+                    else if (i < pnb && c >= i) a[rr][c] *= s_fin[3 * NB + i];
+                }
+            }
+            if (tid < pnb) udinv[j0 + tid] = s_fin[NB + tid] * s_fin[2 * NB + tid];
+        }
+        // publish: L | U11 to the band (the owner's columns) and to the slot
+        // (rows x NB, zero past pnb), pivots and the failure flag after them
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr) {
+            const int i = tid + rr * NT, r = j0 + i;
+            if (i < nr) {
+#pragma unroll
+                for (int c = 0; c < NB; c += 2)
+                    reinterpret_cast<double2 *>(slot + i * NB)[c >> 1] = make_double2(a[rr][c], a[rr][c + 1]);
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    const int col = j0 + c;
+                    if (c < pnb && r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = a[rr][c];
+                }
+            }
+        }
+        // row moves for the consumers, from the pivots (every thread holds
+        // them): final top row q came from the row found by undoing the swaps;
+        // each distinct pivot row below the panel receives a top row
+        if (wid == 0) {
+            int *si = reinterpret_cast<int *>(slot + (long long)(kl + NB) * NB);
+            const int q = lane & (NB - 1);
+            int x = q;
+#pragma unroll
+            for (int c = NB - 1; c >= 0; --c)
+                if (c < pnb) x = (x == c) ? piv[c] : (x == piv[c] ? c : x);
+            int pz = 0;
+            bool lowv = false;
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c == q) { pz = piv[c]; lowv = c < pnb && piv[c] >= pnb; }
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c < q && piv[c] == pz) lowv = false;
+            int y = pz;
+#pragma unroll
+            for (int c = NB - 1; c >= 0; --c)
+                if (c < pnb) y = (y == c) ? piv[c] : (y == piv[c] ? c : y);
+            const unsigned m = __ballot_sync(0xffffffffu, lane < NB && lowv);
+            const int pos = __popc(m & ((1u << q) - 1u));
+            if (lane < NB) {
+                si[lane] = x;
+                if (lowv) {
+                    si[NB + pos] = pz;
+                    si[2 * NB + pos] = y;
+                }
+            }
+            if (lane == 0) {
+                si[3 * NB] = __popc(m);
+                si[3 * NB + 1] = fail;
+                *s_fail = fail;
+            }
+        }
+    }
+    __syncthreads();
+    FPROF(14);
+    if (tid == 0) {
+        __threadfence();
+        st_release(ready, (unsigned int)(kp + 1));
+    }
+    FPROF(15);
+    return *s_fail;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT)
 band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ sys_pat,
@@ -98,13 +366,13 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     constexpr int PST = NB + 1;          // odd stride: lane-varying rows hit distinct banks
     constexpr int NW = NT / 32;
     extern __shared__ double smem[];
-    __shared__ double red_v[NW];
-    __shared__ int red_i[NW];
-    __shared__ int s_ipiv[NB];
-    __shared__ int s_low[NB];
+    __shared__ int s_tsrc[NB], s_ldst[NB], s_lsrc[NB];
     __shared__ int s_nlow;
     __shared__ double s_u11[NB * NB];
     __shared__ int s_flag;
+    __shared__ double s_cand[2 * NW * NB], s_rowc[2 * NB], s_fin[4 * NB];
+    __shared__ unsigned long long s_fred_k[2 * NW];
+    __shared__ int s_ffail;
 #ifdef MFB_PROFILE
     __shared__ long long s_bt0;
 #endif
@@ -119,7 +387,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     const int n = P.n, kl = P.kl, ku = P.ku, ldab = P.ldab, nb = P.nb;
     const int nrhs = P.ndof + 1;
     const int ncy = nrhs;              // rhs block: N_dof mortar columns + bar
-    const int UST = kl + ku + 8;
+    const int UST = (kl + ku + 16) | 1;  // odd: the 16 staged rows hit distinct banks
     double *AB = work + sys_woff[s];
     double *Y = AB + (long long)ldab * n;
     double *Pnl = smem;                          // (kl + NB) x PST   panel L | U11
@@ -127,8 +395,11 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     double *Tmp = U12s + NB * UST;               // NB x UST          staged A12
     const int TMPN = max(NB * UST, 3 * MAX_NB * MAX_NCY);   // also kernel-projection scratch
     double *Ytop = Tmp + TMPN;                   // NB x ncy          rhs rows of the panel
-    int *s_perm = reinterpret_cast<int *>(Ytop + NB * ncy);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (kl + NB > 2 * NT) {                   // panel rows exceed two per thread
+        if (tid == 0 && rank == 0) info[s] = -2;
+        return;
+    }
 
     // ---- 1. assembly ---------------------------------------------------
     const long long nab = (long long)ldab * n, ny = (long long)n * ncy;
@@ -216,170 +487,202 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             Y[(long long)i * ncy + c] = v;
         }
     }
-    if (tid == 0) s_flag = 0;
-    __syncthreads();
-    // ---- 2. blocked banded LU with partial pivoting (gbtrf) --------------
-    for (int j0 = 0; j0 < n; j0 += NB) {
+    // ---- 2. banded LU with partial pivoting (gbtrf), look-ahead over the group
+    // Column block b (NB columns) belongs to rank b % C, which applies every
+    // panel's row swaps and updates to it. The owner of block k+1 updates that
+    // block first when panel k arrives, factors panel k+1 and publishes it
+    // (slot (k+1) % D + release of `ready`), and only then updates the rest of
+    // its columns, so the panel chain does not wait for the trailing updates.
+    // D = C + 1 slots suffice: a rank loads panel k before it can publish any
+    // later panel, and the owners of panels k+1..k+C cover every rank.
+    const int nblk = (n + NB - 1) / NB;
+    const int D = C + 1, D_MAX = BAND_GROUP_MAX + 1;
+    const long long SLOT = (long long)(kl + NB) * NB + 32;   // factors + 64 ints of row moves
+    double *slots = Y + ny + ((ldab * (long long)n + ny) & 1);   // 16-byte aligned (double2 stores)
+    double *udinv = slots + D_MAX * SLOT;          // 1 / U(j, j), written by the panel owners
+    unsigned int *ready = bar + gridDim.x / C + s;
+    const int NTF = kl + NB <= NT ? 1 : 2;
+    auto factor = [&](int kp) -> int {
+        double *slot = slots + (kp % D) * SLOT;
+        return NTF == 1 ? factor_publish<NT, 1>(AB, n, kl, ku, ldab, kp, slot, udinv, ready,
+                                                s_cand, s_rowc, s_fin, s_fred_k, &s_ffail)
+                        : factor_publish<NT, 2>(AB, n, kl, ku, ldab, kp, slot, udinv, ready,
+                                                s_cand, s_rowc, s_fin, s_fred_k, &s_ffail);
+    };
+#define OWNB(b) (((b) % C) == rank)
+    if (rank == 0) {
+        const int f = factor(0);
+        if (f) {
+            if (tid == 0) info[s] = f;
+            return;
+        }
+    }
+    for (int k = 0; k < nblk; ++k) {
         BPROF(0);
+        const int j0 = k * NB;
         const int pnb = min(NB, n - j0);
         const int r1 = min(n, j0 + pnb + kl);
         const int nr = r1 - j0;
         const int c0 = j0 + pnb;
         const int c1 = min(n, j0 + pnb + kl + ku);
-        const int nc = max(0, c1 - c0);
-        // panel columns j0..j0+pnb of rows j0..r1 (zero beyond the band / pnb)
-        for (int t = tid; t < nr * NB; t += NT) {
-            const int i = t % nr, c = t / nr;
-            const int r = j0 + i, col = j0 + c;
-            Pnl[i * PST + c] = (c < pnb && r - col <= kl && col - r <= kl + ku)
-                                   ? __ldcg(AB + bidx(r, col, kl, ku, ldab)) : 0.0;
+        if (k + 1 < nblk && OWNB(k + 1)) TL(3, k);
+        if (tid == 0)
+            while (ld_acquire(ready) < (unsigned int)(k + 1)) {}
+        __syncthreads();
+        const double *slot = slots + (k % D) * SLOT;
+        const int *si = reinterpret_cast<const int *>(slot + (long long)(kl + NB) * NB);
+        for (int t = tid; t < nr * NB; t += NT) Pnl[(t >> 4) * PST + (t & (NB - 1))] = __ldcg(slot + t);
+        // row moves of the panel's swaps: top row q <- row s_tsrc[q]; moved
+        // lower rows s_ldst[z] <- s_lsrc[z], z < nlow (local panel rows)
+        if (tid < NB) {
+            s_tsrc[tid] = __ldcg(si + tid);
+            s_ldst[tid] = __ldcg(si + NB + tid);
+            s_lsrc[tid] = __ldcg(si + 2 * NB + tid);
         }
-        // every CTA must hold the panel before rank 0 writes its factors back
-        group_sync(ctr, C, bar_target);
+        if (tid == 0) {
+            s_nlow = __ldcg(si + 3 * NB);
+            s_flag = __ldcg(si + 3 * NB + 1);
+        }
+        __syncthreads();
+        if (s_flag) return;                  // the panel's owner set info[s]
         BPROF(1);
-        if (tid < 128) {
-            // panel LU with partial pivoting on 4 warps (named barrier 2); the
-            // pivot candidate of column c+1 is found while column c is applied
-            const int pw = tid >> 5;
-            double best = -1.0;
-            int bi = 0;
-            for (int i = tid; i < nr; i += 128) {
-                const double a = fabs(Pnl[i * PST]);
-                if (a > best) { best = a; bi = i; }
+        const int nlow = s_nlow;
+
+        // swaps + U12 + trailing update of the owned blocks in [blo, bhi]
+        auto update_blocks = [&](int blo, int bhi) {
+            if (blo > bhi) return;
+            const int bf0 = blo + ((rank - blo) % C + C) % C;
+            if (bf0 > bhi) return;
+            const int nob = (bhi - bf0) / C + 1;
+            const int nel = nob * NB * NB;
+            // stage the permuted top rows (Tmp) and the moved lower rows (U12s)
+            for (int t = tid; t < nel; t += NT) {
+                const int q = t & (NB - 1), c16 = (t >> 4) & (NB - 1), ob = t >> 8;
+                const int col = (bf0 + ob * C) * NB + c16, cc = col - c0;
+                const int src = j0 + (q < pnb ? s_tsrc[q] : 0);
+                const bool vt = q < pnb && col < c1 && col - src <= kl + ku && src - col <= kl;
+                const int srl = j0 + (q < nlow ? s_lsrc[q] : 0);
+                const bool vl = q < nlow && col < c1 && col - srl <= kl + ku && srl - col <= kl;
+                const double x = vt ? AB[bidx(src, col, kl, ku, ldab)] : 0.0;
+                const double y = vl ? AB[bidx(srl, col, kl, ku, ldab)] : 0.0;
+                Tmp[q * UST + cc] = x;
+                U12s[q * UST + cc] = y;
             }
-            for (int c = 0; c < pnb; ++c) {
+            __syncthreads();
+            BPROF(8);
+            for (int t = tid; t < nel; t += NT) {
+                const int z = t & (NB - 1), c16 = (t >> 4) & (NB - 1), ob = t >> 8;
+                if (z >= nlow) continue;
+                const int col = (bf0 + ob * C) * NB + c16, cc = col - c0;
+                const int row = j0 + s_ldst[z];
+                if (col < c1 && row - col <= kl) AB[bidx(row, col, kl, ku, ldab)] = U12s[z * UST + cc];
+            }
+            __syncthreads();
+            BPROF(9);
+            // U12 = L11^-1 A12 by forward substitution (thread per column)
+            for (int u = tid; u < nob * NB; u += NT) {
+                const int col = (bf0 + (u >> 4) * C) * NB + (u & (NB - 1)), cc = col - c0;
+                double uu[NB];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double ov = __shfl_down_sync(0xffffffffu, best, o);
-                    const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-                    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-                }
-                if (lane == 0) { red_v[pw] = best; red_i[pw] = bi; }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-                double bv = red_v[0];
-                int p = red_i[0];
+                for (int q = 0; q < NB; ++q) uu[q] = Tmp[q * UST + cc];
+                // column-oriented (axpy) order: dependent chain NB deep, not NB^2/2
 #pragma unroll
-                for (int w = 1; w < 4; ++w)
-                    if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < p)) { bv = red_v[w]; p = red_i[w]; }
-                if (!(bv > 0.0)) {
-                    if (tid == 0) { if (rank == 0) info[s] = j0 + c + 1; s_flag = -1; }
-                    break;
+                for (int qq = 0; qq < NB - 1; ++qq)
+#pragma unroll
+                    for (int q = qq + 1; q < NB; ++q) uu[q] -= Pnl[q * PST + qq] * uu[qq];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) uu[q] = q < pnb ? uu[q] : 0.0;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    U12s[q * UST + cc] = q < pnb ? uu[q] : 0.0;
+                    const int row = j0 + q;
+                    if (q < pnb && col < c1 && col - row <= kl + ku) AB[bidx(row, col, kl, ku, ldab)] = uu[q];
                 }
-                if (tid == 0) s_ipiv[c] = p;
-                if (p != c && tid < NB) {
-                    const double t0 = Pnl[c * PST + tid];
-                    Pnl[c * PST + tid] = Pnl[p * PST + tid];
-                    Pnl[p * PST + tid] = t0;
+            }
+            __syncthreads();
+            BPROF(10);
+            // A22 -= L21 U12 on FP64 tensor cores (DMMA 8x8x4); work item =
+            // (8-column tile, group of four 8-row tiles), U12 fragments in registers
+            const int mrows = nr - pnb;
+            const int tr = (mrows + 7) >> 3, nrg = (tr + 3) >> 2, ntc = 2 * nob;
+            const int g = lane >> 2, q4 = lane & 3;
+            for (int it = wid; it < ntc * nrg; it += NW) {
+                const int rg = it / ntc, ot = it - rg * ntc;
+                const int col8 = (bf0 + (ot >> 1) * C) * NB + (ot & 1) * 8;
+                const int cct = col8 - c0;
+                double bf[NB / 4];
+#pragma unroll
+                for (int kk = 0; kk < NB / 4; ++kk) bf[kk] = U12s[(4 * kk + q4) * UST + cct + g];
+                const int ca = col8 + 2 * q4, cb = ca + 1;
+                double *pa = AB + (long long)ca * ldab + (kl + ku - ca);
+                double *pb = pa + (ldab - 1);
+                const int lima = ca < c1 ? min(r1, ca + kl + 1) : 0;
+                const int limb = cb < c1 ? min(r1, cb + kl + 1) : 0;
+                const int rbase = j0 + pnb + g;
+                const int tg = rg * 4;
+                double d0[4], d1[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int row = rbase + (tg + h) * 8;
+                    d0[h] = row < lima ? pa[row] : 0.0;
+                    d1[h] = row < limb ? pb[row] : 0.0;
                 }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-                const double inv = 1.0 / Pnl[c * PST + c];
-                best = -1.0;
-                bi = c + 1;
-                for (int i = c + 1 + tid; i < nr; i += 128) {
-                    const double l = Pnl[i * PST + c] * inv;
-                    Pnl[i * PST + c] = l;
-                    for (int cc = c + 1; cc < pnb; ++cc) Pnl[i * PST + cc] -= l * Pnl[c * PST + cc];
-                    if (c + 1 < pnb) {
-                        const double a = fabs(Pnl[i * PST + c + 1]);
-                        if (a > best) { best = a; bi = i; }
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int prow = pnb + (tg + h) * 8 + g;
+                    const bool ra = prow < nr;
+#pragma unroll
+                    for (int kk = 0; kk < NB / 4; ++kk) {
+                        const double a = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
+                        dmma884(d0[h], d1[h], a, bf[kk]);
                     }
                 }
-            }
-        }
-        __syncthreads();
-        BPROF(2);
-        if (s_flag < 0) return;
-        // net row permutation of the panel's swaps
-        if (tid == 0) {
-            for (int i = 0; i < nr; ++i) s_perm[i] = i;
-            int nl = 0;
-            for (int q = 0; q < pnb; ++q) {
-                const int p = s_ipiv[q];
-                const int t0 = s_perm[q];
-                s_perm[q] = s_perm[p];
-                s_perm[p] = t0;
-                if (p >= pnb) {
-                    bool seen = false;
-                    for (int z = 0; z < nl; ++z) seen |= (s_low[z] == p);
-                    if (!seen) s_low[nl++] = p;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int row = rbase + (tg + h) * 8;
+                    if (row < lima) pa[row] = d0[h];
+                    if (row < limb) pb[row] = d1[h];
                 }
             }
-            s_nlow = nl;
-        }
-        __syncthreads();
-        BPROF(3);
-        if (rank == 0)
-            for (int t = tid; t < nr * pnb; t += NT) {
-                const int i = t % nr, c = t / nr;
-                const int r = j0 + i, col = j0 + c;
-                if (r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = Pnl[i * PST + c];
+            __syncthreads();
+            BPROF(11);
+        };
+
+        const int bend = c1 > c0 ? (c1 - 1) / NB : k;
+        if (k + 1 < nblk && OWNB(k + 1)) {
+            TL(0, k);
+            update_blocks(k + 1, k + 1);
+            TL(1, k);
+            BPROF(2);
+            const int f = factor(k + 1);
+            TL(2, k);
+            if (f) {
+                if (tid == 0) info[s] = f;
+                return;
             }
-        // phase A: stage the permuted top rows of every trailing column (Tmp)
-        // and the moved lower rows (U12s used as staging); all reads first
-        const int nlow = s_nlow;
-        const int ncpad = (nc + 7) & ~7;
-        for (int t = tid; t < NB * ncpad; t += NT) {
-            const int q = t / ncpad, cc = t % ncpad, col = c0 + cc;
-            if (!OWN((c0 >> 3) + (cc >> 3))) continue;
-            const int src = j0 + (q < pnb ? s_perm[q] : 0);
-            const bool vt = q < pnb && cc < nc && col - src <= kl + ku && src - col <= kl;
-            const int srl = j0 + (q < nlow ? s_perm[s_low[q]] : 0);
-            const bool vl = q < nlow && cc < nc && col - srl <= kl + ku && srl - col <= kl;
-            const double x = __ldcg(AB + (vt ? bidx(src, col, kl, ku, ldab) : 0));
-            const double y = __ldcg(AB + (vl ? bidx(srl, col, kl, ku, ldab) : 0));
-            Tmp[q * UST + cc] = vt ? x : 0.0;
-            U12s[q * UST + cc] = vl ? y : 0.0;
+            BPROF(3);
+            update_blocks(k + 2, bend);
+        } else {
+            update_blocks(k + 1, bend);
         }
-        __syncthreads();
-        for (int t = tid; t < nlow * nc; t += NT) {
-            const int z = t / nc, cc = t % nc, col = c0 + cc;
-            if (!OWN((c0 >> 3) + (cc >> 3))) continue;
-            const int row = j0 + s_low[z];
-            if (row - col <= kl) AB[bidx(row, col, kl, ku, ldab)] = U12s[z * UST + cc];
-        }
-        __syncthreads();
-        // U12 = L11^-1 A12 by forward substitution (thread per column, as gbtrf's
-        // dtrsm): written to the band (top rows) and to U12s
-        for (int cc = tid; cc < ncpad; cc += NT) {
-            if (!OWN((c0 >> 3) + (cc >> 3))) continue;
-            double u[NB];
-#pragma unroll
-            for (int q = 0; q < NB; ++q) u[q] = Tmp[q * UST + cc];
-#pragma unroll
-            for (int q = 1; q < NB; ++q) {
-                double v = u[q];
-#pragma unroll
-                for (int qq = 0; qq < q; ++qq) v -= Pnl[q * PST + qq] * u[qq];
-                u[q] = q < pnb ? v : 0.0;
-            }
-            const int col = c0 + cc;
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                U12s[q * UST + cc] = q < pnb ? u[q] : 0.0;
-                const int row = j0 + q;
-                if (q < pnb && cc < nc && col - row <= kl + ku) AB[bidx(row, col, kl, ku, ldab)] = u[q];
-            }
-        }
-        // phase A': right-hand sides -- permute + forward substitution (thread per column)
+        BPROF(4);
+        // right-hand sides: permute + forward substitution (thread per column)
         for (int cy = tid; cy < ncy; cy += NT) {
             if (!OWN(cy >> 3)) continue;
             double u[NB], low[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q)
-                u[q] = q < pnb ? Y[(long long)(j0 + s_perm[q]) * ncy + cy] : 0.0;
+                u[q] = q < pnb ? Y[(long long)(j0 + s_tsrc[q]) * ncy + cy] : 0.0;
 #pragma unroll
             for (int z = 0; z < NB; ++z)
-                low[z] = z < nlow ? Y[(long long)(j0 + s_perm[s_low[z]]) * ncy + cy] : 0.0;
+                low[z] = z < nlow ? Y[(long long)(j0 + s_lsrc[z]) * ncy + cy] : 0.0;
 #pragma unroll
             for (int z = 0; z < NB; ++z)
-                if (z < nlow) Y[(long long)(j0 + s_low[z]) * ncy + cy] = low[z];
+                if (z < nlow) Y[(long long)(j0 + s_ldst[z]) * ncy + cy] = low[z];
 #pragma unroll
-            for (int q = 1; q < NB; ++q) {
-                double v = u[q];
+            for (int qq = 0; qq < NB - 1; ++qq)
 #pragma unroll
-                for (int qq = 0; qq < q; ++qq) v -= Pnl[q * PST + qq] * u[qq];
-                u[q] = v;
-            }
+                for (int q = qq + 1; q < NB; ++q) u[q] -= Pnl[q * PST + qq] * u[qq];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
                 if (q < pnb) Y[(long long)(j0 + q) * ncy + cy] = u[q];
@@ -387,57 +690,8 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             }
         }
         __syncthreads();
-        // phase B: A22 -= L21 U12 on FP64 tensor cores (DMMA 8x8x4 tiles).
-        // A warp owns a column tile: its U12 fragments stay in registers while
-        // it walks down the row tiles, four tiles in flight at a time.
-        {
-            const int mrows = nr - pnb;
-            const int tr = (mrows + 7) >> 3, tcn = ncpad >> 3;
-            const int g = lane >> 2, q4 = lane & 3;
-            // absolute tile ownership: a column keeps its owner across panels,
-            // so its (L1-cached) reads only ever see the owner's own writes
-            const int tbase = c0 >> 3;
-            const int tj0 = ((rank - tbase) % C + C) % C;
-            for (int tj = tj0 + C * wid; tj < tcn; tj += C * NW) {
-                double bf[NB / 4];
-#pragma unroll
-                for (int kk = 0; kk < NB / 4; ++kk) bf[kk] = U12s[(4 * kk + q4) * UST + tj * 8 + g];
-                const int ca = c0 + tj * 8 + 2 * q4, cb = ca + 1;
-                // band column pointers: element (row, col) = colp[row]
-                double *pa = AB + (long long)ca * ldab + (kl + ku - ca);
-                double *pb = pa + (ldab - 1);
-                const int lima = ca < c1 ? min(r1, ca + kl + 1) : 0;
-                const int limb = cb < c1 ? min(r1, cb + kl + 1) : 0;
-                const int rbase = j0 + pnb + g;
-                for (int tg = 0; tg < tr; tg += 4) {
-                    double d0[4], d1[4];
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const int row = rbase + (tg + h) * 8;
-                        d0[h] = row < lima ? pa[row] : 0.0;
-                        d1[h] = row < limb ? pb[row] : 0.0;
-                    }
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const int prow = pnb + (tg + h) * 8 + g;
-                        const bool ra = prow < nr;
-#pragma unroll
-                        for (int kk = 0; kk < NB / 4; ++kk) {
-                            const double a = ra ? -Pnl[prow * PST + 4 * kk + q4] : 0.0;
-                            dmma884(d0[h], d1[h], a, bf[kk]);
-                        }
-                    }
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const int row = rbase + (tg + h) * 8;
-                        if (row < lima) pa[row] = d0[h];
-                        if (row < limb) pb[row] = d1[h];
-                    }
-                }
-            }
-        }
-        // phase B': rhs rows below the panel, Y -= L21 Ytop (DMMA tiles; a warp
-        // owns a row tile and keeps its L21 fragments in registers)
+        // rhs rows below the panel, Y -= L21 Ytop (DMMA tiles; a warp owns a
+        // row tile and keeps its L21 fragments in registers)
         {
             const int mrows = nr - pnb;
             const int tr = (mrows + 7) >> 3, tcy = (ncy + 7) >> 3;
@@ -464,9 +718,13 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 }
             }
         }
-        group_sync(ctr, C, bar_target);
+        __syncthreads();
         BPROF(5);
     }
+#undef OWNB
+    // every rank's factors and rhs updates in place before the back substitution
+    group_sync(ctr, C, bar_target);
+
 
     // ---- 3. blocked column-oriented back substitution with U ---------------
     const int last = ((n - 1) / NB) * NB;
@@ -474,7 +732,8 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         const int pnb = min(NB, n - j0);
         for (int t = tid; t < NB * NB; t += NT) {
             const int r = t / NB, c = t % NB;
-            s_u11[t] = (r < pnb && c < pnb && c >= r) ? __ldcg(AB + bidx(j0 + r, j0 + c, kl, ku, ldab)) : 0.0;
+            s_u11[t] = (r < pnb && c < pnb && c > r) ? __ldcg(AB + bidx(j0 + r, j0 + c, kl, ku, ldab))
+                       : (r < pnb && c == r) ? __ldcg(udinv + j0 + r) : 0.0;   // diagonal: 1/U(r,r)
         }
         __syncthreads();
         for (int cy = tid; cy < ncy; cy += NT) {
@@ -486,7 +745,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 double v = Y[(long long)(j0 + r) * ncy + cy];
 #pragma unroll
                 for (int rr = r + 1; rr < NB; ++rr) v -= s_u11[r * NB + rr] * x[rr];
-                x[r] = v / s_u11[r * NB + r];
+                x[r] = v * s_u11[r * NB + r];
             }
 #pragma unroll
             for (int r = 0; r < NB; ++r) {
@@ -623,14 +882,15 @@ static int launch_band(int n_sys, int C, size_t smem, cudaStream_t st, const Mfb
     if (cudaFuncSetAttribute(band_solve_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return MFB_ERR_SMEM;
+    // bar: n_sys group-barrier counters, then n_sys panel-ready counters
+    if (cudaMemsetAsync(bar, 0, sizeof(unsigned int) * 2 * n_sys, st) != cudaSuccess)
+        return MFB_ERR_LAUNCH;
     if (C == 1) {
         band_solve_kernel<NT><<<n_sys, NT, smem, st>>>(pats, sys_pat, Kbuf, sys_koff, work,
                                                        sys_woff, X, sys_xoff, info, C, bar);
     } else {
         // the C CTAs of a system wait on one another: cooperative launch
         // guarantees they are co-resident
-        if (cudaMemsetAsync(bar, 0, sizeof(unsigned int) * n_sys, st) != cudaSuccess)
-            return MFB_ERR_LAUNCH;
         void *args[] = {(void *)&pats, (void *)&sys_pat, (void *)&Kbuf, (void *)&sys_koff,
                         (void *)&work, (void *)&sys_woff, (void *)&X, (void *)&sys_xoff,
                         (void *)&info, (void *)&C, (void *)&bar};
@@ -648,7 +908,7 @@ extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *s
                                  const long long *sys_xoff, int *info, int threads,
                                  int smem_doubles, int group, unsigned int *bar, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
-    if (group < 1 || (group > 1 && bar == nullptr)) return MFB_ERR_ARG;
+    if (group < 1 || group > BAND_GROUP_MAX || bar == nullptr) return MFB_ERR_ARG;
     const size_t smem = (size_t)smem_doubles * sizeof(double);
     cudaStream_t st = mfb_stream(stream);
     switch (threads) {
@@ -660,6 +920,15 @@ extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *s
                                           work, sys_woff, X, sys_xoff, info, bar);
         default: return MFB_ERR_ARG;
     }
+}
+
+extern "C" int mfb_debug_timeline(unsigned long long *out) {
+#ifdef MFB_PROFILE
+    return cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * 4 * 4096) == cudaSuccess ? 0 : 2;
+#else
+    (void)out;
+    return 1;
+#endif
 }
 
 extern "C" int mfb_debug_bprof(unsigned long long *out) {

@@ -84,7 +84,12 @@ class Pattern:
 
     @property
     def work_doubles(self):
-        return self.ldab * self.n + self.n * (self.ndof + 1)
+        # band, rhs rows, BAND_GROUP_MAX + 1 panel-publication slots ((kl + 16)
+        # x 16 factors + 32 doubles of row moves/flag), then n reciprocal U
+        # diagonals (mfb_band.cu)
+        w = (self.ldab * self.n + self.n * (self.ndof + 1) + 1
+             + 17 * ((self.kl + 16) * 16 + 32) + self.n)
+        return w + (w & 1)                 # even: every system's slots stay 16-byte aligned
 
     @property
     def x_doubles(self):
@@ -98,11 +103,12 @@ class Pattern:
 
     @property
     def smem_doubles(self):
-        # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 + staging 2 x 16 x (kl + ku + 8),
-        # rhs rows 16 x (nb + ndof + 1), (kl + 16) ints of row permutation
-        return ((self.kl + 16) * 17 + 16 * (self.kl + self.ku + 8)
-                + max(16 * (self.kl + self.ku + 8), 3 * 8 * 160)
-                + 16 * (self.ndof + 1) + (self.kl + 16) // 2 + 1)
+        # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 + staging 2 x 16 x ust,
+        # rhs rows 16 x (ndof + 1)
+        ust = (self.kl + self.ku + 16) | 1
+        return ((self.kl + 16) * 17 + 16 * ust
+                + max(16 * ust, 3 * 8 * 160)
+                + 16 * (self.ndof + 1))
 
 
 class _TermTable:

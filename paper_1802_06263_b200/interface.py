@@ -191,7 +191,11 @@ class _S3Static:
                 pos += 1
             woff = np.concatenate([[0], np.cumsum([work_d[i] for i in grp])])
             xoff = np.concatenate([[0], np.cumsum([x_d[i] for i in grp])])
-            nt = 512 if max(pats[systems[i][0]].kl for i in grp) > 128 else 256
+            klmax = max(pats[systems[i][0]].kl for i in grp)
+            nt = 512 if klmax > 128 else 256
+            if klmax + 16 > 2 * nt:
+                raise SizeCapError(f"band half-width {klmax} exceeds the panel kernel's "
+                                   f"{2 * nt - 16} (two panel rows per thread)")
             w = sub(grp)
             w["info"] = torch.zeros(len(grp), dtype=i32, device="cuda")
             # CTAs per system: fill the SMs when systems are few (one CTA per SM
@@ -233,7 +237,8 @@ class _S3Static:
                 self.hwaves.append(w)
                 lmax, hxmax = max(lmax, int(loff[-1])), max(hxmax, int(hxoff[-1]))
         self.work = torch.empty(max(wmax, 1), dtype=f64, device="cuda")
-        self.bar = torch.zeros(max(len(systems), 1), dtype=torch.int32, device="cuda")
+        # per system: group-barrier counter and panel-ready counter (mfb_band.cu)
+        self.bar = torch.zeros(2 * max(len(systems), 1), dtype=torch.int32, device="cuda")
         self.X = torch.empty(max(xmax, 1), dtype=f64, device="cuda")
         self.Lstore = torch.empty(max(lmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
         self.HX = torch.empty(max(hxmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
