@@ -133,7 +133,7 @@ int mfb_kl_realize(const double *phi, const double *mean, int n_cells, int n_ter
  * sys_woff[s] holds ldab*n band + n*(nb+ndof+1) doubles; the solution
  * X (n+nb rows x ndof+1 columns, row-major) goes to X + sys_xoff[s].
  * info[s]: 0 ok, j+1 zero pivot at band column j, -1 singular border.
- * threads: 128/256/512 per CTA; smem_doubles: Pattern.smem_doubles of
+ * threads: 256 or 384 per CTA (panel rows <= 2 x threads); smem_doubles: Pattern.smem_doubles of
  * the widest pattern. group: CTAs per system (>1: cooperative launch of
  * n_sys*group CTAs that split the trailing and rhs columns; `bar` is a
  * device scratch of n_sys counters, zeroed by the call).

@@ -54,7 +54,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 #ifdef MFB_FTS
 __device__ long long g_fts[16 * 8];
-#define FTS(c, k) do { if (threadIdx.x == 0) s_fts[(c) * 8 + (k)] = clock64(); } while (0)
+__device__ long long g_fts2[16 * 16 * 8];
+#define FTS(c, k) do { if (threadIdx.x == 0) s_fts[(c) * 8 + (k)] = clock64(); \
+    if ((threadIdx.x & 31) == 0) s_fts2[((threadIdx.x >> 5) * 16 + (c)) * 8 + (k)] = clock64(); } while (0)
 #else
 #define FTS(c, k) do {} while (0)
 #endif
@@ -128,25 +130,30 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
 // pivoting, held in registers: thread t owns panel rows t, t+NT, .. (RPT of
 // them); only the warps holding rows take part (named barrier 1).
 //
-// FP64 ALU latency on sm_100 is ~90 cycles, so the column loop is built to
-// keep divisions off its dependency chain. Elimination is division-free
-// (scaled, Bareiss-like): with pivot P~ and pivot row u~ of step c,
-//     a~(i,j) <- sigma * (a~(i,j) * P~ - a~(i,c) * u~(j)),   sigma = 2^-e(P~),
-// so every remaining row carries the same scale S_c (S_{c+1} = sigma S_c P~,
-// 1 <= S grows < 2x per step); pivot choice is unchanged because all rows
-// share the scale. Afterwards L(i,c) = a~(i,c) / P~_c and U(c,j) = a~(c,j) / S_c
-// with 2*NB reciprocals computed once. Per column: warp argmax of a packed
-// (|a|, -row) key by redux, each warp posts its candidate row and the thread
-// holding row c posts that row (buffers alternate by column parity), one
-// barrier, tree max over the warps, swap, update.
+// FP64 ALU latency on sm_100 is ~90 cycles, so the column loop keeps
+// divisions and data movement off its dependency chain:
+//  * rows never move: each row carries its logical position `pos`; a pivot
+//    step only exchanges the positions of the pivot row and of the row at
+//    position c (getf2's swap), and rows are written out by position;
+//  * elimination is division-free (scaled, Bareiss-like): with pivot P~ and
+//    pivot row u~ of step c,  a~(i,j) <- sigma (a~(i,j) P~ - a~(i,c) u~(j)),
+//    sigma = 2^-e(P~) exact, so all active rows share one scale S_c
+//    (S_{c+1} = sigma S_c P~, 1 <= S < 2^NB) and the pivot choice is that of
+//    the unscaled matrix; afterwards L(i,c) = a~(i,c)/P~_c, U(c,j) = a~(c,j)/S_c
+//    with 2*NB reciprocals computed once;
+//  * argmax key = |a| bits with the low mantissa bits replaced by
+//    (1023 - pos, warp): one warp redux pair, one barrier, a tree max over
+//    the warps' posted keys (ties within 2^-38 go to the first position, as
+//    idamax's first index); each warp posts its candidate row.
 // The factors go to the band (the owner's own columns), to the publication
-// slot (L rows, ipiv, fail) and 1/U(c,c) to udinv; then `ready` is released
-// to kp+1. Returns 0, or j+1 for a zero pivot at band column j.
+// slot (L rows by position, row moves, fail) and 1/U(c,c) to udinv; then
+// `ready` is released to kp+1. Returns 0, or j+1 for a zero pivot at band
+// column j.
 template <int NT, int RPT>
 __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int kl, int ku,
                                            int ldab, int kp, double *__restrict__ slot,
                                            double *__restrict__ udinv, unsigned int *ready,
-                                           double *s_cand, double *s_rowc, double *s_fin,
+                                           double *s_cand, double *s_fin,
                                            unsigned long long *red_k, int *s_fail) {
     constexpr int NB = BAND_NB, NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -154,8 +161,9 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
     const int nr = min(n, j0 + pnb + kl) - j0;
     const int nwf = RPT == 1 ? (nr + 31) >> 5 : NW;
     int fail = 0;
-    int piv[NB];
     double a[RPT][NB];
+    int pos[RPT];
+    int *spiv = reinterpret_cast<int *>(slot + (long long)(kl + NB) * NB + 2 * NB);
 #ifdef MFB_PROFILE
     long long f_t0 = 0;
 #endif
@@ -164,6 +172,7 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
 #pragma unroll
         for (int rr = 0; rr < RPT; ++rr) {
             const int i = tid + rr * NT, r = j0 + i;
+            pos[rr] = i < nr ? i : 0x3ff;         // 0x3ff: no row
 #pragma unroll
             for (int c = 0; c < NB; ++c) {
                 const int col = j0 + c;
@@ -171,74 +180,65 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
                                ? __ldcg(AB + bidx(r, col, kl, ku, ldab)) : 0.0;
             }
         }
-        if (tid == 0) {
-            double t = 0;
-            for (int c = 0; c < NB; ++c) t += a[0][c];
-            if (t == 12345.678) piv[0] = 1;
-        }
-        FPROF(12);
 #ifdef MFB_FTS
         __shared__ long long s_fts[16 * 8];
+        __shared__ long long s_fts2[16 * 16 * 8];
 #endif
+        FPROF(12);
         double S = 1.0;                          // running row scale (thread 0)
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
-            piv[c] = c;
-            if (c >= pnb) continue;
+            if (c >= pnb) {
+                if (tid == 0) spiv[c] = c;
+                continue;
+            }
             const int par = c & 1;
             FTS(c, 0);
-            // key: |a(i,c)| bits (non-negative doubles order like their bit
-            // patterns; the low 10 mantissa bits give way to 1023 - i, so
-            // near-ties within 2^-42 go to the first row), 0 = no candidate
             unsigned long long key = 0ull;
+            int crow = -1;                       // which of my rows is my key's
 #pragma unroll
             for (int rr = 0; rr < RPT; ++rr) {
-                const int i = tid + rr * NT;
                 const unsigned long long k2 =
-                    ((unsigned long long)__double_as_longlong(a[rr][c]) & 0x7FFFFFFFFFFFFC00ull) |
-                    (unsigned long long)(1023 - i);
-                if (i >= c && i < nr && k2 > key) key = k2;
+                    ((unsigned long long)__double_as_longlong(a[rr][c]) & 0x7FFFFFFFFFFFC000ull) |
+                    ((unsigned long long)(1023 - pos[rr]) << 4) | (unsigned long long)wid;
+                if (pos[rr] >= c && pos[rr] < nr && k2 > key) { key = k2; crow = rr; }
             }
             {   // warp max: redux on the high word, then on the low word among
                 // the lanes holding the high maximum
                 const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
                 const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
                 const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-                key = ((unsigned long long)mh << 32) | ml;
+                const unsigned long long wk = ((unsigned long long)mh << 32) | ml;
+                if (key != wk) crow = -1;        // not the warp's candidate
+                key = wk;
             }
-            const int bi = 1023 - (int)(key & 1023ull);
             FTS(c, 1);
             double *cand = s_cand + (par * NW + wid) * NB;
-            double *rowc = s_rowc + par * NB;
 #pragma unroll
-            for (int rr = 0; rr < RPT; ++rr) {
-                const int i = tid + rr * NT;
-                if (key != 0ull && i == bi) {
+            for (int rr = 0; rr < RPT; ++rr)
+                if (crow == rr) {
 #pragma unroll
                     for (int cc = 0; cc < NB; ++cc) cand[cc] = a[rr][cc];
                 }
-                if (i == c) {
-#pragma unroll
-                    for (int cc = 0; cc < NB; ++cc) rowc[cc] = a[rr][cc];
-                }
-            }
             if (lane == 0) red_k[par * NW + wid] = key;
             FTS(c, 2);
+#ifndef FB_NOBAR
             asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
-            unsigned long long kw[NW];
-#pragma unroll
-            for (int w = 0; w < NW; ++w) kw[w] = w < nwf ? red_k[par * NW + w] : 0ull;
-#pragma unroll
-            for (int h = 1; h < NW; h <<= 1)          // tree max
-#pragma unroll
-                for (int w = 0; w + h < NW; w += 2 * h) kw[w] = kw[w + h] > kw[w] ? kw[w + h] : kw[w];
-            const unsigned long long kb = kw[0];
+#endif
+            // max over the warps' keys: lane w reads warp w's key, one redux pair
+            unsigned long long kb;
+            {
+                const unsigned long long kl_ = lane < nwf ? red_k[par * NW + lane] : 0ull;
+                const unsigned hi = (unsigned)(kl_ >> 32), lo = (unsigned)kl_;
+                const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+                const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+                kb = ((unsigned long long)mh << 32) | ml;
+            }
             FTS(c, 3);
-            if ((kb & ~1023ull) == 0ull) { fail = j0 + c + 1; break; }   // uniform over the warps
-            const int p = 1023 - (int)(kb & 1023ull);
-            piv[c] = p;
-            const int wb = (p & (NT - 1)) >> 5;
-            const double *prow = s_cand + (par * NW + wb) * NB;
+            if ((kb & ~0x3FFFull) == 0ull) { fail = j0 + c + 1; break; }   // uniform over the warps
+            const int p = 1023 - (int)((kb >> 4) & 1023ull);
+            if (tid == 0) spiv[c] = p;
+            const double *prow = s_cand + (par * NW + (int)(kb & 15ull)) * NB;
             const double P = prow[c];
             // P' = sigma P~ in [1, 2) and sigma = 2^-e, from the bits (exact)
             const long long pbits = __double_as_longlong(P);
@@ -248,102 +248,53 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
                                                          0x3FF0000000000000ll) : P;
             const double sg = nrm ? __longlong_as_double((long long)(2046 - ef) << 52) : 1.0;
             FTS(c, 4);
-            if (tid == 0) {
+            if (tid == 0) {                       // the scales, for the unscaling
                 s_fin[c] = P;
                 s_fin[NB + c] = S;
                 S = sg * S * P;
             }
 #pragma unroll
             for (int rr = 0; rr < RPT; ++rr) {
-                const int i = tid + rr * NT;
-                if (i == c) {                 // whole rows swap: L columns too (getf2)
-#pragma unroll
-                    for (int cc = 0; cc < NB; ++cc) a[rr][cc] = prow[cc];
-                } else if (i == p) {
-#pragma unroll
-                    for (int cc = 0; cc < NB; ++cc) a[rr][cc] = rowc[cc];
-                }
-                if (i > c && i < nr) {
+                const bool active = pos[rr] > c && pos[rr] != p && pos[rr] < nr;
+                const bool rowc = pos[rr] == c && p != c;    // moves to position p, stays active
+#ifdef FB_NOUPD
+                if (false) {
+#else
+                if (active || rowc) {
+#endif
                     const double t = sg * a[rr][c];
+                    if (c + 1 < NB) a[rr][c + 1] = fma(-t, prow[c + 1], a[rr][c + 1] * Pp);
 #pragma unroll
-                    for (int cc = c + 1; cc < NB; ++cc) a[rr][cc] = fma(-t, prow[cc], a[rr][cc] * Pp);
+                    for (int cc = c + 2; cc < NB; ++cc) a[rr][cc] = fma(-t, prow[cc], a[rr][cc] * Pp);
                 }
+                pos[rr] = pos[rr] == p ? c : (rowc ? p : pos[rr]);
             }
             FTS(c, 5);
         }
 #ifdef MFB_FTS
         if (tid == 0) for (int q = 0; q < 16 * 8; ++q) g_fts[q] = s_fts[q];
+        if (lane == 0) for (int q = 0; q < 16 * 8; ++q) g_fts2[wid * 128 + q] = s_fts2[wid * 128 + q];
 #endif
         FPROF(13);
-        // 1/P~_c and 1/S_c once, then unscale: L = a~ / P~, U row c = a~ / S_c
-        asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
-        if (tid < 2 * NB && (tid & (NB - 1)) < pnb && !fail) s_fin[2 * NB + tid] = 1.0 / s_fin[tid];
-        asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
-        if (!fail) {
-#pragma unroll
-            for (int rr = 0; rr < RPT; ++rr) {
-                const int i = tid + rr * NT;
-#pragma unroll
-                for (int c = 0; c < NB; ++c) {
-                    if (c < pnb && c < i) a[rr][c] *= s_fin[2 * NB + c];
-                    else if (i < pnb && c >= i) a[rr][c] *= s_fin[3 * NB + i];
-                }
-            }
-            if (tid < pnb) udinv[j0 + tid] = s_fin[NB + tid] * s_fin[2 * NB + tid];
-        }
-        // publish: L | U11 to the band (the owner's columns) and to the slot
-        // (rows x NB, zero past pnb), pivots and the failure flag after them
+        // publish by position: the scaled rows a~ (rows x NB, zero past pnb),
+        // then P~_c, S_c, the pivot positions and the flag; consumers unscale
+        // (L = a~ / P~_c, U row c = a~ / S_c) and derive the row moves
 #pragma unroll
         for (int rr = 0; rr < RPT; ++rr) {
-            const int i = tid + rr * NT, r = j0 + i;
+            const int i = pos[rr];
             if (i < nr) {
 #pragma unroll
                 for (int c = 0; c < NB; c += 2)
                     reinterpret_cast<double2 *>(slot + i * NB)[c >> 1] = make_double2(a[rr][c], a[rr][c + 1]);
-#pragma unroll
-                for (int c = 0; c < NB; ++c) {
-                    const int col = j0 + c;
-                    if (c < pnb && r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = a[rr][c];
-                }
             }
         }
-        // row moves for the consumers, from the pivots (every thread holds
-        // them): final top row q came from the row found by undoing the swaps;
-        // each distinct pivot row below the panel receives a top row
-        if (wid == 0) {
-            int *si = reinterpret_cast<int *>(slot + (long long)(kl + NB) * NB);
-            const int q = lane & (NB - 1);
-            int x = q;
-#pragma unroll
-            for (int c = NB - 1; c >= 0; --c)
-                if (c < pnb) x = (x == c) ? piv[c] : (x == piv[c] ? c : x);
-            int pz = 0;
-            bool lowv = false;
-#pragma unroll
-            for (int c = 0; c < NB; ++c)
-                if (c == q) { pz = piv[c]; lowv = c < pnb && piv[c] >= pnb; }
-#pragma unroll
-            for (int c = 0; c < NB; ++c)
-                if (c < q && piv[c] == pz) lowv = false;
-            int y = pz;
-#pragma unroll
-            for (int c = NB - 1; c >= 0; --c)
-                if (c < pnb) y = (y == c) ? piv[c] : (y == piv[c] ? c : y);
-            const unsigned m = __ballot_sync(0xffffffffu, lane < NB && lowv);
-            const int pos = __popc(m & ((1u << q) - 1u));
-            if (lane < NB) {
-                si[lane] = x;
-                if (lowv) {
-                    si[NB + pos] = pz;
-                    si[2 * NB + pos] = y;
-                }
-            }
-            if (lane == 0) {
-                si[3 * NB] = __popc(m);
-                si[3 * NB + 1] = fail;
-                *s_fail = fail;
-            }
+        double *sd = slot + (long long)(kl + NB) * NB;
+        if (tid == 0) {
+            spiv[NB] = fail;
+            *s_fail = fail;
         }
+        asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");   // s_fin complete
+        if (tid < 2 * NB) sd[tid] = s_fin[tid];
     }
     __syncthreads();
     FPROF(14);
@@ -352,6 +303,26 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
         st_release(ready, (unsigned int)(kp + 1));
     }
     FPROF(15);
+    // off the chain: the unscaled band copy (read by the back substitution,
+    // after the group barrier) and 1/U(c,c)
+    if (wid < nwf && !fail) {
+        if (tid < 2 * NB && (tid & (NB - 1)) < pnb) s_fin[2 * NB + tid] = 1.0 / s_fin[tid];
+        asm volatile("bar.sync 1, %0;" ::"r"(nwf * 32) : "memory");
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr) {
+            const int i = pos[rr], r = j0 + i;
+            if (i < nr) {
+#pragma unroll
+                for (int c = 0; c < NB; ++c) {
+                    const int col = j0 + c;
+                    const double v = (c < pnb && c < i) ? a[rr][c] * s_fin[2 * NB + c]
+                                   : (i < pnb && c >= i) ? a[rr][c] * s_fin[3 * NB + i] : a[rr][c];
+                    if (c < pnb && r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = v;
+                }
+            }
+        }
+        if (tid < pnb) udinv[j0 + tid] = s_fin[NB + tid] * s_fin[2 * NB + tid];   // S_c / P~_c
+    }
     return *s_fail;
 }
 
@@ -367,10 +338,11 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     constexpr int NW = NT / 32;
     extern __shared__ double smem[];
     __shared__ int s_tsrc[NB], s_ldst[NB], s_lsrc[NB];
+    __shared__ double s_cinv[2 * NB];
     __shared__ int s_nlow;
     __shared__ double s_u11[NB * NB];
     __shared__ int s_flag;
-    __shared__ double s_cand[2 * NW * NB], s_rowc[2 * NB], s_fin[4 * NB];
+    __shared__ double s_cand[2 * NW * NB], s_fin[4 * NB];
     __shared__ unsigned long long s_fred_k[2 * NW];
     __shared__ int s_ffail;
 #ifdef MFB_PROFILE
@@ -497,7 +469,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     // later panel, and the owners of panels k+1..k+C cover every rank.
     const int nblk = (n + NB - 1) / NB;
     const int D = C + 1, D_MAX = BAND_GROUP_MAX + 1;
-    const long long SLOT = (long long)(kl + NB) * NB + 32;   // factors + 64 ints of row moves
+    const long long SLOT = (long long)(kl + NB) * NB + 48;   // rows, P~ and S, 32 ints
     double *slots = Y + ny + ((ldab * (long long)n + ny) & 1);   // 16-byte aligned (double2 stores)
     double *udinv = slots + D_MAX * SLOT;          // 1 / U(j, j), written by the panel owners
     unsigned int *ready = bar + gridDim.x / C + s;
@@ -505,9 +477,9 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     auto factor = [&](int kp) -> int {
         double *slot = slots + (kp % D) * SLOT;
         return NTF == 1 ? factor_publish<NT, 1>(AB, n, kl, ku, ldab, kp, slot, udinv, ready,
-                                                s_cand, s_rowc, s_fin, s_fred_k, &s_ffail)
+                                                s_cand, s_fin, s_fred_k, &s_ffail)
                         : factor_publish<NT, 2>(AB, n, kl, ku, ldab, kp, slot, udinv, ready,
-                                                s_cand, s_rowc, s_fin, s_fred_k, &s_ffail);
+                                                s_cand, s_fin, s_fred_k, &s_ffail);
     };
 #define OWNB(b) (((b) % C) == rank)
     if (rank == 0) {
@@ -530,19 +502,57 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
             while (ld_acquire(ready) < (unsigned int)(k + 1)) {}
         __syncthreads();
         const double *slot = slots + (k % D) * SLOT;
-        const int *si = reinterpret_cast<const int *>(slot + (long long)(kl + NB) * NB);
+        const double *sd = slot + (long long)(kl + NB) * NB;
+        const int *si = reinterpret_cast<const int *>(sd + 2 * NB);
         for (int t = tid; t < nr * NB; t += NT) Pnl[(t >> 4) * PST + (t & (NB - 1))] = __ldcg(slot + t);
-        // row moves of the panel's swaps: top row q <- row s_tsrc[q]; moved
-        // lower rows s_ldst[z] <- s_lsrc[z], z < nlow (local panel rows)
-        if (tid < NB) {
-            s_tsrc[tid] = __ldcg(si + tid);
-            s_ldst[tid] = __ldcg(si + NB + tid);
-            s_lsrc[tid] = __ldcg(si + 2 * NB + tid);
+        if (wid == 0) {
+            // reciprocal scales 1/P~_c (lanes 0..15) and 1/S_c (16..31)
+            const double sv = __ldcg(sd + lane);
+            s_cinv[lane] = (lane & (NB - 1)) < pnb ? 1.0 / sv : 0.0;
+            // row moves of the panel's swaps: final top row q holds the row
+            // found by undoing the swaps; each distinct pivot row below the
+            // panel receives a top row (getf2 swap order)
+            int pv[NB];
+#pragma unroll
+            for (int c = 0; c < NB; ++c) pv[c] = __ldcg(si + c);
+            const int q = lane & (NB - 1);
+            int x = q;
+#pragma unroll
+            for (int c = NB - 1; c >= 0; --c)
+                if (c < pnb) x = (x == c) ? pv[c] : (x == pv[c] ? c : x);
+            int pz = 0;
+            bool lowv = false;
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c == q) { pz = pv[c]; lowv = c < pnb && pv[c] >= pnb; }
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+                if (c < q && pv[c] == pz) lowv = false;
+            int y = pz;
+#pragma unroll
+            for (int c = NB - 1; c >= 0; --c)
+                if (c < pnb) y = (y == c) ? pv[c] : (y == pv[c] ? c : y);
+            const unsigned m = __ballot_sync(0xffffffffu, lane < NB && lowv);
+            const int zp = __popc(m & ((1u << q) - 1u));
+            if (lane < NB) {
+                s_tsrc[lane] = x;
+                if (lowv) {
+                    s_ldst[zp] = pz;
+                    s_lsrc[zp] = y;
+                }
+            }
+            if (lane == 0) {
+                s_nlow = __popc(m);
+                s_flag = __ldcg(si + NB);
+            }
         }
-        if (tid == 0) {
-            s_nlow = __ldcg(si + 3 * NB);
-            s_flag = __ldcg(si + 3 * NB + 1);
-        }
+        __syncthreads();
+        if (!s_flag)
+            for (int t = tid; t < nr * NB; t += NT) {
+                const int i = t >> 4, c = t & (NB - 1);
+                if (c < pnb && c < i) Pnl[i * PST + c] *= s_cinv[c];
+                else if (i < pnb && c >= i) Pnl[i * PST + c] *= s_cinv[NB + i];
+            }
         __syncthreads();
         if (s_flag) return;                  // the panel's owner set info[s]
         BPROF(1);
@@ -912,11 +922,9 @@ extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *s
     const size_t smem = (size_t)smem_doubles * sizeof(double);
     cudaStream_t st = mfb_stream(stream);
     switch (threads) {
-        case 128: return launch_band<128>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
-                                          work, sys_woff, X, sys_xoff, info, bar);
         case 256: return launch_band<256>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
                                           work, sys_woff, X, sys_xoff, info, bar);
-        case 512: return launch_band<512>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
+        case 384: return launch_band<384>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
                                           work, sys_woff, X, sys_xoff, info, bar);
         default: return MFB_ERR_ARG;
     }

@@ -85,10 +85,10 @@ class Pattern:
     @property
     def work_doubles(self):
         # band, rhs rows, BAND_GROUP_MAX + 1 panel-publication slots ((kl + 16)
-        # x 16 factors + 32 doubles of row moves/flag), then n reciprocal U
+        # x 16 scaled factors + 32 scales + 16 doubles of pivots/flag), then n reciprocal U
         # diagonals (mfb_band.cu)
         w = (self.ldab * self.n + self.n * (self.ndof + 1) + 1
-             + 17 * ((self.kl + 16) * 16 + 32) + self.n)
+             + 17 * ((self.kl + 16) * 16 + 48) + self.n)
         return w + (w & 1)                 # even: every system's slots stay 16-byte aligned
 
     @property

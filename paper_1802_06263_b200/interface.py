@@ -192,7 +192,9 @@ class _S3Static:
             woff = np.concatenate([[0], np.cumsum([work_d[i] for i in grp])])
             xoff = np.concatenate([[0], np.cumsum([x_d[i] for i in grp])])
             klmax = max(pats[systems[i][0]].kl for i in grp)
-            nt = 512 if klmax > 128 else 256
+            # one panel row per thread when it fits (384 threads keep 170
+            # registers per thread, 512 would cap them at 128 and spill)
+            nt = 256 if klmax + 16 <= 256 else 384
             if klmax + 16 > 2 * nt:
                 raise SizeCapError(f"band half-width {klmax} exceeds the panel kernel's "
                                    f"{2 * nt - 16} (two panel rows per thread)")
