@@ -248,7 +248,7 @@ int mfb_selftest_dmma(double *err, void *stream);
 /* Phase cycle counters of the condense kernel (builds with -DMFB_PROFILE
  * only; returns 1 otherwise). Host pointer, 16 counters. */
 int mfb_debug_prof(unsigned long long *out);
-/* Same for the banded LU kernel (-DMFB_PROFILE builds only). */
+/* Same for the banded LU kernel (24 counters; -DMFB_PROFILE builds only). */
 int mfb_debug_bprof(unsigned long long *out);
 /* -DMFB_PROFILE builds: per-panel timeline of system 0 (4 x 4096 globaltimer ns). */
 int mfb_debug_timeline(unsigned long long *out);

@@ -20,7 +20,7 @@
 #include "mfb_common.cuh"
 
 #ifdef MFB_PROFILE
-__device__ unsigned long long g_bprof[16];
+__device__ unsigned long long g_bprof[24];
 __device__ unsigned long long g_tl[4][4096];     // system 0 timeline (globaltimer ns)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -340,7 +340,6 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     __shared__ int s_tsrc[NB], s_ldst[NB], s_lsrc[NB];
     __shared__ double s_cinv[2 * NB];
     __shared__ int s_nlow;
-    __shared__ double s_u11[NB * NB];
     __shared__ int s_flag;
     __shared__ double s_cand[2 * NW * NB], s_fin[4 * NB];
     __shared__ unsigned long long s_fred_k[2 * NW];
@@ -736,67 +735,118 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     group_sync(ctr, C, bar_target);
 
 
-    // ---- 3. blocked column-oriented back substitution with U ---------------
-    const int last = ((n - 1) / NB) * NB;
-    for (int j0 = last; j0 >= 0; j0 -= NB) {
-        const int pnb = min(NB, n - j0);
-        for (int t = tid; t < NB * NB; t += NT) {
-            const int r = t / NB, c = t % NB;
-            s_u11[t] = (r < pnb && c < pnb && c > r) ? __ldcg(AB + bidx(j0 + r, j0 + c, kl, ku, ldab))
-                       : (r < pnb && c == r) ? __ldcg(udinv + j0 + r) : 0.0;   // diagonal: 1/U(r,r)
-        }
-        __syncthreads();
-        for (int cy = tid; cy < ncy; cy += NT) {
-            if (!OWN(cy >> 3)) continue;
-            double x[NB];
-#pragma unroll
-            for (int r = NB - 1; r >= 0; --r) {
-                if (r >= pnb) { x[r] = 0.0; continue; }
-                double v = Y[(long long)(j0 + r) * ncy + cy];
-#pragma unroll
-                for (int rr = r + 1; rr < NB; ++rr) v -= s_u11[r * NB + rr] * x[rr];
-                x[r] = v * s_u11[r * NB + r];
+    // ---- 3. back substitution U x = y, per owned rhs tile of 8 columns -----
+    // The tile's active rows live in a circular shared-memory window (the
+    // panel being solved and the kl+ku rows above it that its solution
+    // updates). Per panel the U block above the diagonal block is copied
+    // global -> shared with cp.async while the panel's triangular solve runs,
+    // then the push Y -= U x is DMMA from shared memory; the next U11 and the
+    // rows entering the window are staged a panel ahead.
+    {
+        const int last = ((n - 1) / NB) * NB;
+        const int WR = kl + ku + 2 * NB;             // window rows (circular)
+        const int LDU = ((kl + ku + 8 + 7) & ~7) + 4;   // U block column stride
+        double *Yw = smem;                           // WR x 8
+        double *Ub = Yw + WR * 8;                    // NB x LDU (column k, row i - i0)
+        double *Xs = Ub + NB * LDU;                  // NB x 8 solved panel rows
+        double *U11b = Xs + NB * 8;                  // 2 x NB x NB (diagonal: 1/U(r,r))
+        const int tcy = (ncy + 7) >> 3;
+        const int g = lane >> 2, q4 = lane & 3;
+        auto u11_load = [&](int jj, double *dst) {
+            const int pn = min(NB, n - jj);
+            for (int t = tid; t < NB * NB; t += NT) {
+                const int r = t >> 4, c = t & (NB - 1);
+                dst[t] = (r < pn && c < pn && c > r) ? __ldcg(AB + bidx(jj + r, jj + c, kl, ku, ldab))
+                         : (r < pn && c == r) ? __ldcg(udinv + jj + r) : 0.0;
             }
-#pragma unroll
-            for (int r = 0; r < NB; ++r) {
-                if (r < pnb) Y[(long long)(j0 + r) * ncy + cy] = x[r];
-                Ytop[r * ncy + cy] = x[r];
+        };
+        if (rank < tcy) __syncthreads();             // smem reuse after the LU loop
+        for (int tc = rank; tc < tcy; tc += C) {
+            const int cb0 = tc * 8;
+            const int rlo = max(0, last - kl - ku);
+            for (int t = tid; t < (n - rlo) * 8; t += NT) {
+                const int r = rlo + (t >> 3), c = t & 7;
+                Yw[(r % WR) * 8 + c] = cb0 + c < ncy ? Y[(long long)r * ncy + cb0 + c] : 0.0;
             }
-        }
-        __syncthreads();
-        // push the solved panel into the rows above: Y[i] -= U(i, panel) x_panel
-        // (DMMA tiles; A = U block straight from the band, B = x from smem)
-        {
-            const int i0 = max(0, j0 - kl - ku);
-            const int mrows = j0 - i0;
-            const int tr = (mrows + 7) >> 3, tcy = (ncy + 7) >> 3;
-            const int g = lane >> 2, q4 = lane & 3;
-            for (int ti = wid; ti < tr; ti += NW) {
-                const int i = i0 + ti * 8 + g;
-                const bool ri = i < j0;
-                double af[NB / 4];
-#pragma unroll
-                for (int kk = 0; kk < NB / 4; ++kk) {
-                    const int k = 4 * kk + q4;
-                    af[kk] = (ri && k < pnb && (j0 + k) - i <= kl + ku)
-                                 ? -__ldcg(AB + bidx(i, j0 + k, kl, ku, ldab)) : 0.0;
+            u11_load(last, U11b);
+            __syncthreads();
+            int buf = 0;
+            for (int j0 = last; j0 >= 0; j0 -= NB) {
+                BPROF(16);
+                const int pnb = min(NB, n - j0);
+                const int i0 = max(0, j0 - kl - ku);
+                const int mrows = j0 - i0;
+                const double *u11 = U11b + buf * NB * NB;
+                // U(i0..j0-1, j0..j0+pnb-1) -> Ub, asynchronously (columns are
+                // contiguous runs of the band)
+                for (int t = tid; t < NB * mrows; t += NT) {
+                    const int k = t / mrows, i = i0 + (t - k * mrows);
+                    double *dst = Ub + k * LDU + (i - i0);
+                    if (k < pnb && (j0 + k) - i <= kl + ku) {
+                        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;"
+                                     ::"r"(sa), "l"(AB + bidx(i, j0 + k, kl, ku, ldab)) : "memory");
+                    } else {
+                        *dst = 0.0;
+                    }
                 }
-                for (int tc = rank; tc < tcy; tc += C) {
-                    const int ca = tc * 8 + 2 * q4, cb = ca + 1;
-                    double d0 = (ri && ca < ncy) ? Y[(long long)i * ncy + ca] : 0.0;
-                    double d1 = (ri && cb < ncy) ? Y[(long long)i * ncy + cb] : 0.0;
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                BPROF(17);
+                // rows entering the window for the next panel, and its U11
+                if (j0 > 0) {
+                    const int ni0 = max(0, j0 - NB - kl - ku);
+                    for (int t = tid; t < (i0 - ni0) * 8; t += NT) {
+                        const int r = ni0 + (t >> 3), c = t & 7;
+                        Yw[(r % WR) * 8 + c] = cb0 + c < ncy ? Y[(long long)r * ncy + cb0 + c] : 0.0;
+                    }
+                    u11_load(j0 - NB, U11b + (buf ^ 1) * NB * NB);
+                }
+                BPROF(18);
+                // triangular solve of the panel rows, column-oriented (the
+                // dependency chain is two FP64 ops per row)
+                if (tid < 8) {
+                    double v[NB];
+#pragma unroll
+                    for (int r = 0; r < NB; ++r) v[r] = r < pnb ? Yw[((j0 + r) % WR) * 8 + tid] : 0.0;
+#pragma unroll
+                    for (int r = NB - 1; r >= 0; --r) {
+                        if (r >= pnb) continue;
+                        const double x = v[r] * u11[r * NB + r];
+                        v[r] = x;
+#pragma unroll
+                        for (int q = 0; q < r; ++q) v[q] -= u11[q * NB + r] * x;
+                    }
+#pragma unroll
+                    for (int r = 0; r < NB; ++r) {
+                        Xs[r * 8 + tid] = r < pnb ? v[r] : 0.0;
+                        if (r < pnb && cb0 + tid < ncy) Y[(long long)(j0 + r) * ncy + cb0 + tid] = v[r];
+                    }
+                }
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncthreads();
+                BPROF(19);
+                // push: Yw[i] -= U(i, panel) x_panel for i in [i0, j0) (DMMA)
+                const int tr = (mrows + 7) >> 3;
+                for (int ti = wid; ti < tr; ti += NW) {
+                    const int il = ti * 8 + g, i = i0 + il;
+                    const bool ri = il < mrows;
+                    double *yr = Yw + ((ri ? i : 0) % WR) * 8 + 2 * q4;
+                    double d0 = ri ? yr[0] : 0.0, d1 = ri ? yr[1] : 0.0;
 #pragma unroll
                     for (int kk = 0; kk < NB / 4; ++kk) {
-                        const int cc = tc * 8 + g;
-                        const double b = cc < ncy ? Ytop[(4 * kk + q4) * ncy + cc] : 0.0;
-                        dmma884(d0, d1, af[kk], b);
+                        const double a = ri ? -Ub[(4 * kk + q4) * LDU + il] : 0.0;
+                        dmma884(d0, d1, a, Xs[(4 * kk + q4) * 8 + g]);
                     }
-                    if (ri && ca < ncy) Y[(long long)i * ncy + ca] = d0;
-                    if (ri && cb < ncy) Y[(long long)i * ncy + cb] = d1;
+                    if (ri) {
+                        yr[0] = d0;
+                        yr[1] = d1;
+                    }
                 }
+                __syncthreads();
+                BPROF(20);
+                buf ^= 1;
             }
         }
-        __syncthreads();
     }
     BPROF(7);
 
@@ -941,7 +991,7 @@ extern "C" int mfb_debug_timeline(unsigned long long *out) {
 
 extern "C" int mfb_debug_bprof(unsigned long long *out) {
 #ifdef MFB_PROFILE
-    return cudaMemcpyFromSymbol(out, g_bprof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 2;
+    return cudaMemcpyFromSymbol(out, g_bprof, sizeof(unsigned long long) * 24) == cudaSuccess ? 0 : 2;
 #else
     (void)out;
     return 1;

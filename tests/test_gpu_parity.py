@@ -88,7 +88,9 @@ def test_s3_sweep_matches_reference(gpu, name):
         m, v = res.moments[key]
         mg, vg = z[f"mean__{key}"], z[f"var__{key}"]
         assert m.shape == mg.shape and v.shape == vg.shape, key
-        assert _rel(m, mg) <= 1e-8 or np.max(np.abs(m - mg)) <= 1e-12, (key, _rel(m, mg))
+        fm = float(z[f"floor_mean__{key}"]) if f"floor_mean__{key}" in z else 0.0
+        assert (_rel(m, mg) <= max(1e-8, 10 * fm)
+                or np.max(np.abs(m - mg)) <= 1e-12), (key, _rel(m, mg), fm)
         floor = float(z[f"floor_var__{key}"]) if f"floor_var__{key}" in z else 0.0
         scale = max(float(np.max(mg * mg)), 1e-300)
         assert (_rel(v, vg) <= max(1e-8, 10 * floor)
@@ -113,7 +115,10 @@ def test_cfg3_sweep_matches_reference(gpu):
             continue
         m, v = res.moments[key]
         mg, vg = z[f"mean__{key}"], z[f"var__{key}"]
-        assert _rel(m, mg) <= 1e-8, key
+        # the reference's own drift under a reordered GEMV (make_golden.py)
+        # bounds how closely two tol-1e-11 sweeps can agree
+        fm = float(z[f"floor_mean__{key}"]) if f"floor_mean__{key}" in z else 0.0
+        assert _rel(m, mg) <= max(1e-8, 10 * fm), (key, _rel(m, mg), fm)
         floor = float(z[f"floor_var__{key}"])
         scale = max(float(np.max(mg * mg)), 1e-300)
         assert (_rel(v, vg) <= max(1e-8, 10 * floor)

@@ -38,13 +38,14 @@ for i, nme in names.items():
 h = plan.hyb[plan.darcy[0]]
 print("n", h.n, "w", h.w, "panels", (h.n + 7) // 8)
 
-out = (ctypes.c_ulonglong * 16)()
+out = (ctypes.c_ulonglong * 24)()
 _lib.load().mfb_debug_bprof(out)
 v = np.array(out[:], dtype=np.float64)
 names = {1: "wait + load panel k", 2: "update block k+1 (owner)", 3: "factor panel k+1 (owner)",
          4: "update other blocks", 5: "rhs forward + DMMA", 0: "loop head", 7: "back substitution",
          8: "  upd: stage rows", 9: "  upd: moved rows", 10: "  upd: U12 forward", 11: "  upd: DMMA", 12: "  fac: load", 13: "  fac: columns", 14: "  fac: publish",
-         15: "  fac: fence+release"}
+         15: "  fac: fence+release", 17: "  bs: issue U loads", 18: "  bs: window+U11 prefetch",
+         19: "  bs: solve", 20: "  bs: push"}
 tot = sum(v[i] for i in names)
 print("band_solve CTA 0 (first Stokes system):")
 for i, nme in names.items():
