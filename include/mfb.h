@@ -166,13 +166,16 @@ int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
  * (region[i] < 0: loc = 0). Outputs per point (indexed k-k0): lam
  * [n_lambda], iters, status (MFB_CG_*), rel. residual history res_hist
  * [hist_cap] (entries beyond hist_cap are dropped), g (may be NULL).
+ * stage_doubles: sum_i ndof_i^2; when the point's blocks fit (200 KiB of
+ * shared memory with the vectors) they are staged per point (0: never).
  */
 int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
                    const int *dof_map, const int *region, const long long *blk_base,
                    const long long *h_base, const int *local_idx, int n_real,
                    const double *blocks, const double *hbar, int k0, int n_pts,
                    double tol, int max_iter, double *lam, int *iters, int *status,
-                   double *res_hist, int hist_cap, double *g, void *stream);
+                   double *res_hist, int hist_cap, double *g, long long stage_doubles,
+                   void *stream);
 
 /*
  * Shifted sufficient statistics per group (one subdomain x one local
@@ -250,6 +253,8 @@ int mfb_selftest_dmma(double *err, void *stream);
 int mfb_debug_prof(unsigned long long *out);
 /* Same for the banded LU kernel (24 counters; -DMFB_PROFILE builds only). */
 int mfb_debug_bprof(unsigned long long *out);
+/* -DMFB_PROFILE builds: CG phase cycles of CTA 0 (8 counters). */
+int mfb_debug_cgprof(unsigned long long *out);
 /* -DMFB_PROFILE builds: per-panel timeline of system 0 (4 x 4096 globaltimer ns). */
 int mfb_debug_timeline(unsigned long long *out);
 

@@ -51,7 +51,7 @@ _SIGS = {
     "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p], _i),
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
-                        _p, _p, _p, _p, _i, _p, _p], _i),
+                        _p, _p, _p, _p, _i, _p, ctypes.c_longlong, _p], _i),
     "mfb_group_stats": ([_i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p,
                          _p], _i),
     "mfb_group_fields": ([_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
@@ -62,6 +62,7 @@ _SIGS = {
     "mfb_debug_prof": ([_p], _i),
     "mfb_debug_bprof": ([_p], _i),
     "mfb_debug_timeline": ([_p], _i),
+    "mfb_debug_cgprof": ([_p], _i),
     "mfb_darcy_condense": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _p], _i),
     "mfb_darcy_backsolve": ([_p, _i, _p, _p, _p, _p, _p, _i, _i, _p], _i),
     "mfb_darcy_recover": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),

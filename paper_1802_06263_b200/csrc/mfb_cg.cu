@@ -13,12 +13,47 @@
 // Stopping test ||r|| <= tol ||g|| after the update, breakdown on p.Sp <= 0,
 // x0 = 0 and the zero-rhs early exit follow the reference line by line.
 #include "mfb_common.cuh"
+#include <stdint.h>
+
+#ifdef MFB_PROFILE
+__device__ unsigned long long g_cgprof[8];
+#define CGP(i) do { if (blockIdx.x == 0 && threadIdx.x == 0) { long long _c = clock64(); \
+    if ((i) > 0) g_cgprof[(i)] += (unsigned long long)(_c - cg_t0); cg_t0 = _c; } } while (0)
+#else
+#define CGP(i) do {} while (0)
+#endif
 
 namespace {
 
-constexpr int CG_NT = 256;
+constexpr int CG_NT_MAX = 1024;
 
-__global__ void __launch_bounds__(CG_NT)
+// one row of a column-major nd x nd basis block against the gathered p:
+// four independent accumulators, 32-bit strides
+__device__ __forceinline__ double row_dot(const double *__restrict__ B, int meta,
+                                          const int *__restrict__ sdm,
+                                          const double *__restrict__ p) {
+    const int nd = meta >> 20;
+    const int *dm = sdm + (meta & 0xFFFFF);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = 0;
+    for (; c + 4 <= nd; c += 4, B += 4 * nd) {
+        a0 = fma(B[0], p[dm[c]], a0);
+        a1 = fma(B[nd], p[dm[c + 1]], a1);
+        a2 = fma(B[2 * nd], p[dm[c + 2]], a2);
+        a3 = fma(B[3 * nd], p[dm[c + 3]], a3);
+    }
+    for (; c < nd; ++c, B += nd) a0 = fma(B[0], p[dm[c]], a0);
+    return (a0 + a1) + (a2 + a3);
+}
+
+// Row r of the stacked basis blocks (r in [0, dof_ptr[n_sub]) enumerates every
+// (subdomain i, local mortar dof a)) is owned by thread r mod blockDim; its
+// per-point metadata lives in shared memory: the block column base, the dof
+// list offset, nd and the output dof. When `stage` > 0 the point's blocks
+// (stage = sum_i nd_i^2 doubles) and the dof lists are copied to shared
+// memory once, so every iteration's GEMV reads shared memory only; the row's
+// dot product runs with four independent accumulators.
+__global__ void __launch_bounds__(CG_NT_MAX)
 cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
           const int *__restrict__ dof_ptr, const int *__restrict__ dof_map,
           const int *__restrict__ region, const long long *__restrict__ blk_base,
@@ -26,21 +61,65 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
           int n_real, const double *__restrict__ blocks, const double *__restrict__ hbar,
           int k0, double tol, int max_iter, double *__restrict__ lam_out,
           int *__restrict__ iters_out, int *__restrict__ status_out,
-          double *__restrict__ res_hist, int hist_cap, double *__restrict__ g_out) {
+          double *__restrict__ res_hist, int hist_cap, double *__restrict__ g_out,
+          long long stage) {
     extern __shared__ double sm[];
-    __shared__ double red[CG_NT / 32];
+    __shared__ double red2[2 * (CG_NT_MAX / 32)];   // alternating reduction buffers
+    int rbuf = 0;
+    const int NT = blockDim.x;
+    const int nrows = dof_ptr[n_sub];
+    if (nrows > 2 * n_lambda) __trap();      // shared layout assumes two sides per dof
     double *x = sm;
     double *r = x + n_lambda;
     double *p = r + n_lambda;
     double *Sp = p + n_lambda;
+    double *sB = Sp + n_lambda;                                       // staged blocks
+    long long *rb = reinterpret_cast<long long *>(sB + stage);        // block base + a
+    int *rmeta = reinterpret_cast<int *>(rb + nrows);                 // dof offset | nd << 20
+    int *rout = rmeta + nrows;                                        // output dof
+    int *sdm = rout + nrows;                                          // staged dof lists
+    int *sbo = sdm + nrows;                                           // staged block offsets
+    int *side0 = sbo + n_sub;                                         // rows of dof d
+    int *side1 = side0 + n_lambda;
+    double *rowval = reinterpret_cast<double *>(side1 + n_lambda + 2);   // (aligned below)
+    rowval = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(rowval) + 15) & ~uintptr_t(15));
     const int pt = blockIdx.x;
     const int k = k0 + pt;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
-    // ---- rhs g = sum_i scatter(h_{i, loc_i(k)}) --------------------------
-    for (int d = tid; d < n_lambda; d += CG_NT) { x[d] = 0.0; r[d] = 0.0; }
+    // ---- per-point row metadata and rhs g = sum_i scatter(h_{i, loc_i(k)}) --
+    for (int d = tid; d < n_lambda; d += NT) { x[d] = 0.0; r[d] = 0.0; }
+    if (stage > 0 && tid == 0) {
+        int o = 0;
+        for (int i = 0; i < n_sub; ++i) {
+            sbo[i] = o;
+            o += ndof[i] * ndof[i];
+        }
+    }
+    for (int d = tid; d < nrows; d += NT) sdm[d] = dof_map[d];
+    for (int d = tid; d < n_lambda; d += NT) { side0[d] = 0x7fffffff; side1[d] = -1; }
     __syncthreads();
-    for (int i = wid; i < n_sub; i += CG_NT / 32) {
+    for (int row = tid; row < nrows; row += NT) {
+        atomicMin(&side0[sdm[row]], row);
+        atomicMax(&side1[sdm[row]], row);
+    }
+    for (int i = wid; i < n_sub; i += NT / 32) {
+        const int nd = ndof[i], d0 = dof_ptr[i];
+        const int loc = region[i] < 0 ? 0 : local_idx[(long long)region[i] * n_real + k];
+        const long long bb = blk_base[i] + (long long)loc * nd * nd;
+        if (stage > 0) {
+            const double *src = blocks + bb;
+            double *dst = sB + sbo[i];
+            for (int e = lane; e < nd * nd; e += 32) dst[e] = src[e];
+        }
+        for (int a = lane; a < nd; a += 32) {
+            rb[d0 + a] = (stage > 0 ? sbo[i] : bb) + a;
+            rmeta[d0 + a] = d0 | (nd << 20);
+            rout[d0 + a] = dof_map[d0 + a];
+        }
+    }
+    __syncthreads();
+    for (int i = wid; i < n_sub; i += NT / 32) {
         const int nd = ndof[i];
         const int loc = region[i] < 0 ? 0 : local_idx[(long long)region[i] * n_real + k];
         const double *h = hbar + h_base[i] + (long long)loc * nd;
@@ -50,40 +129,48 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     __syncthreads();
     double *lam = lam_out + (long long)pt * n_lambda;
     if (g_out)
-        for (int d = tid; d < n_lambda; d += CG_NT) g_out[(long long)pt * n_lambda + d] = r[d];
+        for (int d = tid; d < n_lambda; d += NT) g_out[(long long)pt * n_lambda + d] = r[d];
     double part = 0.0;
-    for (int d = tid; d < n_lambda; d += CG_NT) {
+    for (int d = tid; d < n_lambda; d += NT) {
         p[d] = r[d];
         part += r[d] * r[d];
     }
-    double rr = block_sum<CG_NT>(part, red);
+    __syncthreads();
+    double rr = block_sum_alt(part, red2, rbuf);
     const double gnorm = sqrt(rr);
     if (gnorm == 0.0) {
-        for (int d = tid; d < n_lambda; d += CG_NT) lam[d] = 0.0;
+        for (int d = tid; d < n_lambda; d += NT) lam[d] = 0.0;
         if (tid == 0) { iters_out[pt] = 0; status_out[pt] = MFB_CG_ZERO_RHS; }
         return;
     }
     double *hist = res_hist + (long long)pt * hist_cap;
     int status = MFB_CG_MAX_ITER, it_done = max_iter;
+#ifdef MFB_PROFILE
+    long long cg_t0 = 0;
+#endif
     for (int it = 1; it <= max_iter; ++it) {
-        // ---- Sp = sum_i scatter(B_i p_i) ----------------------------------
-        for (int d = tid; d < n_lambda; d += CG_NT) Sp[d] = 0.0;
-        __syncthreads();
-        for (int i = wid; i < n_sub; i += CG_NT / 32) {
-            const int nd = ndof[i];
-            const int loc = region[i] < 0 ? 0 : local_idx[(long long)region[i] * n_real + k];
-            const double *B = blocks + blk_base[i] + (long long)loc * nd * nd;
-            const int *dm = dof_map + dof_ptr[i];
-            for (int a = lane; a < nd; a += 32) {
-                double acc = 0.0;
-                for (int c = 0; c < nd; ++c) acc = fma(B[(long long)c * nd + a], p[dm[c]], acc);
-                atomicAdd(&Sp[dm[a]], acc);
-            }
-        }
+        CGP(0);
+        // ---- Sp = sum_i scatter(B_i p_i): row results, then each dof adds
+        // its two sides (0 + a + b of basis_apply, order free in IEEE) ------
+        __syncthreads();                         // p of the previous iteration
+        CGP(1);
+        if (stage > 0)
+            for (int row = tid; row < nrows; row += NT)
+                rowval[row] = row_dot(sB + rb[row], rmeta[row], sdm, p);
+        else
+            for (int row = tid; row < nrows; row += NT)
+                rowval[row] = row_dot(blocks + rb[row], rmeta[row], sdm, p);
         __syncthreads();
         part = 0.0;
-        for (int d = tid; d < n_lambda; d += CG_NT) part += p[d] * Sp[d];
-        const double pSp = block_sum<CG_NT>(part, red);
+        for (int d = tid; d < n_lambda; d += NT) {
+            const int s0 = side0[d], s1 = side1[d];
+            const double v = s1 != s0 ? rowval[s0] + rowval[s1] : rowval[s0];
+            Sp[d] = v;
+            part += p[d] * v;
+        }
+        CGP(2);
+        const double pSp = block_sum_alt(part, red2, rbuf);
+        CGP(3);
         if (!(pSp > 0.0)) {
             status = MFB_CG_NOT_SPD;
             it_done = it;
@@ -91,13 +178,15 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         }
         const double a = rr / pSp;
         part = 0.0;
-        for (int d = tid; d < n_lambda; d += CG_NT) {
+        for (int d = tid; d < n_lambda; d += NT) {
             x[d] += a * p[d];
             const double rd = r[d] - a * Sp[d];
             r[d] = rd;
             part += rd * rd;
         }
-        const double rr_new = block_sum<CG_NT>(part, red);
+        CGP(4);
+        const double rr_new = block_sum_alt(part, red2, rbuf);
+        CGP(5);
         const double rn = sqrt(rr_new);
         if (tid == 0 && it <= hist_cap) hist[it - 1] = rn / gnorm;
         if (rn <= tol * gnorm) {
@@ -106,15 +195,26 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             break;
         }
         const double beta = rr_new / rr;
-        for (int d = tid; d < n_lambda; d += CG_NT) p[d] = r[d] + beta * p[d];
+        for (int d = tid; d < n_lambda; d += NT) p[d] = r[d] + beta * p[d];
         rr = rr_new;
-        __syncthreads();
+        CGP(6);
     }
-    for (int d = tid; d < n_lambda; d += CG_NT) lam[d] = x[d];
+    for (int d = tid; d < n_lambda; d += NT) lam[d] = x[d];
     if (tid == 0) { iters_out[pt] = it_done; status_out[pt] = status; }
 }
 
+
+
 }  // namespace
+
+extern "C" int mfb_debug_cgprof(unsigned long long *out) {
+#ifdef MFB_PROFILE
+    return cudaMemcpyFromSymbol(out, g_cgprof, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 2;
+#else
+    (void)out;
+    return 1;
+#endif
+}
 
 extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
                               const int *dof_map, const int *region,
@@ -122,17 +222,27 @@ extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const in
                               const int *local_idx, int n_real, const double *blocks,
                               const double *hbar, int k0, int n_pts, double tol,
                               int max_iter, double *lam, int *iters, int *status,
-                              double *res_hist, int hist_cap, double *g, void *stream) {
+                              double *res_hist, int hist_cap, double *g,
+                              long long stage_doubles, void *stream) {
     if (n_pts <= 0) return n_pts == 0 ? MFB_OK : MFB_ERR_ARG;
-    size_t smem = (size_t)4 * n_lambda * sizeof(double);
+    // every mortar dof has two sides: the stacked block rows number 2 n_lambda
+    const int nrows = 2 * n_lambda;
+    int nt = ((nrows + 31) / 32) * 32;
+    if (nt > CG_NT_MAX) nt = CG_NT_MAX;
+    if (nt < 64) nt = 64;
+    size_t smem = (size_t)4 * n_lambda * sizeof(double) + (size_t)nrows * (8 + 4 + 4 + 4 + 8) +
+                  (size_t)n_sub * 4 + (size_t)n_lambda * 8 + 64;
+    // stage the point's blocks in shared memory when they fit
+    long long stage = stage_doubles;
+    if (stage < 0 || smem + (size_t)stage * sizeof(double) > 200 * 1024) stage = 0;
+    smem += (size_t)stage * sizeof(double);
     if (smem > 227 * 1024) return MFB_ERR_SMEM;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return MFB_ERR_SMEM;
-    cg_kernel<<<n_pts, CG_NT, smem, mfb_stream(stream)>>>(
+    cg_kernel<<<n_pts, nt, smem, mfb_stream(stream)>>>(
         n_lambda, n_sub, ndof, dof_ptr, dof_map, region, blk_base, h_base, local_idx, n_real,
-        blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, g);
+        blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, g, stage);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }

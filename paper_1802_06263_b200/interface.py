@@ -471,7 +471,8 @@ class S3Engine:
             _ptr(plan.d_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(plan.d_local), n_real,
             _ptr(st.blocks), _ptr(st.hbar), k0, n_pts, float(tol), int(max_iter),
             _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
-            _ptr(g) if keep_g else None, self.sp), "mfb_cg_batched")
+            _ptr(g) if keep_g else None, int(np.sum(plan.ndof.astype(np.int64) ** 2)),
+            self.sp), "mfb_cg_batched")
         return lam, iters, status, hist, g
 
     # ----------------------------------------------------- (4) moments ----
