@@ -111,16 +111,34 @@ group_fields_kernel(const int *__restrict__ grp_sid, const int *__restrict__ ndo
     }
     __syncthreads();
     const double *Mg = M + grp_moff[g];
+    constexpr int NDR = 32;                  // rows up to 32 dofs live in registers
     for (int f = blockIdx.x * GS_NT + threadIdx.x; f < nf; f += gridDim.x * GS_NT) {
         const double *row = Mg + (long long)f * nd;
         double ml = 0.0, ms = 0.0, qq = 0.0;
-        for (int a = 0; a < nd; ++a) {
-            const double ma = row[a];
-            ml += ma * ls[a];
-            ms += ma * ss[a];
-            double cm = 0.0;
-            for (int b = 0; b < nd; ++b) cm += Cs[a * nd + b] * row[b];
-            qq += ma * cm;
+        if (nd <= NDR) {
+            double m[NDR];
+#pragma unroll
+            for (int b = 0; b < NDR; ++b) m[b] = b < nd ? row[b] : 0.0;
+#pragma unroll
+            for (int a = 0; a < NDR; ++a) {
+                if (a >= nd) break;
+                ml += m[a] * ls[a];
+                ms += m[a] * ss[a];
+                double cm = 0.0;
+#pragma unroll
+                for (int b = 0; b < NDR; ++b)
+                    if (b < nd) cm += Cs[a * nd + b] * m[b];
+                qq += m[a] * cm;
+            }
+        } else {
+            for (int a = 0; a < nd; ++a) {
+                const double ma = row[a];
+                ml += ma * ls[a];
+                ms += ma * ss[a];
+                double cm = 0.0;
+                for (int b = 0; b < nd; ++b) cm += Cs[a * nd + b] * row[b];
+                qq += ma * cm;
+            }
         }
         const long long o = grp_fboff[g] + f;
         fstar[o] = Fb[o] - ml;

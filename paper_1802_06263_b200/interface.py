@@ -293,7 +293,14 @@ class _S3Static:
             sgptr.append(cur)
         nf = plan.nfield[list(sids)].astype(np.int64)
         out_off = np.concatenate([[0], np.cumsum(nf)])
+        keys, kstart, kshape = [], [], []
+        for j, s in enumerate(sids):
+            for name, start, shape in plan.patterns[s].field_layout:
+                keys.append(f"{s}:{name}")
+                kstart.append(int(out_off[j] + start))
+                kshape.append(tuple(shape))
         tab = {"n": len(sel), "pat": _dev(sys_pat, i32), "gptr": _dev(gptr, i32),
+               "keys": keys, "key_start": np.array(kstart, dtype=np.int64), "key_shape": kshape,
                "mem": _dev(mem, i32), "voff": _dev(self._voff[:-1][sel], i64),
                "coff": _dev(self._coff[:-1][sel], i64),
                "moff": _dev(self._moff[:-1][sel], i64),
@@ -525,14 +532,24 @@ class S3Engine:
             st.wtot, _ptr(tab["d_outoff"]), _ptr(mv), ctypes.c_void_p(mv.data_ptr() + 8 * nout),
             self.sp), "mfb_moments_reduce")
         mvh = mv.cpu().numpy()
-        mf, vf = mvh[:nout], mvh[nout:]
-        for j, s in enumerate(sids):
-            base = out_off[j]
-            for name, start, shape in plan.patterns[s].field_layout:
-                size = int(np.prod(shape))
-                mm = mf[base + start: base + start + size].reshape(shape)
-                vv = vf[base + start: base + start + size].reshape(shape)
-                out[f"{s}:{name}"] = _finalize(f"{s}:{name}", mm, vv, vv + mm * mm)
+        mf, vf = mvh[:nout], mvh[nout:].copy()
+        # moments.py:43-58 for every key at once: per-key scale, warn, clamp
+        keys, starts, shapes = tab["keys"], tab["key_start"], tab["key_shape"]
+        if len(starts):
+            sumsq = np.abs(vf + mf * mf)
+            scale = np.maximum(1.0, np.maximum.reduceat(sumsq, starts))
+            sizes = np.diff(np.append(starts, nout))
+            bad = vf < -1e-12 * np.repeat(scale, sizes)
+            if bad.any():
+                nbad = np.add.reduceat(bad.astype(np.int64), starts)
+                for j in np.nonzero(nbad)[0]:
+                    seg = vf[starts[j]: starts[j] + sizes[j]]
+                    log.warning("field %s: %d variance entries below -1e-12*scale (min %.3e), "
+                                "clamping", keys[j], int(nbad[j]), float(seg.min()))
+            np.maximum(vf, 0.0, out=vf)
+        for j, key in enumerate(keys):
+            a, b = starts[j], starts[j] + int(np.prod(shapes[j]))
+            out[key] = (mf[a:b].reshape(shapes[j]), vf[a:b].reshape(shapes[j]))
         return out
 
 
