@@ -904,8 +904,9 @@ extract_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ sys_
     const MfbPattern P = pats[sys_pat[s]];
     const double *X = Xall + sys_xoff[s];
     const int nd = P.ndof, nrhs = nd + 1;
+    const int t0 = blockIdx.y * NT + threadIdx.x, TS = gridDim.y * NT;   // CTAs split outputs
     if (blocks || hbar) {
-        for (int t = threadIdx.x; t < nd * nrhs; t += NT) {
+        for (int t = t0; t < nd * nrhs; t += TS) {
             const int r = t / nrhs, c = t % nrhs;
             double v = 0.0;
             for (int q = P.q_ptr[r]; q < P.q_ptr[r + 1]; ++q)
@@ -918,7 +919,7 @@ extract_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ sys_
         }
     }
     if (M || Fb) {
-        for (long long t = threadIdx.x; t < (long long)P.nfield * nrhs; t += NT) {
+        for (long long t = t0; t < (long long)P.nfield * nrhs; t += TS) {
             const int f = (int)(t / nrhs), c = (int)(t % nrhs);
             double v = 0.0;
             for (int q = P.p_ptr[f]; q < P.p_ptr[f + 1]; ++q)
@@ -1005,7 +1006,9 @@ extern "C" int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int 
                                    const long long *sys_moff, double *Fb,
                                    const long long *sys_fboff, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
-    extract_kernel<256><<<n_sys, 256, 0, mfb_stream(stream)>>>(
+    // few systems (Stokes) get many CTAs each; many systems need no split
+    const int split = n_sys >= 148 ? 1 : (n_sys >= 37 ? 4 : 32);
+    extract_kernel<256><<<dim3(n_sys, split), 256, 0, mfb_stream(stream)>>>(
         pats, sys_pat, X, sys_xoff, blocks, sys_boff, hbar, sys_hoff, M, sys_moff, Fb,
         sys_fboff);
     MFB_CHECK_LAUNCH();

@@ -179,6 +179,7 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                 for (int q = 0; q < 8; ++q)
                     if (i < nb) Lb[i * LS + q] = (q <= i && q < nb) ? a[i][q] : 0.0;
                 s_inv[i] = 1.0 / a[i][i];
+                if (i < nb) Lb[i * LS + BP] = s_inv[i];   // padding column: 1 / L(i,i)
             }
         }
         if (wid == 0) {
@@ -347,15 +348,26 @@ backsolve_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__
             Tp[(ti * 8 + g) * Cp + ca + 1] = d1;
         }
         __syncthreads();
-        // L11^T x = Tp (backward, one thread per column)
+        // L11^T x = Tp (backward, one thread per column, column-oriented so the
+        // dependency chain is two ops per row; 1/L(q,q) sits in column BP)
         for (int c = tid; c < Cp; c += HYB_NT) {
-            for (int q = nb - 1; q >= 0; --q) {
-                double v = Tp[q * Cp + c];
-                for (int qq = q + 1; qq < nb; ++qq) v -= Lp[qq * LS + q] * Tp[qq * Cp + c];
-                v /= Lp[q * LS + q];
-                Tp[q * Cp + c] = v;
-                Xw[((k + q) % m) * Cp + c] = v;
-                Xs[(long long)(k + q) * Cp + c] = v;
+            double t[BP];
+#pragma unroll
+            for (int q = 0; q < BP; ++q) t[q] = q < nb ? Tp[q * Cp + c] : 0.0;
+#pragma unroll
+            for (int q = BP - 1; q >= 0; --q) {
+                if (q >= nb) continue;
+                const double v = t[q] * Lp[q * LS + BP];
+                t[q] = v;
+#pragma unroll
+                for (int qq = 0; qq < q; ++qq) t[qq] -= Lp[q * LS + qq] * v;
+            }
+#pragma unroll
+            for (int q = 0; q < BP; ++q) {
+                if (q >= nb) continue;
+                Tp[q * Cp + c] = t[q];
+                Xw[((k + q) % m) * Cp + c] = t[q];
+                Xs[(long long)(k + q) * Cp + c] = t[q];
             }
         }
         __syncthreads();
