@@ -115,6 +115,16 @@ def _peaks():
     return peaks, fp64
 
 
+def _traffic(kind):
+    """DRAM bytes per launch of a kernel kind from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as fh:
+        t = json.load(fh).get(kind)
+    return (t["dram_bytes_per_launch"], t["source"]) if t else (None, None)
+
+
 def cpu_baseline(cfg_path, tol, sample_points=None):
     """Reference CPU algorithm (oracle port of sdmortar S3), 1 thread."""
     from threadpoolctl import threadpool_limits
@@ -355,7 +365,9 @@ def run_ours(a):
                 "share_of_step": t_ms / tot_ms if tot_ms else None,
                 "executed_tflops": fl / (t_ms / 1000.0) / 1e12,
                 "executed_frac": (fl / (t_ms / 1000.0) / 1e12) / peak if peak else None,
-                "traffic": None,
+                "traffic": _traffic(dom)[0],
+                "traffic_unit": "bytes/launch (dram read + write, ncu --set full)",
+                "traffic_source": _traffic(dom)[1],
                 "per_kind_ms_per_step": {k: v[0] / len(dev_ms) for k, v in kinds.items()}}
     basis_ms = sum(v[0] for v in kinds.values()) / max(len(dev_ms), 1)
     # bytes of the per-step inputs run_method uploads (collocation + KL tables)
