@@ -46,6 +46,21 @@ __device__ __forceinline__ double row_dot(const double *__restrict__ B, int meta
     return (a0 + a1) + (a2 + a3);
 }
 
+// same with p already gathered into the stacked row space (pr = p_rows + d0)
+__device__ __forceinline__ double row_dot_r(const double *__restrict__ B, int nd,
+                                            const double *__restrict__ pr) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = 0;
+    for (; c + 4 <= nd; c += 4, B += 4 * nd) {
+        a0 = fma(B[0], pr[c], a0);
+        a1 = fma(B[nd], pr[c + 1], a1);
+        a2 = fma(B[2 * nd], pr[c + 2], a2);
+        a3 = fma(B[3 * nd], pr[c + 3], a3);
+    }
+    for (; c < nd; ++c, B += nd) a0 = fma(B[0], pr[c], a0);
+    return (a0 + a1) + (a2 + a3);
+}
+
 // Row r of the stacked basis blocks (r in [0, dof_ptr[n_sub]) enumerates every
 // (subdomain i, local mortar dof a)) is owned by thread r mod blockDim; its
 // per-point metadata lives in shared memory: the block column base, the dof
@@ -62,7 +77,7 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
           int k0, double tol, int max_iter, double *__restrict__ lam_out,
           int *__restrict__ iters_out, int *__restrict__ status_out,
           double *__restrict__ res_hist, int hist_cap, double *__restrict__ g_out,
-          long long stage) {
+          long long stage, int use_prow) {
     extern __shared__ double sm[];
     __shared__ double red2[2 * (CG_NT_MAX / 32)];   // alternating reduction buffers
     int rbuf = 0;
@@ -74,15 +89,14 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     double *p = r + n_lambda;
     double *Sp = p + n_lambda;
     double *sB = Sp + n_lambda;                                       // staged blocks
-    long long *rb = reinterpret_cast<long long *>(sB + stage);        // block base + a
-    int *rmeta = reinterpret_cast<int *>(rb + nrows);                 // dof offset | nd << 20
-    int *rout = rmeta + nrows;                                        // output dof
-    int *sdm = rout + nrows;                                          // staged dof lists
-    int *sbo = sdm + nrows;                                           // staged block offsets
+    double *rowval = sB + stage;                                      // row results
+    double *prow = rowval + nrows;                                    // p in row space
+    int *rb = reinterpret_cast<int *>(prow + (use_prow ? nrows : 0)); // block base + a
+    int *rmeta = rb + nrows;                                          // dof offset | nd << 20
+    int *sdm = rmeta + nrows;                                         // dof lists (no prow)
+    int *sbo = sdm + (use_prow ? 0 : nrows);                          // staged block offsets
     int *side0 = sbo + n_sub;                                         // rows of dof d
     int *side1 = side0 + n_lambda;
-    double *rowval = reinterpret_cast<double *>(side1 + n_lambda + 2);   // (aligned below)
-    rowval = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(rowval) + 15) & ~uintptr_t(15));
     const int pt = blockIdx.x;
     const int k = k0 + pt;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -96,12 +110,13 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             o += ndof[i] * ndof[i];
         }
     }
-    for (int d = tid; d < nrows; d += NT) sdm[d] = dof_map[d];
+    if (!use_prow)
+        for (int d = tid; d < nrows; d += NT) sdm[d] = dof_map[d];
     for (int d = tid; d < n_lambda; d += NT) { side0[d] = 0x7fffffff; side1[d] = -1; }
     __syncthreads();
     for (int row = tid; row < nrows; row += NT) {
-        atomicMin(&side0[sdm[row]], row);
-        atomicMax(&side1[sdm[row]], row);
+        atomicMin(&side0[dof_map[row]], row);
+        atomicMax(&side1[dof_map[row]], row);
     }
     for (int i = wid; i < n_sub; i += NT / 32) {
         const int nd = ndof[i], d0 = dof_ptr[i];
@@ -113,9 +128,8 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             for (int e = lane; e < nd * nd; e += 32) dst[e] = src[e];
         }
         for (int a = lane; a < nd; a += 32) {
-            rb[d0 + a] = (stage > 0 ? sbo[i] : bb) + a;
+            rb[d0 + a] = (int)((stage > 0 ? sbo[i] : bb) + a);
             rmeta[d0 + a] = d0 | (nd << 20);
-            rout[d0 + a] = dof_map[d0 + a];
         }
     }
     __syncthreads();
@@ -133,6 +147,10 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     double part = 0.0;
     for (int d = tid; d < n_lambda; d += NT) {
         p[d] = r[d];
+        if (use_prow) {
+            prow[side0[d]] = r[d];
+            prow[side1[d]] = r[d];
+        }
         part += r[d] * r[d];
     }
     __syncthreads();
@@ -154,12 +172,19 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         // its two sides (0 + a + b of basis_apply, order free in IEEE) ------
         __syncthreads();                         // p of the previous iteration
         CGP(1);
-        if (stage > 0)
+        if (use_prow) {
+            const double *Bs = stage > 0 ? sB : blocks;
+            for (int row = tid; row < nrows; row += NT) {
+                const int meta = rmeta[row];
+                rowval[row] = row_dot_r(Bs + rb[row], meta >> 20, prow + (meta & 0xFFFFF));
+            }
+        } else if (stage > 0) {
             for (int row = tid; row < nrows; row += NT)
                 rowval[row] = row_dot(sB + rb[row], rmeta[row], sdm, p);
-        else
+        } else {
             for (int row = tid; row < nrows; row += NT)
                 rowval[row] = row_dot(blocks + rb[row], rmeta[row], sdm, p);
+        }
         __syncthreads();
         part = 0.0;
         for (int d = tid; d < n_lambda; d += NT) {
@@ -195,7 +220,14 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             break;
         }
         const double beta = rr_new / rr;
-        for (int d = tid; d < n_lambda; d += NT) p[d] = r[d] + beta * p[d];
+        for (int d = tid; d < n_lambda; d += NT) {
+            const double pd = r[d] + beta * p[d];
+            p[d] = pd;
+            if (use_prow) {
+                prow[side0[d]] = pd;
+                prow[side1[d]] = pd;
+            }
+        }
         rr = rr_new;
         CGP(6);
     }
@@ -230,9 +262,13 @@ extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const in
     int nt = ((nrows + 31) / 32) * 32;
     if (nt > CG_NT_MAX) nt = CG_NT_MAX;
     if (nt < 64) nt = 64;
-    size_t smem = (size_t)4 * n_lambda * sizeof(double) + (size_t)nrows * (8 + 4 + 4 + 4 + 8) +
-                  (size_t)n_sub * 4 + (size_t)n_lambda * 8 + 64;
-    // stage the point's blocks in shared memory when they fit
+    // vectors, row results, row block offsets + metadata, stage offsets, sides
+    size_t smem = (size_t)4 * n_lambda * 8 + (size_t)nrows * (8 + 4 + 4) + (size_t)n_sub * 4 +
+                  (size_t)n_lambda * 8 + 64;
+    // p gathered into row space (no index chase in the GEMV) when it fits,
+    // else the dof lists; then the point's blocks when they fit too
+    int use_prow = smem + (size_t)nrows * 8 <= 200 * 1024;
+    smem += use_prow ? (size_t)nrows * 8 : (size_t)nrows * 4;
     long long stage = stage_doubles;
     if (stage < 0 || smem + (size_t)stage * sizeof(double) > 200 * 1024) stage = 0;
     smem += (size_t)stage * sizeof(double);
@@ -242,7 +278,8 @@ extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const in
         return MFB_ERR_SMEM;
     cg_kernel<<<n_pts, nt, smem, mfb_stream(stream)>>>(
         n_lambda, n_sub, ndof, dof_ptr, dof_map, region, blk_base, h_base, local_idx, n_real,
-        blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, g, stage);
+        blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, g, stage,
+        use_prow);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }
