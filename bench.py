@@ -115,14 +115,17 @@ def _peaks():
     return peaks, fp64
 
 
-def _traffic(kind):
-    """DRAM bytes per launch of a kernel kind from the committed ncu capture."""
+def _traffic(kind, config):
+    """DRAM bytes per launch of a kernel kind from the committed ncu capture
+    (only for the workload that capture was taken on)."""
     path = os.path.join(ROOT, "profiles", "r01", "traffic.json")
     if not os.path.exists(path):
         return None, None
     with open(path) as fh:
         t = json.load(fh).get(kind)
-    return (t["dram_bytes_per_launch"], t["source"]) if t else (None, None)
+    if not t or t.get("config") != config:
+        return None, None
+    return t["dram_bytes_per_launch"], t["source"]
 
 
 def cpu_baseline(cfg_path, tol, sample_points=None):
@@ -288,7 +291,7 @@ def run_ours(a):
     if ws > 1:
         torch.distributed.barrier()
     dev_ms, e2e_s = [], []
-    solve_ms, launches = [], 0
+    solve_ms, cg_ms, launches = [], [], 0
     iters_host = None
     with ClockSampler(local) as clocks:
         for _ in range(a.steps):
@@ -308,6 +311,8 @@ def run_ours(a):
             launches = core.launches
             for kind, s0, s1, fl, sfl in core.solve_events:
                 solve_ms.append((kind, s0.elapsed_time(s1), fl, sfl))
+            for c0, c1, _ in core.cg_events:
+                cg_ms.append(c0.elapsed_time(c1))
             if ws > 1:
                 iters_host = out[2] if out is not None else np.zeros(1)
             else:
@@ -366,11 +371,26 @@ def run_ours(a):
                 "share_of_step": t_ms / tot_ms if tot_ms else None,
                 "executed_tflops": fl / (t_ms / 1000.0) / 1e12,
                 "executed_frac": (fl / (t_ms / 1000.0) / 1e12) / peak if peak else None,
-                "traffic": _traffic(dom)[0],
+                "traffic": _traffic(dom, a.config)[0],
                 "traffic_unit": "bytes/launch (dram read + write, ncu --set full)",
-                "traffic_source": _traffic(dom)[1],
+                "traffic_source": _traffic(dom, a.config)[1],
                 "per_kind_ms_per_step": {k: v[0] / len(dev_ms) for k, v in kinds.items()}}
     basis_ms = sum(v[0] for v in kinds.values()) / max(len(dev_ms), 1)
+    # batched CG: SURVEY 8(d) bytes per point-iteration 8 sum_i N_dof,i^2 + 48 n_lambda
+    roof_cg = None
+    if cg_ms and iters_host is not None and ws == 1:
+        per_it = 8.0 * float(np.sum(plan.ndof.astype(np.int64) ** 2)) + 48.0 * nl
+        t = float(np.mean(cg_ms)) / 1000.0
+        ach = per_it * float(np.sum(iters_host)) / t / 1e9
+        hbm = float(peaks.get("hbm_copy_gbs", peaks.get("hbm_gbs", 0.0)) or 0.0) if peaks else 0.0
+        roof_cg = {"kernel": "cg_kernel (all points, blocks staged per point)", "bound": "hbm",
+                   "achieved": ach, "peak": hbm or None, "unit": "GB/s",
+                   "frac": ach / hbm if hbm else None,
+                   "algorithmic_bytes_per_point_iteration": per_it,
+                   "point_iterations": int(np.sum(iters_host)), "launch_ms": t * 1000.0,
+                   "traffic": _traffic("cg", a.config)[0],
+                   "note": "algorithmic bytes as if every block were read from HBM per "
+                           "point-iteration; the kernel stages them once per point"}
     # bytes of the per-step inputs run_method uploads (collocation + KL tables)
     h2d = int(res.timings.get("h2d_bytes", 0)) if (res is not None and hasattr(res, "timings")) \
         else 0
@@ -394,6 +414,7 @@ def run_ours(a):
             "basis_local_solves_per_s": local_solves / (basis_ms / 1000.0) if basis_ms else None,
             "cg_iters_mean": float(iters_host.mean()), "cg_iters_max": int(iters_host.max()),
             "roofline": roof,
+            "roofline_cg": roof_cg,
             "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": "realizations/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "run_method(problem, grid, 'S3', tol)"},

@@ -374,8 +374,9 @@ class S3Engine:
         self.stream = torch.cuda.current_stream() if stream is None else stream
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
         self.launches = 0            # kernels launched through the C ABI
-        self.timing = False          # record CUDA events around the basis solves
+        self.timing = False          # record CUDA events around the basis solves and CG
         self.solve_events = []
+        self.cg_events = []
         self.solve_flops = []
 
     def __getattr__(self, name):     # pools live in the static state
@@ -473,6 +474,8 @@ class S3Engine:
         hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=torch.float64, device="cuda")
         g = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda") if keep_g else None
         self.launches += 1
+        if self.timing:
+            e0 = self._ev()
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
             _ptr(plan.d_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(plan.d_local), n_real,
@@ -480,6 +483,8 @@ class S3Engine:
             _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
             _ptr(g) if keep_g else None, int(np.sum(plan.ndof.astype(np.int64) ** 2)),
             self.sp), "mfb_cg_batched")
+        if self.timing:
+            self.cg_events.append((e0, self._ev(), n_pts))
         return lam, iters, status, hist, g
 
     # ----------------------------------------------------- (4) moments ----
