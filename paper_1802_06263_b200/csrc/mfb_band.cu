@@ -503,7 +503,16 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         const double *slot = slots + (k % D) * SLOT;
         const double *sd = slot + (long long)(kl + NB) * NB;
         const int *si = reinterpret_cast<const int *>(sd + 2 * NB);
-        for (int t = tid; t < nr * NB; t += NT) Pnl[(t >> 4) * PST + (t & (NB - 1))] = __ldcg(slot + t);
+        for (int t0 = tid; t0 < nr * NB; t0 += 8 * NT) {     // eight loads in flight
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = t0 + u * NT < nr * NB ? __ldcg(slot + t0 + u * NT) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int t = t0 + u * NT;
+                if (t < nr * NB) Pnl[(t >> 4) * PST + (t & (NB - 1))] = v[u];
+            }
+        }
         if (wid == 0) {
             // reciprocal scales 1/P~_c (lanes 0..15) and 1/S_c (16..31)
             const double sv = __ldcg(sd + lane);

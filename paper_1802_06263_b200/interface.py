@@ -195,7 +195,7 @@ class _S3Static:
             # one panel row per thread when it fits (384 threads keep 170
             # registers per thread, 512 would cap them at 128 and spill)
             nt = 256 if klmax + 16 <= 256 else 384
-            if klmax + 16 > 2 * nt or 2 * klmax > 8 * 8 * (nt // 32):
+            if klmax + 16 > 2 * nt:
                 raise SizeCapError(f"band half-width {klmax} exceeds the panel kernel's "
                                    f"{2 * nt - 16} (two panel rows per thread)")
             w = sub(grp)
