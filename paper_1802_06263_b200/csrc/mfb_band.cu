@@ -116,6 +116,38 @@ __device__ __forceinline__ void group_sync(unsigned int *ctr, int C, unsigned in
     }
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+// one-dimensional TMA bulk copies completing on an mbarrier
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MFB_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra MFB_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -339,6 +371,8 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     extern __shared__ double smem[];
     __shared__ int s_tsrc[NB], s_ldst[NB], s_lsrc[NB];
     __shared__ double s_cinv[2 * NB];
+    __shared__ unsigned long long s_bsbar[2];
+    __shared__ int s_ush[2][NB];
     __shared__ int s_nlow;
     __shared__ int s_flag;
     __shared__ double s_cand[2 * NW * NB], s_fin[4 * NB];
@@ -747,20 +781,50 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     // ---- 3. back substitution U x = y, per owned rhs tile of 8 columns -----
     // The tile's active rows live in a circular shared-memory window (the
     // panel being solved and the kl+ku rows above it that its solution
-    // updates). Per panel the U block above the diagonal block is copied
-    // global -> shared with cp.async while the panel's triangular solve runs,
-    // then the push Y -= U x is DMMA from shared memory; the next U11 and the
-    // rows entering the window are staged a panel ahead.
+    // updates). The U block above each diagonal block is copied global ->
+    // shared by TMA bulk copies (one per column, mbarrier completion) one
+    // panel ahead into a double buffer, so the copy overlaps the previous
+    // panel's solve and push; the push Y -= U x is DMMA from shared memory;
+    // the next U11 and the rows entering the window are staged a panel ahead.
     {
         const int last = ((n - 1) / NB) * NB;
         const int WR = kl + ku + 2 * NB;             // window rows (circular)
         const int LDU = ((kl + ku + 8 + 7) & ~7) + 4;   // U block column stride
         double *Yw = smem;                           // WR x 8
-        double *Ub = Yw + WR * 8;                    // NB x LDU (column k, row i - i0)
-        double *Xs = Ub + NB * LDU;                  // NB x 8 solved panel rows
+        double *Ub2 = Yw + WR * 8;                   // 2 x NB x LDU (column k, row i - i0)
+        double *Xs = Ub2 + 2 * NB * LDU;             // NB x 8 solved panel rows
         double *U11b = Xs + NB * 8;                  // 2 x NB x NB (diagonal: 1/U(r,r))
         const int tcy = (ncy + 7) >> 3;
         const int g = lane >> 2, q4 = lane & 3;
+        if (tid == 0) {
+            mbar_init(&s_bsbar[0], 1);
+            mbar_init(&s_bsbar[1], 1);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        unsigned bsphase[2] = {0u, 0u};
+        // U(i0..jj-1, jj..jj+pn-1) -> buffer b: a contiguous run of the band per
+        // column, started one element early when odd (16-byte aligned ends)
+        auto issue_u = [&](int jj, int b) {
+            if (tid != 0) return;
+            const int pn = min(NB, n - jj), ii0 = max(0, jj - kl - ku), mr = jj - ii0;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            unsigned tot = 0;
+            const double *srcs[NB];
+            unsigned bytes[NB];
+#pragma unroll
+            for (int k = 0; k < NB; ++k) {
+                const long long off = (long long)(jj + k) * ldab + (kl + ku + ii0 - (jj + k));
+                const int sh = (int)(off & 1);
+                s_ush[b][k] = sh;
+                srcs[k] = AB + off - sh;
+                bytes[k] = (k < pn && mr > 0) ? (unsigned)(((mr + sh + 1) & ~1) * 8) : 0u;
+                tot += bytes[k];
+            }
+            mbar_arrive_expect_tx(&s_bsbar[b], tot);
+#pragma unroll
+            for (int k = 0; k < NB; ++k)
+                if (bytes[k]) bulk_g2s(Ub2 + (b * NB + k) * LDU, srcs[k], bytes[k], &s_bsbar[b]);
+        };
         auto u11_load = [&](int jj, double *dst) {
             const int pn = min(NB, n - jj);
             for (int t = tid; t < NB * NB; t += NT) {
@@ -773,6 +837,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         for (int tc = rank; tc < tcy; tc += C) {
             const int cb0 = tc * 8;
             const int rlo = max(0, last - kl - ku);
+            issue_u(last, 0);
             for (int t = tid; t < (n - rlo) * 8; t += NT) {
                 const int r = rlo + (t >> 3), c = t & 7;
                 Yw[(r % WR) * 8 + c] = cb0 + c < ncy ? Y[(long long)r * ncy + cb0 + c] : 0.0;
@@ -786,37 +851,35 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 const int i0 = max(0, j0 - kl - ku);
                 const int mrows = j0 - i0;
                 const double *u11 = U11b + buf * NB * NB;
-                // U(i0..j0-1, j0..j0+pnb-1) -> Ub, asynchronously (columns are
-                // contiguous runs of the band)
-                for (int t = tid; t < NB * mrows; t += NT) {
-                    const int k = t / mrows, i = i0 + (t - k * mrows);
-                    double *dst = Ub + k * LDU + (i - i0);
-                    if (k < pnb && (j0 + k) - i <= kl + ku) {
-                        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;"
-                                     ::"r"(sa), "l"(AB + bidx(i, j0 + k, kl, ku, ldab)) : "memory");
-                    } else {
-                        *dst = 0.0;
-                    }
-                }
-                asm volatile("cp.async.commit_group;" ::: "memory");
+                const double *Ub = Ub2 + buf * NB * LDU;
+                const int *ush = s_ush[buf];
+                // the next panel's U block into the other buffer (its last
+                // reader, the previous push, finished at the loop-end barrier)
+                if (j0 > 0) issue_u(j0 - NB, buf ^ 1);
                 BPROF(17);
                 // rows entering the window for the next panel, and its U11
                 if (j0 > 0) {
-                    const int ni0 = max(0, j0 - NB - kl - ku);
+                    const int ni0 = max(0, j0 - NB - kl - ku), nbase = ni0 % WR;
                     for (int t = tid; t < (i0 - ni0) * 8; t += NT) {
                         const int r = ni0 + (t >> 3), c = t & 7;
-                        Yw[(r % WR) * 8 + c] = cb0 + c < ncy ? Y[(long long)r * ncy + cb0 + c] : 0.0;
+                        int w = nbase + (t >> 3);
+                        if (w >= WR) w -= WR;
+                        Yw[w * 8 + c] = cb0 + c < ncy ? Y[(long long)r * ncy + cb0 + c] : 0.0;
                     }
                     u11_load(j0 - NB, U11b + (buf ^ 1) * NB * NB);
                 }
                 BPROF(18);
                 // triangular solve of the panel rows, column-oriented (the
                 // dependency chain is two FP64 ops per row)
+                const int jbase = j0 % WR, ibase = i0 % WR;    // window slots of j0, i0
                 if (tid < 8) {
                     double v[NB];
 #pragma unroll
-                    for (int r = 0; r < NB; ++r) v[r] = r < pnb ? Yw[((j0 + r) % WR) * 8 + tid] : 0.0;
+                    for (int r = 0; r < NB; ++r) {
+                        int w = jbase + r;
+                        if (w >= WR) w -= WR;
+                        v[r] = r < pnb ? Yw[w * 8 + tid] : 0.0;
+                    }
 #pragma unroll
                     for (int r = NB - 1; r >= 0; --r) {
                         if (r >= pnb) continue;
@@ -831,7 +894,8 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                         if (r < pnb && cb0 + tid < ncy) Y[(long long)(j0 + r) * ncy + cb0 + tid] = v[r];
                     }
                 }
-                asm volatile("cp.async.wait_all;" ::: "memory");
+                mbar_wait(&s_bsbar[buf], bsphase[buf]);
+                bsphase[buf] ^= 1u;
                 __syncthreads();
                 BPROF(19);
                 // push: Yw[i] -= U(i, panel) x_panel for i in [i0, j0) (DMMA)
@@ -839,12 +903,16 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                 for (int ti = wid; ti < tr; ti += NW) {
                     const int il = ti * 8 + g, i = i0 + il;
                     const bool ri = il < mrows;
-                    double *yr = Yw + ((ri ? i : 0) % WR) * 8 + 2 * q4;
+                    int w = ibase + (ri ? il : 0);
+                    if (w >= WR) w -= WR;
+                    double *yr = Yw + w * 8 + 2 * q4;
                     double d0 = ri ? yr[0] : 0.0, d1 = ri ? yr[1] : 0.0;
 #pragma unroll
                     for (int kk = 0; kk < NB / 4; ++kk) {
-                        const double a = ri ? -Ub[(4 * kk + q4) * LDU + il] : 0.0;
-                        dmma884(d0, d1, a, Xs[(4 * kk + q4) * 8 + g]);
+                        const int k = 4 * kk + q4;
+                        const double a = (ri && k < pnb && (j0 + k) - i <= kl + ku)
+                                             ? -Ub[k * LDU + ush[k] + il] : 0.0;
+                        dmma884(d0, d1, a, Xs[k * 8 + g]);
                     }
                     if (ri) {
                         yr[0] = d0;

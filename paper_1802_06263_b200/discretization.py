@@ -105,13 +105,13 @@ class Pattern:
     def smem_doubles(self):
         # band_solve_kernel (NB = 16): panel (kl + 16) x 17, U12 + staging 2 x 16 x ust,
         # rhs rows 16 x (ndof + 1)
-        # back substitution reuses it: window 8 x (kl + ku + 32), U block
+        # back substitution reuses it: window 8 x (kl + ku + 32), two U blocks
         # 16 x ldu, solved rows 16 x 8, two U11 blocks
         ust = (self.kl + self.ku + 16) | 1
         ldu = ((self.kl + self.ku + 15) & ~7) + 4
         lu = ((self.kl + 16) * 17 + 16 * ust + max(16 * ust, 3 * 8 * 160)
               + 16 * (self.ndof + 1))
-        bs = 8 * (self.kl + self.ku + 32) + 16 * ldu + 16 * 8 + 2 * 16 * 16
+        bs = 8 * (self.kl + self.ku + 32) + 2 * 16 * ldu + 16 * 8 + 2 * 16 * 16
         return max(lu, bs)
 
 
