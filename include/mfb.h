@@ -9,6 +9,7 @@
  *
  *   mfb_kl_realize        <- LogPermField.realize / evaluate_log
  *                            (random_field.py:232-243, 125-140)
+ *   mfb_kl_realize_ld     <- problem.permeability (problem.py:85-96), S2
  *   mfb_systems_solve     <- problem.assemble_subdomain + DarcyOperator /
  *                            StokesOperator factor + the N_dof star solves of
  *                            compute_flux_basis and the bar solve
@@ -125,6 +126,13 @@ const char *mfb_strerror(int code);
 /* K[l*n_cells + c] = exp(mean[c] + sum_j phi[c*n_term + j] * xi[l*n_term + j]) */
 int mfb_kl_realize(const double *phi, const double *mean, int n_cells, int n_term,
                    const double *xi, int n_loc, double *K, void *stream);
+
+/* Same with a row stride: K[l*ld + c]. Method S2 writes realization k of a
+ * Darcy subdomain into the k-th full-problem K row (problem.permeability(y),
+ * problem.py:85-96), so the Stokes BJS terms of realization k read the same
+ * row (ld >= n_cells). */
+int mfb_kl_realize_ld(const double *phi, const double *mean, int n_cells, int n_term,
+                      const double *xi, int n_loc, double *K, long long ld, void *stream);
 
 /*
  * Assemble, factor (banded LU, partial pivoting) and solve every system s

@@ -14,6 +14,7 @@ _lib = None
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int
+_ll = ctypes.c_longlong
 _d = ctypes.c_double
 
 
@@ -48,6 +49,7 @@ _SIGS = {
     "mfb_version": ([], ctypes.c_char_p),
     "mfb_strerror": ([_i], ctypes.c_char_p),
     "mfb_kl_realize": ([_p, _p, _i, _i, _p, _i, _p, _p], _i),
+    "mfb_kl_realize_ld": ([_p, _p, _i, _i, _p, _i, _p, _ll, _p], _i),
     "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p], _i),
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,

@@ -13,7 +13,7 @@ constexpr int KL_MAX_TERM = 64;
 __global__ void kl_realize_kernel(const double *__restrict__ phi,
                                   const double *__restrict__ mean, int n_cells,
                                   int n_term, const double *__restrict__ xi,
-                                  int n_loc, double *__restrict__ K) {
+                                  int n_loc, double *__restrict__ K, long long ld) {
     __shared__ double s_xi[KL_MAX_TERM];
     const int l = blockIdx.y;
     if (threadIdx.x < n_term) s_xi[threadIdx.x] = xi[(long long)l * n_term + threadIdx.x];
@@ -23,22 +23,29 @@ __global__ void kl_realize_kernel(const double *__restrict__ phi,
         const double *row = phi + (long long)c * n_term;
         double dot = 0.0;
         for (int j = 0; j < n_term; ++j) dot = fma(row[j], s_xi[j], dot);
-        K[(long long)l * n_cells + c] = exp(mean[c] + dot);
+        K[(long long)l * ld + c] = exp(mean[c] + dot);
     }
 }
 }  // namespace
 
-extern "C" int mfb_kl_realize(const double *phi, const double *mean, int n_cells,
-                              int n_term, const double *xi, int n_loc, double *K,
-                              void *stream) {
-    if (n_cells < 0 || n_loc < 0 || n_term < 0 || n_term > KL_MAX_TERM) return MFB_ERR_ARG;
+extern "C" int mfb_kl_realize_ld(const double *phi, const double *mean, int n_cells,
+                                 int n_term, const double *xi, int n_loc, double *K,
+                                 long long ld, void *stream) {
+    if (n_cells < 0 || n_loc < 0 || n_term < 0 || n_term > KL_MAX_TERM || ld < n_cells)
+        return MFB_ERR_ARG;
     if (n_cells == 0 || n_loc == 0) return MFB_OK;
     const int nt = 256;
     int bx = (n_cells + nt - 1) / nt;
     if (bx > 64) bx = 64;
     dim3 grid(bx, n_loc);
     kl_realize_kernel<<<grid, nt, 0, mfb_stream(stream)>>>(phi, mean, n_cells, n_term,
-                                                          xi, n_loc, K);
+                                                          xi, n_loc, K, ld);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
+}
+
+extern "C" int mfb_kl_realize(const double *phi, const double *mean, int n_cells,
+                              int n_term, const double *xi, int n_loc, double *K,
+                              void *stream) {
+    return mfb_kl_realize_ld(phi, mean, n_cells, n_term, xi, n_loc, K, n_cells, stream);
 }

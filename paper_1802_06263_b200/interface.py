@@ -1,4 +1,4 @@
-"""Drop-in `run_method` for Method S3 on one B200.
+"""Drop-in `run_method` for Methods S3 and S2 on one B200.
 
 Same signature, return type and error behaviour as the reference's
 `sdmortar.interface.run_method` (interface.py:288-346): a `RunResult` with
@@ -15,11 +15,13 @@ the device through the C ABI (include/mfb.h):
   4. moment kernels (lambda streamed in realization order; fields through
      per-group shifted statistics)
 
-Methods S1 and S2 are not part of this tier's hot path and
-raise NotImplementedError -- there is no CPU fallback.
+Method S2 (the deterministic MFB) runs the same kernels
+with one system per (subdomain, global realization). Method S1 is not on
+this path and raises NotImplementedError -- there is no CPU fallback.
 """
 
 import ctypes
+from collections.abc import Sequence
 import logging
 import time
 from dataclasses import dataclass, field
@@ -87,6 +89,43 @@ class RunResult:
     timings: dict = field(default_factory=dict)
 
 
+class ResidualHistories(Sequence):
+    """Per-point CG residual histories (reference: `RunResult.residuals`, a
+    list of per-point lists, interface.py:284,335) kept as one flat array.
+
+    Indexing returns the point's history as a Python list, like the
+    reference; the flat storage keeps a cfg4-scale sweep (54,273 points x
+    ~13k iterations) at 8 bytes per entry instead of a Python float each.
+    """
+
+    def __init__(self, flat, iters):
+        self.flat = flat
+        self.iters = np.asarray(iters, dtype=np.int64)
+        self.offsets = np.concatenate([[0], np.cumsum(self.iters)])
+
+    def __len__(self):
+        return len(self.iters)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[j] for j in range(*k.indices(len(self)))]
+        k = range(len(self))[k]
+        return self.flat[self.offsets[k]:self.offsets[k + 1]].tolist()
+
+    def array(self, k):
+        """Point k's history as a numpy view (no copy)."""
+        return self.flat[self.offsets[k]:self.offsets[k + 1]]
+
+
+def _pack_histories(hist, iters):
+    """Device [n_pts, cap] histories -> host ResidualHistories (only the
+    first iters[k] entries of row k travel to the host)."""
+    import torch
+    it = iters.to(torch.int64).clamp(max=hist.shape[1])
+    mask = torch.arange(hist.shape[1], device=hist.device)[None, :] < it[:, None]
+    return ResidualHistories(hist[mask].cpu().numpy(), it.cpu().numpy())
+
+
 def _check_basis_cap(sizes_bytes, cap_mb):
     total = sum(sizes_bytes)
     if cap_mb is not None and total > cap_mb * 2 ** 20:
@@ -105,45 +144,74 @@ def get_plan(problem, grid):
 
 
 class _S3Static:
-    """Everything an S3 sweep needs that depends only on (problem, grid).
+    """Everything a sweep needs that depends only on (problem, grid, method).
 
     Built once per DevicePlan and kept resident: the system list and its
     offsets, the KL tables, the wave partition of the basis launches with
     their workspaces, the output pools and the moment group tables. A call
     to run_method then only launches kernels and copies results back.
+
+    method "S3" (stochastic MFB, interface.py:349-414): one system per
+    (subdomain, local realization of its KL region); Stokes once, frozen at
+    the mean field. method "S2" (deterministic MFB, interface.py:317-328):
+    one system per (subdomain, global realization) -- Stokes included, with
+    the realization's BJS permeability -- and the CG gathers realization k's
+    own blocks.
     """
 
-    def __init__(self, plan, keep_fields=True, darcy_kernel="hybrid"):
+    def __init__(self, plan, keep_fields=True, darcy_kernel="hybrid", method="S3"):
         import torch
         self.darcy_kernel = darcy_kernel
+        self.method = method
         pb, grid = plan.problem, plan.grid
         lay = pb.layout
         f64, i32, i64 = torch.float64, torch.int32, torch.int64
-        self.systems = systems = plan.s3_systems()
+        n_real = grid.n_real
+        if method == "S2":
+            systems = [(s, k) for s in range(plan.n_sub) for k in range(n_real)]
+            self.n_loc = np.full(plan.n_sub, n_real, dtype=np.int64)
+        else:
+            systems = plan.s3_systems()
+            self.n_loc = plan.n_loc.astype(np.int64).copy()
+        self.systems = systems
         nsys = len(systems)
-        # (1) KL: K buffer = [K0 | K(sid, loc) for Darcy systems]
+        # (1) KL: K buffer = [K0 (all Darcy cells, mean field) | per-system K].
+        # S3: K(sid, loc) per Darcy system. S2: one full K0-layout row per
+        # realization (problem.permeability(y_k)); Stokes systems of
+        # realization k read their BJS cells from that row.
         koff = np.zeros(nsys, dtype=np.int64)
         first = {}
-        cur = plan.k0_len
-        for idx, (s, l) in enumerate(systems):
+        for idx, (s, _) in enumerate(systems):
             first.setdefault(s, idx)
-            if lay.physics(s) == "darcy":
-                koff[idx] = cur
-                cur += pb.meshes[s].n_cells
+        if method == "S2":
+            for idx, (s, k) in enumerate(systems):
+                koff[idx] = plan.k0_len * (1 + k) + (plan.k0_off[s] if s in plan.k0_off else 0)
+            cur = plan.k0_len * (1 + n_real)
+        else:
+            cur = plan.k0_len
+            for idx, (s, l) in enumerate(systems):
+                if lay.physics(s) == "darcy":
+                    koff[idx] = cur
+                    cur += pb.meshes[s].n_cells
         self.koff, self.sys_first = koff, first
         self.K = torch.empty(max(cur, 1), dtype=f64, device="cuda")
         self.kl = []
         for s in plan.darcy:
-            r = lay.blocks[s].kl_region
-            c = pb.meshes[s].centroids
-            phi, mean = pb.perm.mode_table(r, c[:, 0], c[:, 1])
-            nt = phi.shape[1]
-            xi = np.zeros((1 + int(plan.n_loc[s]), nt))
-            xi[1:] = grid.local_points[r][:, :nt]
-            self.kl.append((s, len(mean), nt, _dev(phi, f64), _dev(mean, f64), _dev(xi, f64),
-                            int(koff[first[s]])))
+            phi, mean, xi = self._kl_tables(plan, s)
+            if method == "S2":
+                dst, ld = plan.k0_len + plan.k0_off[s], plan.k0_len
+            else:
+                dst, ld = int(koff[first[s]]), len(mean)
+            self.kl.append((s, len(mean), phi.shape[1], _dev(phi, f64), _dev(mean, f64),
+                            _dev(xi, f64), int(dst), xi.shape[0] - 1, int(ld)))
         self.kl_h2d_bytes = sum(8 * (t[3].numel() + t[4].numel() + t[5].numel())
                                 for t in self.kl)
+        # CG gather tables: block of subdomain i at point k is loc = table[region_i][k]
+        if method == "S2":
+            self.d_cg_region = _dev(np.zeros(plan.n_sub, dtype=np.int32), i32)
+            self.d_cg_local = _dev(np.arange(n_real, dtype=np.int32)[None, :], i32)
+        else:
+            self.d_cg_region, self.d_cg_local = plan.d_region, plan.d_local
         self._plan = plan
         # (2) systems: pools and waves
         pats = plan.patterns
@@ -251,7 +319,9 @@ class _S3Static:
         members, gptr, order_cache = [], [0], {}
         for s, l in systems:
             r = plan.region[s]
-            if r < 0:
+            if method == "S2":                  # one realization per system
+                mem = np.array([l])
+            elif r < 0:
                 mem = np.arange(grid.n_real)
             else:
                 if r not in order_cache:
@@ -338,6 +408,20 @@ class _S3Static:
             self._wave_cache[key] = tuple(out)
         return self._wave_cache[key]
 
+    def _kl_tables(self, plan, s):
+        """Phi, mean and the xi rows (row 0 = the mean field) of Darcy sid s."""
+        pb, grid = plan.problem, plan.grid
+        r = pb.layout.blocks[s].kl_region
+        c = pb.meshes[s].centroids
+        phi, mean = pb.perm.mode_table(r, c[:, 0], c[:, 1])
+        nt = phi.shape[1]
+        pts = grid.local_points[r][:, :nt]
+        if self.method == "S2":        # realization k's region coordinates
+            pts = pts[np.asarray(grid.local_indices[r])]
+        xi = np.zeros((1 + len(pts), nt))
+        xi[1:] = pts
+        return phi, mean, xi
+
     def refresh_inputs(self):
         """Re-upload the sweep's inputs from the host: collocation weights, local
         index tables and the KL tables (Phi, mean, local points). Returns bytes."""
@@ -349,13 +433,8 @@ class _S3Static:
         plan.d_local.copy_(torch.from_numpy(li))
         plan.d_weights.copy_(torch.from_numpy(np.ascontiguousarray(grid.weights)))
         nbytes += li.nbytes + grid.weights.nbytes
-        pb = plan.problem
-        for s, nc, nt, d_phi, d_mean, d_xi, first in self.kl:
-            r = pb.layout.blocks[s].kl_region
-            c = pb.meshes[s].centroids
-            phi, mean = pb.perm.mode_table(r, c[:, 0], c[:, 1])
-            xi = np.zeros((1 + int(plan.n_loc[s]), nt))
-            xi[1:] = grid.local_points[r][:, :nt]
+        for s, nc, nt, d_phi, d_mean, d_xi, *_ in self.kl:
+            phi, mean, xi = self._kl_tables(plan, s)
             for d, h in ((d_phi, phi), (d_mean, mean), (d_xi, xi)):
                 d.copy_(torch.from_numpy(np.ascontiguousarray(h)).view(d.shape))
                 nbytes += h.nbytes
@@ -365,12 +444,13 @@ class _S3Static:
 class S3Engine:
     """Device work of one S3 sweep; methods map 1:1 onto the C ABI calls."""
 
-    def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid"):
+    def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid", method="S3"):
         import torch
         self.torch = torch
         self.plan = plan
+        self.method = method
         self.L = _lib.lib()
-        self.st = plan.s3_static(keep_fields, darcy_kernel)
+        self.st = plan.s3_static(keep_fields, darcy_kernel, method)
         self.stream = torch.cuda.current_stream() if stream is None else stream
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
         self.launches = 0            # kernels launched through the C ABI
@@ -392,15 +472,15 @@ class S3Engine:
         """K for every (Darcy sid, loc) system plus the mean-field K0 buffer."""
         st, plan = self.st, self.plan
         K = st.K
-        for s, nc, nt, d_phi, d_mean, d_xi, first in st.kl:
+        for s, nc, nt, d_phi, d_mean, d_xi, dst, nrows, ld in st.kl:
             self.launches += 2
             _lib.check(self.L.mfb_kl_realize(
                 _ptr(d_phi), _ptr(d_mean), nc, nt, _ptr(d_xi), 1,
                 ctypes.c_void_p(K.data_ptr() + 8 * plan.k0_off[s]), self.sp), "mfb_kl_realize")
-            _lib.check(self.L.mfb_kl_realize(
+            _lib.check(self.L.mfb_kl_realize_ld(
                 _ptr(d_phi), _ptr(d_mean), nc, nt, ctypes.c_void_p(d_xi.data_ptr() + 8 * nt),
-                int(plan.n_loc[s]), ctypes.c_void_p(K.data_ptr() + 8 * first), self.sp),
-                "mfb_kl_realize")
+                nrows, ctypes.c_void_p(K.data_ptr() + 8 * dst), ld, self.sp),
+                "mfb_kl_realize_ld")
         return K
 
     # ------------------------------------------------------- (2) bases ----
@@ -478,7 +558,7 @@ class S3Engine:
             e0 = self._ev()
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
-            _ptr(plan.d_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(plan.d_local), n_real,
+            _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(st.d_cg_local), n_real,
             _ptr(st.blocks), _ptr(st.hbar), k0, n_pts, float(tol), int(max_iter),
             _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
             _ptr(g) if keep_g else None, int(np.sum(plan.ndof.astype(np.int64) ** 2)),
@@ -577,9 +657,9 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     """
     if method not in METHODS:
         raise ValueError(f"unknown method {method!r}, expected one of {METHODS}")
-    if method != "S3":
+    if method == "S1":
         raise NotImplementedError(
-            f"method {method} is not on this B200 path (S3 only); no CPU fallback")
+            "method S1 (matrix-free) is not on this B200 path (S2/S3 only); no CPU fallback")
     _lib.lib()                      # raises NativeLibraryError: no CPU fallback
     import torch
     t0 = time.perf_counter()
@@ -590,9 +670,9 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     if max_iter is None:
         max_iter = max(50, 10 * nl)
     plan = get_plan(problem, grid)
-    _check_basis_cap(plan.basis_bytes(), basis_cap_mb)
+    _check_basis_cap(plan.basis_bytes(method), basis_cap_mb)
     timings = {"plan": time.perf_counter() - t0}
-    eng = S3Engine(plan)
+    eng = S3Engine(plan, method=method)
     timings["h2d_bytes"] = eng.st.refresh_inputs()
     t1 = time.perf_counter()
     eng.kl_fields()
@@ -606,10 +686,9 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     it = iters.cpu().numpy()
     timings["cg"] = time.perf_counter() - t2
     fail = np.nonzero((st == 1) | (st == 2))[0]
-    hist_h = hist.cpu().numpy()
     if len(fail):
         k = int(fail[0])
-        res = hist_h[k, :min(int(it[k]), hist_h.shape[1])].tolist()
+        res = hist[k, :min(int(it[k]), hist.shape[1])].cpu().numpy().tolist()
         if st[k] == 1:
             raise ConvergenceError(f"interface operator is not positive definite "
                                    f"(p.Sp <= 0 at iteration {int(it[k])}, point {k})",
@@ -621,10 +700,11 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     timings["moments"] = time.perf_counter() - t3
     lam_h = lam.cpu().numpy()
     lambdas = [lam_h[k] for k in range(grid.n_real)]
-    residuals = [hist_h[k, :int(it[k])].tolist() for k in range(grid.n_real)]
+    residuals = _pack_histories(hist, iters)
     stats.cg_iters = [int(x) for x in it]
     for s in range(n_sub):
-        nloc = int(plan.n_loc[s])
+        # S3: one factorization per (sid, loc); S2: per (sid, realization)
+        nloc = int(eng.st.n_loc[s])
         stats.factorizations[s] = nloc
         stats.basis_backsolves[s] = int(plan.ndof[s]) * nloc
         stats.backsolves[s] = int(plan.ndof[s]) * nloc + 2 * grid.n_real

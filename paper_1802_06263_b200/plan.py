@@ -176,15 +176,21 @@ class DevicePlan:
             out += [(s, l) for l in range(int(self.n_loc[s]))]
         return out
 
-    def s3_static(self, keep_fields=True, darcy_kernel="hybrid"):
-        st = getattr(self, "_s3_static", None)
+    def s3_static(self, keep_fields=True, darcy_kernel="hybrid", method="S3"):
+        """Resident sweep state for `method` ("S3" or "S2"), cached per method."""
+        cache = self.__dict__.setdefault("_statics", {})
+        st = cache.get(method)
         if (st is None or (keep_fields and not st.keep_fields)
                 or st.darcy_kernel != darcy_kernel):
             from .interface import _S3Static
-            self._s3_static = None
-            st = _S3Static(self, keep_fields, darcy_kernel)
-            self._s3_static = st
+            cache.pop(method, None)
+            st = _S3Static(self, keep_fields, darcy_kernel, method)
+            cache[method] = st
         return st
 
-    def basis_bytes(self):
+    def basis_bytes(self, method="S3"):
+        """Basis storage the reference's size cap checks (interface.py:271-276):
+        S3 the whole per-(sid, loc) pool (375), S2 one realization (320-322)."""
+        if method == "S2":
+            return [8 * int(self.ndof[s]) ** 2 for s in range(self.n_sub)]
         return [8 * int(self.ndof[s]) ** 2 * int(self.n_loc[s]) for s in range(self.n_sub)]

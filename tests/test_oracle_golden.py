@@ -64,3 +64,20 @@ def test_oracle_cg_error_paths():
     with pytest.raises(ConvergenceError) as err:
         cg_solve(lambda v: A @ v, np.ones(30), tol=1e-14, max_iter=3)
     assert len(err.value.residuals) == 3
+
+
+@pytest.mark.parametrize("name", ["cfg1", "darcy_twoblock", "case1_mini"])
+def test_oracle_s2_matches_reference(name):
+    """The oracle's Method S2 (deterministic MFB) against the reference's own
+    S2 sweep (tests/golden/make_golden_s2.py)."""
+    from oracle import s3_cpu
+    z = golden(name + "_s2")
+    _, problem, grid, _ = case_from_golden(name)
+    r = s3_cpu.run_s2(problem, grid, tol=TOL)
+    assert _rel(np.array(r["lambdas"]), z["s2_lambda"]) <= 1e-9
+    for key, (m, v) in r["moments"].items():
+        mg, vg = z[f"mean__{key}"], z[f"var__{key}"]
+        assert _rel(m, mg) <= 1e-8 or np.max(np.abs(m - mg)) <= 1e-12, key
+        scale = max(float(np.max(mg ** 2)), 1e-300)
+        assert (_rel(v, vg) <= max(1e-8, 10 * float(z[f"floor_var__{key}"]))
+                or np.max(np.abs(v - vg)) / scale <= 1e-12), key
