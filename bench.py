@@ -318,7 +318,13 @@ def run_ours(a):
             else:
                 iters_host = out[1].cpu().numpy()
             core.check_info()
-        # end-to-end through the public API, host in / host out
+        # end-to-end through the public API, host in / host out (one untimed
+        # call first: first-use costs of the host-side packing stay outside)
+        if ws > 1:
+            run_method_distributed(problem, grid, tol=a.tol)
+        else:
+            run_method(problem, grid, method="S3", tol=a.tol)
+        torch.cuda.synchronize()
         for _ in range(a.steps):
             flush.fill_(1)
             torch.cuda.synchronize()

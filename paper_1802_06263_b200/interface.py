@@ -121,9 +121,15 @@ def _pack_histories(hist, iters):
     """Device [n_pts, cap] histories -> host ResidualHistories (only the
     first iters[k] entries of row k travel to the host)."""
     import torch
-    it = iters.to(torch.int64).clamp(max=hist.shape[1])
-    mask = torch.arange(hist.shape[1], device=hist.device)[None, :] < it[:, None]
-    return ResidualHistories(hist[mask].cpu().numpy(), it.cpu().numpy())
+    it_h = np.minimum(iters.cpu().numpy().astype(np.int64), hist.shape[1])
+    width = int(it_h.max(initial=0))
+    if hist.shape[0] * width * 8 <= (256 << 20):      # small: pack on the host
+        h = hist[:, :width].cpu().numpy()
+        mask = np.arange(width)[None, :] < it_h[:, None]
+        return ResidualHistories(h[mask], it_h)
+    it = torch.from_numpy(it_h).to(hist.device)
+    mask = torch.arange(width, device=hist.device)[None, :] < it[:, None]
+    return ResidualHistories(hist[:, :width][mask].cpu().numpy(), it_h)
 
 
 def _check_basis_cap(sizes_bytes, cap_mb):
