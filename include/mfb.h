@@ -18,7 +18,7 @@
  *   mfb_systems_extract   <- compute_flux_basis readout (interface.py:210-235),
  *                            side_functionals (problem.py:132-148),
  *                            postprocess (problem.py:150-158)
- *   mfb_cg_batched        <- the S3 main loop's compute_rhs + cg_solve with
+ *   mfb_cg_batched, _multi <- the S3 main loop's compute_rhs + cg_solve with
  *                            basis_apply (interface.py:107-139, 238-247,
  *                            331-334), all collocation points at once
  *   mfb_group_stats,
@@ -184,6 +184,43 @@ int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
                    double tol, int max_iter, double *lam, int *iters, int *status,
                    double *res_hist, int hist_cap, double *g, long long stage_doubles,
                    void *stream);
+
+/*
+ * Same contract for interfaces whose per-point blocks exceed shared memory
+ * (cfg4): 8 points in flight per CTA over n_cta persistent CTAs, S p on the
+ * FP64 tensor cores with the 8 points as the MMA's N dimension, each block
+ * read once per iteration for every point using it; points are taken from
+ * a work counter (counter: one int of device memory, reset by the call).
+ * n_rows = dof_ptr[n_sub]; n_regions: rows of local_idx. tasks[4 * n_tasks]: runs of <= 8 mortar
+ * dofs of one interface {first dof, strip offset in the lower subdomain's
+ * packed block, same in the upper one, i | (j + 1) << 12 | rows << 24};
+ * sides[4 * n_lambda]: per dof {i, row in i, j, row in j} (j = -1: one
+ * side). packed: the blocks in strip order (mfb_cg_pack), block of
+ * (sid, loc) at pk_base[sid] + loc * pk_size[sid]. scratch:
+ * mfb_cg_multi_scratch_doubles(n_lambda, n_cta) doubles (x, r and S p of
+ * the points in flight).
+ */
+long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta);
+int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int *dof_ptr,
+                 const int *dof_map, const int *region, int n_regions,
+                 const long long *blk_base, const long long *h_base, const int *local_idx,
+                 int n_real, const double *blocks, const double *hbar, int k0, int n_pts,
+                 double tol, int max_iter, double *lam, int *iters, int *status,
+                 double *res_hist, int hist_cap, double *g, const int *tasks, int n_tasks,
+                 const int *sides, const double *packed, const long long *pk_base,
+                 const int *pk_size, int n_cta, double *scratch, int *counter, void *stream);
+
+/*
+ * Repack the basis pool for mfb_cg_multi: strips[4 * n_strips] = {sid, first
+ * row, rows (<= 8), strip offset}; for every local realization l <
+ * n_loc[sid] the strip's rows of block (sid, l) (column-major at blk_base[sid]
+ * + l * ndof^2) are written as MMA A fragments: fragment t of lane (g, q) =
+ * B[row0 + g][4 t + q] at packed[pk_base[sid] + l * pk_size[sid] + offset +
+ * 32 t + lane], zero-padded. max_loc = max n_loc.
+ */
+int mfb_cg_pack(int n_strips, const int *strips, const int *ndof, const int *n_loc,
+                int max_loc, const long long *blk_base, const long long *pk_base,
+                const int *pk_size, const double *blocks, double *packed, void *stream);
 
 /*
  * Shifted sufficient statistics per group (one subdomain x one local

@@ -54,6 +54,10 @@ _SIGS = {
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
                         _p, _p, _p, _p, _i, _p, ctypes.c_longlong, _p], _i),
+    "mfb_cg_multi_scratch_doubles": ([_i, _i], _ll),
+    "mfb_cg_multi": ([_i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
+                      _p, _p, _p, _p, _i, _p, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p], _i),
+    "mfb_cg_pack": ([_i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p], _i),
     "mfb_group_stats": ([_i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p,
                          _p], _i),
     "mfb_group_fields": ([_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,

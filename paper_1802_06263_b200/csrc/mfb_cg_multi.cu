@@ -1,0 +1,458 @@
+// Batched interface CG for large interfaces: MP collocation points per CTA.
+//
+// When a point's gathered flux-basis blocks no longer fit in shared memory
+// (cfg4: n_lambda = 2,720, 128 subdomains, 2.1 MB of blocks per point), the
+// one-CTA-per-point kernel (mfb_cg.cu) re-reads every block from L2 on every
+// CG iteration, and the sweep runs at the L2 bandwidth (~11 TB/s, 27 us per
+// point-iteration on cfg4). This kernel keeps MP = 8 points of the sweep in
+// flight per CTA, in lockstep: each block tile is read from L2 ONCE per
+// iteration and applied to every slot whose local realization uses it (all
+// slots for the frozen Stokes blocks; the slots sharing a Darcy local
+// realization otherwise). Slots are refilled from a global work counter as
+// their points converge (persistent CTAs), so points with long iteration
+// counts do not hold the others back.
+//
+// Per point the algorithm is the reference's (interface.py:107-139, 238-247)
+// and the arithmetic is independent of which slot / CTA / neighbours a point
+// gets: the row products accumulate over the block's columns in order,
+// Sp[d] = row_lower + row_upper (basis_apply's ascending-sid scatter from
+// zero), and the dot products use a fixed shuffle tree + fixed warp order.
+// Same stopping test, breakdown test, zero-rhs exit and outputs as
+// mfb_cg_batched.
+//
+// S p runs on the FP64 tensor cores: with MP = 8 the slots are exactly the
+// N dimension of mma.m8n8k4.f64 -- a warp multiplies an 8-row tile of a
+// block (A, read from L2 once per iteration) by the 4 x 8 tile of the slots'
+// p at those columns (B, from shared memory) into an 8 (rows) x 8 (slots)
+// accumulator. A slot on another local realization gets a zero B column,
+// which leaves its accumulator untouched, so per slot the result is the same
+// sequence of MMA updates whatever the other slots hold.
+//
+// Layout: p of the MP slots in shared memory, interleaved [n_lambda][MP]
+// (64 bytes per mortar dof); x, r and S p in a per-CTA global scratch with
+// the same layout (3 x 174 KB per CTA at cfg4). Work items ("tasks") are
+// runs of <= 8 mortar dofs of one interface: the warp computes both sides'
+// 8-row tiles (an interface's dofs are contiguous in both adjacent
+// subdomains' local orders) and adds them, lower subdomain first. The
+// vector phases run elementwise over (dof, slot pair) with 16-byte accesses.
+#include "mfb_common.cuh"
+
+namespace {
+
+constexpr int MP = 8;            // points in flight per CTA (= the MMA's N)
+constexpr int MNT = 512;         // threads per CTA
+constexpr int MW = MNT / 32;
+constexpr int MREG = 64;         // KL regions cached per slot
+constexpr int MPF = 8;           // A fragments prefetched per side (32 columns)
+
+struct CgMultiArgs {
+    int n_lambda, n_sub, n_regions, n_real, k0, n_pts, max_iter, hist_cap, n_tasks;
+    double tol;
+    const int *ndof, *dof_ptr, *dof_map, *region, *local_idx;
+    const long long *blk_base, *h_base;
+    const double *blocks, *hbar;
+    const int4 *tasks;           // {d0, strip lower, strip upper, i | (j + 1) << 12 | R << 24}
+    const double *packed;        // blocks as MMA-fragment strips (mfb_cg_pack)
+    const long long *pk_base;    // per sid: packed block of loc l at pk_base + l * pk_size
+    const int *pk_size;
+    const int4 *sides;           // per dof {i, a_i, j, a_j} (j = -1: one side)
+    double *lam, *res_hist, *g, *scratch;
+    int *iters, *status, *next;
+};
+
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// per-slot sums of the two slots (2 q, 2 q + 1) a thread accumulated, with
+// q = threadIdx.x & 3 fixed for the thread: fixed xor tree over the lanes
+// sharing q, then the warps in order
+__device__ __forceinline__ void reduce_pairs(double &v0, double &v1, double (*red)[MP],
+                                             double *out) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    if (lane < 4) {
+        red[wid][2 * lane] = v0;
+        red[wid][2 * lane + 1] = v1;
+    }
+    __syncthreads();
+    if (threadIdx.x < MP) {
+        double t = 0.0;
+        for (int w = 0; w < MW; ++w) t += red[w][threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+    __syncthreads();
+}
+
+// acc += the 8-row strip at `soff` of subdomain sid's packed block (slot
+// n's block: local realization s_loc[region][n]) times the slots' p. A strip
+// holds the A fragments of its MMAs in lane order: fragment t of lane
+// (g, q) = B[r0 + g][4 t + q] at strip[32 t + lane] (zero-padded), so every
+// A load is one coalesced 256-byte warp access.
+__device__ __forceinline__ void side_mma(const CgMultiArgs &A, int sid, int soff,
+                                         const double *__restrict__ ps, const int *sdm,
+                                         const int *s_loc, int live, double &d0, double &d1) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const int nd = A.ndof[sid];
+    const int nt4 = (nd + 3) >> 2;
+    const int reg = A.region[sid];
+    const int *dm = sdm + A.dof_ptr[sid];       // shared: dof * MP
+    const double *base = A.packed + A.pk_base[sid] + soff + lane;
+    const int psz = A.pk_size[sid];
+    int rem = live;
+    while (rem) {
+        int m = rem, l = 0;
+        if (reg >= 0) {
+            const int s0 = __ffs(rem) - 1;
+            l = s_loc[reg * MP + s0];
+            m = 0;
+#pragma unroll
+            for (int s = 0; s < MP; ++s)
+                if (((rem >> s) & 1) && s_loc[reg * MP + s] == l) m |= 1 << s;
+        }
+        rem &= ~m;
+        // B column n = slot g; slots outside this realization's group get 0.
+        // Two accumulator chains (even / odd fragments) halve the MMA
+        // dependency chain; their sum is the row product.
+        const bool all = (m == live);
+        const double bm = ((m >> g) & 1) ? 1.0 : 0.0;
+        const double *Sl = base + (long long)l * psz;
+        double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+        for (int t0 = 0; t0 < nt4; t0 += MPF) {
+            double af[MPF];
+            int dv[MPF];
+#pragma unroll
+            for (int t = 0; t < MPF; ++t) {
+                if (t0 + t < nt4) {
+                    af[t] = __ldg(Sl + 32 * (t0 + t));
+                    const int c = 4 * (t0 + t) + q;
+                    dv[t] = c < nd ? dm[c] + g : g;
+                }
+            }
+            if (all) {
+#pragma unroll
+                for (int t = 0; t < MPF; t += 2) {
+                    if (t0 + t >= nt4) break;
+                    dmma884(e0, e1, af[t], ps[dv[t]]);
+                    if (t0 + t + 1 < nt4) dmma884(o0, o1, af[t + 1], ps[dv[t + 1]]);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < MPF; t += 2) {
+                    if (t0 + t >= nt4) break;
+                    dmma884(e0, e1, af[t], ps[dv[t]] * bm);
+                    if (t0 + t + 1 < nt4) dmma884(o0, o1, af[t + 1], ps[dv[t + 1]] * bm);
+                }
+            }
+        }
+        // slots outside the group have e = o = 0 here: d + 0 leaves them
+        d0 += e0 + o0;
+        d1 += e1 + o1;
+    }
+}
+
+// strips[e] = {sid, r0, rows, strip offset}: copy rows r0..r0+rows-1 of every
+// local realization's block of sid (column-major Bt[c*nd + r]) into
+// fragment order (zero-padded to 8 rows x 4-column multiples)
+__global__ void cg_pack_kernel(const int4 *__restrict__ strips, const int *__restrict__ ndof,
+                               const int *__restrict__ n_loc, const long long *__restrict__ blk_base,
+                               const long long *__restrict__ pk_base,
+                               const int *__restrict__ pk_size, const double *__restrict__ blocks,
+                               double *__restrict__ packed) {
+    const int4 S = strips[blockIdx.x];
+    const int sid = S.x, nd = ndof[sid], nt4 = (nd + 3) >> 2;
+    for (int l = blockIdx.y; l < n_loc[sid]; l += gridDim.y) {
+        const double *B = blocks + blk_base[sid] + (long long)l * nd * nd;
+        double *D = packed + pk_base[sid] + (long long)l * pk_size[sid] + S.w;
+        for (int e = threadIdx.x; e < 32 * nt4; e += blockDim.x) {
+            const int lane = e & 31, g = lane >> 2, c = 4 * (e >> 5) + (lane & 3);
+            D[e] = (g < S.z && c < nd) ? B[(long long)c * nd + S.y + g] : 0.0;
+        }
+    }
+}
+
+enum { SLOT_RUN = 0, SLOT_NEW = 1, SLOT_DONE = 2 };
+
+__global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
+    extern __shared__ double ps[];                 // [n_lambda][MP], then the dof lists
+    __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP];
+    __shared__ double s_rr[MP], s_gn[MP], s_a[MP], s_b[MP], s_tot[MP];
+    __shared__ int s_loc[MREG * MP];
+    __shared__ double s_red[MW][MP];
+    __shared__ int s_any;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int n = A.n_lambda;
+    const int npair = n * (MP / 2);
+    const int sq = 2 * (tid & 3);                  // this thread's slot pair (vector phases)
+    double *Xs = A.scratch + (long long)blockIdx.x * 3 * n * MP;
+    double *Rs = Xs + (long long)n * MP;
+    double *Ss = Rs + (long long)n * MP;
+    double2 *X2 = reinterpret_cast<double2 *>(Xs);
+    double2 *R2 = reinterpret_cast<double2 *>(Rs);
+    double2 *S2 = reinterpret_cast<double2 *>(Ss);
+    double2 *P2 = reinterpret_cast<double2 *>(ps);
+    int *sdm = reinterpret_cast<int *>(ps + (long long)n * MP);   // dof_map * MP
+    if (tid < MP) { s_k[tid] = -1; s_state[tid] = SLOT_DONE; }
+    for (int e = tid; e < n * MP; e += MNT) ps[e] = 0.0;
+    for (int e = tid; e < A.dof_ptr[A.n_sub]; e += MNT) sdm[e] = A.dof_map[e] * MP;
+
+    for (;;) {
+        __syncthreads();
+        // ---- refill empty slots from the global work counter --------------
+        if (tid == 0) {
+            int any = 0;
+            for (int s = 0; s < MP; ++s) {
+                if (s_k[s] == -1) {
+                    const int t = atomicAdd(A.next, 1);
+                    s_k[s] = t < A.n_pts ? t : -2;
+                    s_state[s] = t < A.n_pts ? SLOT_NEW : SLOT_DONE;
+                    s_it[s] = 0;
+                }
+                any |= s_k[s] >= 0;
+            }
+            s_any = any;
+        }
+        __syncthreads();
+        if (!s_any) break;
+        int fresh = 0;
+#pragma unroll
+        for (int s = 0; s < MP; ++s) fresh |= (s_state[s] == SLOT_NEW) << s;
+        const bool f0 = (fresh >> sq) & 1, f1 = (fresh >> (sq + 1)) & 1;
+        double v0 = 0.0, v1 = 0.0;
+        if (fresh) {
+            for (int e = tid; e < A.n_regions * MP; e += MNT) {
+                const int s = e % MP;
+                if ((fresh >> s) & 1)
+                    s_loc[e] = A.local_idx[(long long)(e / MP) * A.n_real + A.k0 + s_k[s]];
+            }
+            __syncthreads();
+            // g = 0 + h_lower + h_upper (mortar.jump of the bar traces), x = 0
+            for (int e = tid; e < npair; e += MNT) {
+                if (!(f0 || f1)) break;
+                const int d = e >> 2;
+                const int4 sd = A.sides[d];
+                const int ri = A.region[sd.x], rj = sd.z >= 0 ? A.region[sd.z] : -1;
+                double gv[2] = {0.0, 0.0};
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int s = sq + h;
+                    if (!((fresh >> s) & 1)) continue;   // s_loc is only set for fresh slots
+                    const int li = ri < 0 ? 0 : s_loc[ri * MP + s];
+                    double gg = A.hbar[A.h_base[sd.x] + (long long)li * A.ndof[sd.x] + sd.y];
+                    if (sd.z >= 0) {
+                        const int lj = rj < 0 ? 0 : s_loc[rj * MP + s];
+                        gg = gg + A.hbar[A.h_base[sd.z] + (long long)lj * A.ndof[sd.z] + sd.w];
+                    }
+                    gv[h] = gg;
+                }
+                double2 p2 = P2[e], r2 = R2[e], x2 = X2[e];
+                if (f0) {
+                    p2.x = gv[0]; r2.x = gv[0]; x2.x = 0.0; v0 += gv[0] * gv[0];
+                    if (A.g) A.g[(long long)s_k[sq] * n + d] = gv[0];
+                }
+                if (f1) {
+                    p2.y = gv[1]; r2.y = gv[1]; x2.y = 0.0; v1 += gv[1] * gv[1];
+                    if (A.g) A.g[(long long)s_k[sq + 1] * n + d] = gv[1];
+                }
+                P2[e] = p2; R2[e] = r2; X2[e] = x2;
+            }
+            reduce_pairs(v0, v1, s_red, s_tot);
+            if (tid < MP && ((fresh >> tid) & 1)) {
+                s_rr[tid] = s_tot[tid];
+                s_gn[tid] = sqrt(s_tot[tid]);
+                s_state[tid] = SLOT_RUN;
+                if (s_gn[tid] == 0.0) {          // interface.py:111-113
+                    s_state[tid] = SLOT_DONE;
+                    s_stat[tid] = MFB_CG_ZERO_RHS;
+                }
+            }
+            __syncthreads();
+        }
+        int run = 0;
+#pragma unroll
+        for (int s = 0; s < MP; ++s) run |= (s_state[s] == SLOT_RUN) << s;
+
+        // ---- Phase A: S p on the tensor cores; p.S p --------------------------
+        v0 = 0.0; v1 = 0.0;
+        if (run) {
+            const int g8 = lane >> 2;
+            for (int ti = wid; ti < A.n_tasks; ti += MW) {
+                const int4 T = A.tasks[ti];
+                const int i = T.w & 0xfff, j = ((T.w >> 12) & 0xfff) - 1, R = T.w >> 24;
+                double lo0 = 0.0, lo1 = 0.0, up0 = 0.0, up1 = 0.0;
+                side_mma(A, i, T.y, ps, sdm, s_loc, run, lo0, lo1);
+                if (j >= 0) side_mma(A, j, T.z, ps, sdm, s_loc, run, up0, up1);
+                if (g8 < R) {
+                    const int d = T.x + g8;
+                    const double2 sp = j >= 0 ? make_double2(lo0 + up0, lo1 + up1)
+                                              : make_double2(lo0, lo1);
+                    const int e = d * (MP / 2) + (lane & 3);
+                    S2[e] = sp;
+                    const double2 pp = P2[e];
+                    v0 += pp.x * sp.x;
+                    v1 += pp.y * sp.y;
+                }
+            }
+        }
+        reduce_pairs(v0, v1, s_red, s_tot);
+        if (tid < MP && ((run >> tid) & 1)) {
+            const double pSp = s_tot[tid];
+            s_it[tid] += 1;
+            if (!(pSp > 0.0)) {                  // interface.py:123-126
+                s_state[tid] = SLOT_DONE;
+                s_stat[tid] = MFB_CG_NOT_SPD;
+            } else {
+                s_a[tid] = s_rr[tid] / pSp;
+            }
+        }
+        __syncthreads();
+        int upd = 0;
+#pragma unroll
+        for (int s = 0; s < MP; ++s) upd |= (((run >> s) & 1) && s_state[s] == SLOT_RUN) << s;
+
+        // ---- Phase B: x += a p, r -= a S p, r.r (elementwise) -----------------
+        v0 = 0.0; v1 = 0.0;
+        const bool u0 = (upd >> sq) & 1, u1 = (upd >> (sq + 1)) & 1;
+        if (u0 || u1) {
+            const double a0 = s_a[sq], a1 = s_a[sq + 1];
+            for (int e = tid; e < npair; e += MNT) {
+                const double2 p2 = P2[e], s2 = S2[e];
+                double2 x2 = X2[e], r2 = R2[e];
+                if (u0) {
+                    x2.x += a0 * p2.x;
+                    r2.x -= a0 * s2.x;
+                    v0 += r2.x * r2.x;
+                }
+                if (u1) {
+                    x2.y += a1 * p2.y;
+                    r2.y -= a1 * s2.y;
+                    v1 += r2.y * r2.y;
+                }
+                X2[e] = x2;
+                R2[e] = r2;
+            }
+        }
+        reduce_pairs(v0, v1, s_red, s_tot);
+        if (tid < MP && ((upd >> tid) & 1)) {
+            const double rr_new = s_tot[tid];
+            const double rn = sqrt(rr_new);
+            const int it = s_it[tid];
+            if (it <= A.hist_cap)
+                A.res_hist[(long long)s_k[tid] * A.hist_cap + it - 1] = rn / s_gn[tid];
+            if (rn <= A.tol * s_gn[tid]) {
+                s_state[tid] = SLOT_DONE;
+                s_stat[tid] = MFB_CG_CONVERGED;
+            } else if (it >= A.max_iter) {
+                s_state[tid] = SLOT_DONE;
+                s_stat[tid] = MFB_CG_MAX_ITER;
+            } else {
+                s_b[tid] = rr_new / s_rr[tid];
+                s_rr[tid] = rr_new;
+            }
+        }
+        __syncthreads();
+
+        // ---- Phase C: p = r + beta p; finished slots write their solution ----
+        int cont = 0, fin = 0;
+#pragma unroll
+        for (int s = 0; s < MP; ++s) {
+            cont |= (((upd >> s) & 1) && s_state[s] == SLOT_RUN) << s;
+            fin |= (s_k[s] >= 0 && s_state[s] == SLOT_DONE) << s;
+        }
+        const bool c0 = (cont >> sq) & 1, c1 = (cont >> (sq + 1)) & 1;
+        const bool z0 = (fin >> sq) & 1, z1 = (fin >> (sq + 1)) & 1;
+        if (c0 || c1 || z0 || z1) {
+            const double b0 = s_b[sq], b1 = s_b[sq + 1];
+            for (int e = tid; e < npair; e += MNT) {
+                const int d = e >> 2;
+                double2 p2 = P2[e];
+                if (c0 || c1) {
+                    const double2 r2 = R2[e];
+                    if (c0) p2.x = r2.x + b0 * p2.x;
+                    if (c1) p2.y = r2.y + b1 * p2.y;
+                    P2[e] = p2;
+                }
+                if (z0 || z1) {
+                    const double2 x2 = X2[e];
+                    if (z0)
+                        A.lam[(long long)s_k[sq] * n + d] =
+                            s_stat[sq] == MFB_CG_ZERO_RHS ? 0.0 : x2.x;
+                    if (z1)
+                        A.lam[(long long)s_k[sq + 1] * n + d] =
+                            s_stat[sq + 1] == MFB_CG_ZERO_RHS ? 0.0 : x2.y;
+                }
+            }
+        }
+        __syncthreads();
+        if (tid < MP && ((fin >> tid) & 1)) {
+            A.iters[s_k[tid]] = s_stat[tid] == MFB_CG_ZERO_RHS ? 0 : s_it[tid];
+            A.status[s_k[tid]] = s_stat[tid];
+            s_k[tid] = -1;
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta) {
+    return (long long)n_cta * 3 * n_lambda * MP;
+}
+
+extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof,
+                            const int *dof_ptr,
+                            const int *dof_map, const int *region, int n_regions,
+                            const long long *blk_base, const long long *h_base,
+                            const int *local_idx, int n_real, const double *blocks,
+                            const double *hbar, int k0, int n_pts, double tol, int max_iter,
+                            double *lam, int *iters, int *status, double *res_hist,
+                            int hist_cap, double *g, const int *tasks, int n_tasks,
+                            const int *sides, const double *packed, const long long *pk_base,
+                            const int *pk_size, int n_cta, double *scratch, int *counter,
+                            void *stream) {
+    if (n_pts <= 0) return n_pts == 0 ? MFB_OK : MFB_ERR_ARG;
+    if (n_lambda <= 0 || n_sub <= 0 || n_sub >= 4095 || n_rows <= 0 || n_regions > MREG || n_cta <= 0 ||
+        max_iter < 1 || hist_cap < 1 || n_tasks <= 0)
+        return MFB_ERR_ARG;
+    const size_t smem = (size_t)n_lambda * MP * sizeof(double) + (size_t)n_rows * sizeof(int);
+    if (smem > 220 * 1024) return MFB_ERR_SMEM;
+    if (cudaFuncSetAttribute(cg_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return MFB_ERR_SMEM;
+    cudaStream_t st = mfb_stream(stream);
+    if (cudaMemsetAsync(counter, 0, sizeof(int), st) != cudaSuccess) return MFB_ERR_LAUNCH;
+    CgMultiArgs A;
+    A.n_lambda = n_lambda; A.n_sub = n_sub; A.n_regions = n_regions; A.n_real = n_real;
+    A.k0 = k0; A.n_pts = n_pts; A.max_iter = max_iter; A.hist_cap = hist_cap;
+    A.n_tasks = n_tasks; A.tol = tol;
+    A.ndof = ndof; A.dof_ptr = dof_ptr; A.dof_map = dof_map; A.region = region;
+    A.local_idx = local_idx; A.blk_base = blk_base; A.h_base = h_base;
+    A.blocks = blocks; A.hbar = hbar;
+    A.tasks = reinterpret_cast<const int4 *>(tasks);
+    A.sides = reinterpret_cast<const int4 *>(sides);
+    A.packed = packed; A.pk_base = pk_base; A.pk_size = pk_size;
+    A.lam = lam; A.res_hist = res_hist; A.g = g; A.scratch = scratch;
+    A.iters = iters; A.status = status; A.next = counter;
+    cg_multi_kernel<<<n_cta, MNT, smem, st>>>(A);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_cg_pack(int n_strips, const int *strips, const int *ndof, const int *n_loc,
+                           int max_loc, const long long *blk_base, const long long *pk_base,
+                           const int *pk_size, const double *blocks, double *packed,
+                           void *stream) {
+    if (n_strips < 0 || max_loc < 0) return MFB_ERR_ARG;
+    if (n_strips == 0 || max_loc == 0) return MFB_OK;
+    dim3 grid(n_strips, max_loc < 64 ? max_loc : 64);
+    cg_pack_kernel<<<grid, 128, 0, mfb_stream(stream)>>>(
+        reinterpret_cast<const int4 *>(strips), ndof, n_loc, blk_base, pk_base, pk_size, blocks,
+        packed);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}

@@ -132,6 +132,67 @@ def _pack_histories(hist, iters):
     return ResidualHistories(hist[:, :width][mask].cpu().numpy(), it_h)
 
 
+def cg_tasks(n_sub, ndof, dof_ptr, dof_map, n_lambda, run=8):
+    """Work items of the multi-point CG (mfb_cg_multi): runs of <= `run`
+    mortar dofs of one interface with both sides' block rows (an interface's
+    dofs are contiguous in both adjacent subdomains' local orders, mortar.py
+    sub_dofs), most expensive first, and the strip layout of the packed
+    basis pool (mfb_cg_pack): every task side is an 8-row strip of its
+    subdomain's block, stored as ceil(ndof / 4) MMA fragments of 32 doubles.
+
+    Returns (tasks [n, 4], sides [n_lambda, 4], strips [m, 4], pk_size
+    [n_sub]) int32: task {first dof, strip offset lower, strip offset upper,
+    i | (j + 1) << 12 | rows << 24}; per dof {i, row in i, j, row in j}
+    (j = -1: none); strip {sid, first row, rows, offset}; packed block size.
+    """
+    dof_ptr = np.asarray(dof_ptr, dtype=np.int64)
+    ndof = np.asarray(ndof, dtype=np.int64)
+    sid_of_row = np.repeat(np.arange(n_sub), np.diff(dof_ptr))
+    rows = -np.ones((n_lambda, 2), dtype=np.int64)
+    for row, d in enumerate(dof_map):
+        rows[d, 0 if rows[d, 0] < 0 else 1] = row
+    sides = np.full((n_lambda, 4), -1, dtype=np.int64)
+    for k in range(2):
+        ok = rows[:, k] >= 0
+        sid = sid_of_row[rows[ok, k]]
+        sides[ok, 2 * k] = sid
+        sides[ok, 2 * k + 1] = rows[ok, k] - dof_ptr[sid]
+    runs, d = [], 0
+    while d < n_lambda:
+        i, ai, j, aj = (int(v) for v in sides[d])
+        R = 1
+        while R < run and d + R < n_lambda:
+            i2, a2, j2, b2 = (int(v) for v in sides[d + R])
+            if i2 != i or j2 != j or a2 != ai + R or (j >= 0 and b2 != aj + R):
+                break
+            R += 1
+        runs.append((d, i, ai, j, aj, R))
+        d += R
+    # strips per subdomain in row order
+    per_sid = [[] for _ in range(n_sub)]
+    for d, i, ai, j, aj, R in runs:
+        per_sid[i].append((ai, R))
+        if j >= 0:
+            per_sid[j].append((aj, R))
+    strip_off, strips = {}, []
+    pk_size = np.zeros(n_sub, dtype=np.int64)
+    for s_ in range(n_sub):
+        w = 32 * ((int(ndof[s_]) + 3) // 4)
+        for k, (r0, R) in enumerate(sorted(per_sid[s_])):
+            strip_off[(s_, r0)] = k * w
+            strips.append((s_, r0, R, k * w))
+        pk_size[s_] = w * len(per_sid[s_])
+    tasks = []
+    for d, i, ai, j, aj, R in runs:
+        cost = int(ndof[i] + (ndof[j] if j >= 0 else 0))
+        tasks.append((-cost, d, strip_off[(i, ai)], strip_off[(j, aj)] if j >= 0 else 0,
+                      i | ((j + 1) << 12) | (R << 24)))
+    tasks.sort()
+    tab = np.array([t[1:] for t in tasks], dtype=np.int32).reshape(-1, 4)
+    return (tab, sides.astype(np.int32), np.array(strips, dtype=np.int32).reshape(-1, 4),
+            pk_size.astype(np.int32))
+
+
 def _check_basis_cap(sizes_bytes, cap_mb):
     total = sum(sizes_bytes)
     if cap_mb is not None and total > cap_mb * 2 ** 20:
@@ -548,7 +609,11 @@ class S3Engine:
                 f"(device info {int(info[bad[0]])})")
 
     # ---------------------------------------------------------- (3) CG ----
-    def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False):
+    def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False,
+                     kernel="auto"):
+        """CG over points k0..k0+n_pts-1. kernel: "auto" (multi-point when the
+        blocks exceed shared memory and the points fill the GPU), "cta" (one
+        CTA per point) or "multi" (forced, for tests)."""
         torch, plan, st = self.torch, self.plan, self.st
         n_real = plan.grid.n_real
         n_pts = n_real - k0 if n_pts is None else n_pts
@@ -562,6 +627,25 @@ class S3Engine:
         self.launches += 1
         if self.timing:
             e0 = self._ev()
+        mt = None if kernel == "cta" else self._multi_tables(n_pts, force=kernel == "multi")
+        if mt is not None:
+            self.launches += 1
+            _lib.check(self.L.mfb_cg_pack(
+                mt["n_strips"], _ptr(mt["strips"]), _ptr(plan.d_ndof), _ptr(mt["n_loc"]),
+                mt["max_loc"], _ptr(st.d_blk), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
+                _ptr(st.blocks), _ptr(mt["packed"]), self.sp), "mfb_cg_pack")
+            _lib.check(self.L.mfb_cg_multi(
+                nl, plan.n_sub, int(plan.dof_ptr[-1]), _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
+                _ptr(st.d_cg_region), int(st.d_cg_local.shape[0]), _ptr(st.d_blk), _ptr(st.d_h),
+                _ptr(st.d_cg_local), n_real, _ptr(st.blocks), _ptr(st.hbar), k0, n_pts,
+                float(tol), int(max_iter), _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist),
+                max(hist_cap, 1), _ptr(g) if keep_g else None, _ptr(mt["tasks"]), mt["n_tasks"],
+                _ptr(mt["sides"]), _ptr(mt["packed"]), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
+                mt["n_cta"], _ptr(mt["scratch"]),
+                _ptr(mt["counter"]), self.sp), "mfb_cg_multi")
+            if self.timing:
+                self.cg_events.append((e0, self._ev(), n_pts))
+            return lam, iters, status, hist, g
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
             _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(st.d_cg_local), n_real,
@@ -572,6 +656,40 @@ class S3Engine:
         if self.timing:
             self.cg_events.append((e0, self._ev(), n_pts))
         return lam, iters, status, hist, g
+
+    def _multi_tables(self, n_pts, force=False):
+        """Work tables of the multi-point CG (mfb_cg_multi), or None when the
+        one-CTA-per-point kernel is the right one: the point's blocks fit in
+        shared memory (staged once per point), there are too few points to
+        keep 8 per SM in flight, or the dof runs are not 16-byte aligned."""
+        torch, st, plan = self.torch, self.st, self.plan
+        nd = plan.ndof.astype(np.int64)
+        nl, n_rows = int(plan.n_lambda), int(plan.dof_ptr[-1])
+        staged = 8 * (int(np.sum(nd * nd)) + 6 * nl + 2 * n_rows) <= 200 * 1024
+        if (8 * 8 * nl + 4 * n_rows > 220 * 1024 or int(st.d_cg_local.shape[0]) > 64
+                or plan.n_sub >= 4095):
+            return None
+        if not force and (staged or n_pts < 4 * N_SMS):
+            return None
+        mt = getattr(st, "_multi", None)
+        if mt is None:
+            tab, sides, strips, pk_size = cg_tasks(plan.n_sub, nd, plan.dof_ptr, plan.dof_map,
+                                                   nl)
+            n_loc = st.n_loc.astype(np.int64)
+            pk_base = np.concatenate([[0], np.cumsum(pk_size.astype(np.int64) * n_loc)])
+            n_cta = N_SMS
+            scratch = int(self.L.mfb_cg_multi_scratch_doubles(nl, n_cta))
+            mt = {"tasks": _dev(tab.ravel(), torch.int32), "n_tasks": int(len(tab)),
+                  "sides": _dev(sides.ravel(), torch.int32), "n_cta": n_cta,
+                  "strips": _dev(strips.ravel(), torch.int32), "n_strips": int(len(strips)),
+                  "pk_size": _dev(pk_size, torch.int32), "pk_base": _dev(pk_base[:-1], torch.int64),
+                  "n_loc": _dev(n_loc.astype(np.int32), torch.int32),
+                  "max_loc": int(n_loc.max()),
+                  "packed": torch.empty(int(pk_base[-1]), dtype=torch.float64, device="cuda"),
+                  "scratch": torch.empty(scratch, dtype=torch.float64, device="cuda"),
+                  "counter": torch.zeros(1, dtype=torch.int32, device="cuda")}
+            st._multi = mt
+        return mt
 
     # ----------------------------------------------------- (4) moments ----
     def moments(self, lam, sids=None, with_lambda=True):

@@ -190,3 +190,31 @@ def test_cfg4_basis_blocks(gpu):
             assert err <= 1e-10, (key, err)
             checked += 1
     assert checked >= 6
+
+
+@pytest.mark.parametrize("name", ["cfg1", "case1_mini", "cfg2", "cfg3"])
+def test_multi_point_cg_matches_reference(gpu, name):
+    """The 8-points-per-CTA CG (mfb_cg_multi, the cfg4 kernel) forced on the
+    configs with reference goldens: lambda per point within 1e-8, same
+    statuses, converged residual histories, g equal to the recorded rhs."""
+    z = golden(name)
+    _, problem, grid, _ = case_from_golden(name)
+    plan, eng = _engine(problem, grid)
+    max_iter = max(50, 10 * plan.n_lambda)
+    lam, iters, status, hist, g = eng.solve_points(TOL, max_iter, keep_g=True, kernel="multi")
+    assert np.all(status.cpu().numpy() == 0)
+    L = lam.cpu().numpy()
+    keep = z["s3_points"]
+    assert _rel(L[keep], z["s3_lambda"]) <= 1e-8
+    if "s3_g" in z:
+        gg = g.cpu().numpy()[keep]
+        assert np.max(np.abs(gg - z["s3_g"])) <= 1e-10 * np.max(np.abs(z["s3_g"]))
+    it = iters.cpu().numpy()
+    h = hist.cpu().numpy()
+    assert all(h[k, it[k] - 1] <= TOL for k in range(grid.n_real))
+    assert abs(it.mean() - z["s3_iters"].mean()) <= 0.05 * z["s3_iters"].mean() + 2
+    # the point's arithmetic does not depend on its slot / CTA / neighbours:
+    # a single point solved alone gives the same bits
+    k = int(grid.n_real // 2)
+    lam1, it1, _, _, _ = eng.solve_points(TOL, max_iter, k0=k, n_pts=1, kernel="multi")
+    assert np.array_equal(lam1.cpu().numpy()[0], L[k]) and int(it1.cpu()[0]) == int(it[k])
