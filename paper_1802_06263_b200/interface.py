@@ -36,7 +36,7 @@ log = logging.getLogger(__name__)
 
 METHODS = ("S1", "S2", "S3")
 _PLAN_CACHE = {}
-WORK_BUDGET_BYTES = 8 << 30
+WORK_BUDGET_BYTES = 16 << 30
 N_SMS = 148                 # B200
 BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 

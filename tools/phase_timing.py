@@ -1,6 +1,6 @@
-"""Per-phase device timing of one S3 sweep (CUDA events on the launch stream).
+"""Per-phase device timing of one S3 (or S2) sweep (CUDA events on the launch stream).
 
-usage: python tools/phase_timing.py cfg2 [--reps 2]
+usage: python tools/phase_timing.py cfg2 [--reps 2] [--method S2]
 """
 import argparse
 import os
@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-11)
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--darcy", default="hybrid", choices=["hybrid", "band"])
+    ap.add_argument("--method", default="S3", choices=["S3", "S2"])
     a = ap.parse_args()
     path = a.config if a.config.endswith(".json") else f"configs/{a.config}.json"
     t = time.time()
@@ -32,9 +33,9 @@ def main():
     plan = get_plan(problem, grid)
     t_plan = time.time() - t
     print(f"setup {t_setup:.2f}s plan {t_plan:.2f}s n_real {grid.n_real} "
-          f"n_lambda {plan.n_lambda} systems {len(plan.s3_systems())}", flush=True)
+          f"n_lambda {plan.n_lambda} method {a.method}", flush=True)
     for rep in range(a.reps):
-        eng = S3Engine(plan, darcy_kernel=a.darcy)
+        eng = S3Engine(plan, darcy_kernel=a.darcy, method=a.method)
         eng.timing = True
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
