@@ -40,6 +40,8 @@ def _args():
     ap.add_argument("--tol", type=float, default=1e-11)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-s2", action="store_true",
+                    help="skip the deterministic-MFB (S2) comparison sweep")
     return ap.parse_args()
 
 
@@ -126,6 +128,46 @@ def _traffic(kind, config):
     if not t or t.get("config") != config:
         return None, None
     return t["dram_bytes_per_launch"], t["source"]
+
+
+def s2_comparison(plan, problem, grid, tol, max_iter, flush, steps=2):
+    """BASELINE configs[1]: "compare deterministic MFB and stochastic MFB on
+    identical inputs" -- the same workload swept with Method S2 (a flux basis
+    per subdomain per realization, Stokes included) on the device, device
+    time per sweep (CUDA events, L2 flushed) and end to end via run_method."""
+    import torch
+    from paper_1802_06263_b200.interface import S3Engine, run_method
+
+    def sweep():
+        e = S3Engine(plan, method="S2")
+        e.kl_fields()
+        e.build_bases()
+        lam, iters, status, hist, _ = e.solve_points(tol, max_iter)
+        e.moments(lam)
+        return iters
+
+    sweep()
+    ms = []
+    for _ in range(steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        iters = sweep()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    run_method(problem, grid, method="S2", tol=tol)
+    t = time.perf_counter()
+    for _ in range(steps):
+        run_method(problem, grid, method="S2", tol=tol)
+    e2e = (time.perf_counter() - t) / steps
+    systems = plan.n_sub * grid.n_real
+    return {"method": "S2 (deterministic MFB)", "value": grid.n_real / (np.mean(ms) / 1e3),
+            "unit": "realizations/s", "ms_per_step": float(np.mean(ms)), "steps": steps,
+            "systems_per_sweep": systems, "cg_iters_mean": float(iters.float().mean().item()),
+            "e2e": {"value": grid.n_real / e2e, "unit": "realizations/s",
+                    "api": "run_method(problem, grid, 'S2', tol)"}}
 
 
 def cpu_baseline(cfg_path, tol, sample_points=None):
@@ -428,6 +470,8 @@ def run_ours(a):
                     "d2h_bytes_per_step": d2h, "api": "run_method(problem, grid, 'S3', tol)"},
             "clocks": clocks.summary(),
         }
+        if not a.no_s2 and ws == 1:
+            line["s2_comparison"] = s2_comparison(plan, problem, grid, a.tol, max_iter, flush)
         if not a.no_cpu_baseline and ws == 1:
             cb = cpu_baseline(cfg_path, a.tol)
             line["cpu_baseline"] = {

@@ -51,6 +51,7 @@ __device__ __forceinline__ double row_dot_r(const double *__restrict__ B, int nd
                                             const double *__restrict__ pr) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int c = 0;
+#pragma unroll 2
     for (; c + 4 <= nd; c += 4, B += 4 * nd) {
         a0 = fma(B[0], pr[c], a0);
         a1 = fma(B[nd], pr[c + 1], a1);
@@ -204,7 +205,6 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         const double a = rr / pSp;
         part = 0.0;
         for (int d = tid; d < n_lambda; d += NT) {
-            x[d] += a * p[d];
             const double rd = r[d] - a * Sp[d];
             r[d] = rd;
             part += rd * rd;
@@ -212,8 +212,10 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         CGP(4);
         const double rr_new = block_sum_alt(part, red2, rbuf);
         CGP(5);
+        for (int d = tid; d < n_lambda; d += NT) x[d] += a * p[d];   // p still this iteration's
         const double rn = sqrt(rr_new);
-        if (tid == 0 && it <= hist_cap) hist[it - 1] = rn / gnorm;
+        // rn now, rn / gnorm after the loop (keeps the division off the chain)
+        if (tid == 0 && it <= hist_cap) hist[it - 1] = rn;
         if (rn <= tol * gnorm) {
             status = MFB_CG_CONVERGED;
             it_done = it;
@@ -233,6 +235,9 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     }
     for (int d = tid; d < n_lambda; d += NT) lam[d] = x[d];
     if (tid == 0) { iters_out[pt] = it_done; status_out[pt] = status; }
+    __syncthreads();                              // tid 0's rn entries
+    const int nh = min(status == MFB_CG_NOT_SPD ? it_done - 1 : it_done, hist_cap);
+    for (int j = tid; j < nh; j += NT) hist[j] = hist[j] / gnorm;
 }
 
 
