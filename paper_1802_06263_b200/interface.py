@@ -489,6 +489,13 @@ class _S3Static:
         xi[1:] = pts
         return phi, mean, xi
 
+    def side_stream(self):
+        """Second stream for the banded (Stokes) waves of build_bases."""
+        if getattr(self, "_side", None) is None:
+            import torch
+            self._side = torch.cuda.Stream()
+        return self._side
+
     def refresh_inputs(self):
         """Re-upload the sweep's inputs from the host: collocation weights, local
         index tables and the KL tables (Phi, mean, local points). Returns bytes."""
@@ -529,9 +536,9 @@ class S3Engine:
     def __getattr__(self, name):     # pools live in the static state
         return getattr(self.__dict__["st"], name)
 
-    def _ev(self):
+    def _ev(self, stream=None):
         ev = self.torch.cuda.Event(enable_timing=True)
-        ev.record(self.stream)
+        ev.record(self.stream if stream is None else stream)
         return ev
 
     # ------------------------------------------------------------ (1) KL --
@@ -552,25 +559,37 @@ class S3Engine:
 
     # ------------------------------------------------------- (2) bases ----
     def build_bases(self, sids=None):
+        """Every (subdomain, realization) system of the sweep. The banded
+        (Stokes) waves run on a second stream, concurrently with the Darcy
+        condensation on the engine's stream: the cooperative Stokes solve is
+        latency bound and leaves SMs free. Both write disjoint pool slices;
+        the engine's stream waits for the side stream before returning."""
+        torch = self.torch
         st, plan = self.st, self.plan
         waves, hwaves = st.waves_for(sids)
         self._last_waves = list(waves) + list(hwaves)
+        side = None
+        if waves and hwaves:
+            side = st.side_stream()
+            side.wait_stream(self.stream)           # K from the KL launches
+        bs = side if side is not None else self.stream
+        sp_b = ctypes.c_void_p(bs.cuda_stream)
         for w in waves:                         # generic banded LU (Stokes)
             cnt = len(w["idx"])
             if self.timing:
-                e0 = self._ev()
+                e0 = self._ev(bs)
             _lib.check(self.L.mfb_systems_solve(
                 _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
                 _ptr(st.work), _ptr(w["woff"]), _ptr(st.X), _ptr(w["xoff"]), _ptr(w["info"]),
-                w["nt"], st.smem, w["group"], _ptr(st.bar), self.sp), "mfb_systems_solve")
+                w["nt"], st.smem, w["group"], _ptr(st.bar), sp_b), "mfb_systems_solve")
             if self.timing:
-                self.solve_events.append(("band", e0, self._ev(), w["flops"], w["flops"]))
+                self.solve_events.append(("band", e0, self._ev(bs), w["flops"], w["flops"]))
             self.launches += 2
             _lib.check(self.L.mfb_systems_extract(
                 _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.X), _ptr(w["xoff"]),
                 _ptr(st.blocks), _ptr(w["boff"]), _ptr(st.hbar), _ptr(w["hoff"]),
                 _ptr(st.M) if st.keep_fields else None, _ptr(w["moff"]),
-                _ptr(st.Fb) if st.keep_fields else None, _ptr(w["fboff"]), self.sp),
+                _ptr(st.Fb) if st.keep_fields else None, _ptr(w["fboff"]), sp_b),
                 "mfb_systems_extract")
         for w in hwaves:                        # hybridised Darcy condensation
             cnt = len(w["idx"])
@@ -596,6 +615,10 @@ class S3Engine:
                     _ptr(plan.hyb_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
                     _ptr(st.HX), _ptr(w["xoff"]), _ptr(st.M), _ptr(w["moff"]), _ptr(st.Fb),
                     _ptr(w["fboff"]), self.sp), "mfb_darcy_recover")
+        if side is not None:
+            self.stream.wait_stream(side)
+            # the side stream's allocations-in-flight: none (all buffers are
+            # the static pools), so no record_stream bookkeeping is needed
 
     def check_info(self):
         info = np.zeros(len(self.st.systems), dtype=np.int64)
