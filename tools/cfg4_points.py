@@ -34,22 +34,32 @@ def main():
     torch.cuda.synchronize()
     print(f"bases {1e3 * (time.time() - t):.1f} ms")
     nl = plan.n_lambda
-    for k in pts:
-        torch.cuda.synchronize()
-        t = time.time()
-        lam, iters, status, hist, _ = eng.solve_points(1e-11, max(50, 10 * nl), k0=k, n_pts=1,
-                                                       hist_cap=1)
-        torch.cuda.synchronize()
-        dt = time.time() - t
-        lam = lam.cpu().numpy()[0]
-        it, st = int(iters.cpu().numpy()[0]), int(status.cpu().numpy()[0])
-        msg = f"point {k}: {it} iterations, status {st}, {1e3 * dt:.0f} ms"
-        if z is not None and k in list(z["points"]):
-            j = list(z["points"]).index(k)
-            ref = z["lambda"][j]
-            msg += (f", lambda rel err {np.linalg.norm(lam - ref) / np.linalg.norm(ref):.2e}"
-                    f" (ref {int(z['iters'][j])} iterations)")
-        print(msg, flush=True)
+    kernels = ["cta", "multi"]
+    for kern in kernels:
+        for k in pts:
+            torch.cuda.synchronize()
+            t = time.time()
+            lam, iters, status, hist, _ = eng.solve_points(1e-11, max(50, 10 * nl), k0=k,
+                                                           n_pts=1, kernel=kern)
+            torch.cuda.synchronize()
+            dt = time.time() - t
+            lam = lam.cpu().numpy()[0]
+            it, st = int(iters.cpu().numpy()[0]), int(status.cpu().numpy()[0])
+            h = hist.cpu().numpy()[0]
+            msg = f"[{kern}] point {k}: {it} iterations, status {st}, {1e3 * dt:.0f} ms"
+            if z is not None and k in list(z["points"]):
+                j = list(z["points"]).index(k)
+                ref = z["lambda"][j]
+                head = z["res_head"][j]
+                rel = np.abs(h[:len(head)] - head[:min(len(head), it)]) / head[:min(len(head), it)] \
+                    if it >= len(head) else np.abs(h[:it] - head[:it]) / head[:it]
+                first = int(np.argmax(rel > 1e-6)) if np.any(rel > 1e-6) else len(rel)
+                msg += (f", lambda rel err {np.linalg.norm(lam - ref) / np.linalg.norm(ref):.2e}"
+                        f" (ref {int(z['iters'][j])} iterations, converged "
+                        f"{bool(z['converged'][j])}); residual head agrees to 1e-6 for the "
+                        f"first {first} iterations, last residual {h[min(it, h.shape[0]) - 1]:.3e}"
+                        f" (ref {float(z['last_residual'][j]):.3e})")
+            print(msg, flush=True)
 
 
 if __name__ == "__main__":
