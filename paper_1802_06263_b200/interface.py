@@ -476,7 +476,14 @@ class _S3Static:
         return self._wave_cache[key]
 
     def _kl_tables(self, plan, s):
-        """Phi, mean and the xi rows (row 0 = the mean field) of Darcy sid s."""
+        """Phi, mean and the xi rows (row 0 = the mean field) of Darcy sid s
+        (host arrays, evaluated once per plan like the rest of the setup)."""
+        cache = self.__dict__.setdefault("_kl_host", {})
+        if s not in cache:
+            cache[s] = self._kl_tables_eval(plan, s)
+        return cache[s]
+
+    def _kl_tables_eval(self, plan, s):
         pb, grid = plan.problem, plan.grid
         r = pb.layout.blocks[s].kl_region
         c = pb.meshes[s].centroids
@@ -497,22 +504,40 @@ class _S3Static:
         return self._side
 
     def refresh_inputs(self):
-        """Re-upload the sweep's inputs from the host: collocation weights, local
-        index tables and the KL tables (Phi, mean, local points). Returns bytes."""
+        """Re-upload the sweep's inputs from the host -- collocation weights,
+        local-index tables and the KL tables (Phi, mean, local points) -- in
+        ONE pinned host->device copy, then device-side copies into place.
+        Returns the bytes transferred."""
         import torch
         plan, grid = self._plan, self._plan.grid
-        nbytes = 0
         li = np.stack(grid.local_indices).astype(np.int32) if grid.local_indices else \
             np.zeros((1, grid.n_real), dtype=np.int32)
-        plan.d_local.copy_(torch.from_numpy(li))
-        plan.d_weights.copy_(torch.from_numpy(np.ascontiguousarray(grid.weights)))
-        nbytes += li.nbytes + grid.weights.nbytes
-        for s, nc, nt, d_phi, d_mean, d_xi, *_ in self.kl:
-            phi, mean, xi = self._kl_tables(plan, s)
-            for d, h in ((d_phi, phi), (d_mean, mean), (d_xi, xi)):
-                d.copy_(torch.from_numpy(np.ascontiguousarray(h)).view(d.shape))
-                nbytes += h.nbytes
-        return nbytes
+        pieces = [(plan.d_local, li), (plan.d_weights, np.ascontiguousarray(grid.weights))]
+        for s_, nc, nt, d_phi, d_mean, d_xi, *_ in self.kl:
+            phi, mean, xi = self._kl_tables(plan, s_)
+            pieces += [(d_phi, phi), (d_mean, mean), (d_xi, xi)]
+        stage = getattr(self, "_stage", None)
+        if stage is None:
+            offs, off = [], 0
+            for _, h in pieces:
+                offs.append(off)
+                off += (h.nbytes + 15) // 16 * 16
+            host = torch.empty(max(off, 16), dtype=torch.uint8, pin_memory=True)
+            dev = torch.empty(max(off, 16), dtype=torch.uint8, device="cuda")
+            stage = self._stage = (offs, off, host, dev)
+        offs, total, host, dev = stage
+        ev = getattr(self, "_stage_ev", None)
+        if ev is not None:
+            ev.synchronize()                     # the previous upload left the pinned buffer
+        hv = host.numpy()
+        for (_, h), o in zip(pieces, offs):
+            hv[o:o + h.nbytes] = np.frombuffer(np.ascontiguousarray(h).tobytes(), dtype=np.uint8)
+        dev.copy_(host, non_blocking=True)
+        self._stage_ev = torch.cuda.Event()
+        self._stage_ev.record()
+        for (d, h), o in zip(pieces, offs):
+            d.view(-1).copy_(dev[o:o + h.nbytes].view(d.dtype))
+        return int(total)
 
 
 class S3Engine:
@@ -530,6 +555,7 @@ class S3Engine:
         self.launches = 0            # kernels launched through the C ABI
         self.timing = False          # record CUDA events around the basis solves and CG
         self.solve_events = []
+        self.bases_events = []
         self.cg_events = []
         self.solve_flops = []
 
@@ -568,6 +594,8 @@ class S3Engine:
         st, plan = self.st, self.plan
         waves, hwaves = st.waves_for(sids)
         self._last_waves = list(waves) + list(hwaves)
+        if self.timing:
+            eb0 = self._ev()
         side = None
         if waves and hwaves:
             side = st.side_stream()
@@ -619,6 +647,8 @@ class S3Engine:
             self.stream.wait_stream(side)
             # the side stream's allocations-in-flight: none (all buffers are
             # the static pools), so no record_stream bookkeeping is needed
+        if self.timing:                 # wall time of the whole basis phase
+            self.bases_events.append((eb0, self._ev()))
 
     def check_info(self):
         info = np.zeros(len(self.st.systems), dtype=np.int64)
