@@ -176,13 +176,16 @@ int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
  * [hist_cap] (entries beyond hist_cap are dropped), g (may be NULL).
  * stage_doubles: sum_i ndof_i^2; when the point's blocks fit (200 KiB of
  * shared memory with the vectors) they are staged per point (0: never).
+ * reg_ndof: max_i ndof_i when every ndof_i is a multiple of 4 (else 0):
+ * with reg_ndof <= 32 and 2 n_lambda <= 640 every block row lives in one
+ * thread's registers for the whole solve and nothing is staged.
  */
 int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
                    const int *dof_map, const int *region, const long long *blk_base,
                    const long long *h_base, const int *local_idx, int n_real,
                    const double *blocks, const double *hbar, int k0, int n_pts,
                    double tol, int max_iter, double *lam, int *iters, int *status,
-                   double *res_hist, int hist_cap, double *g, long long stage_doubles,
+                   double *res_hist, int hist_cap, double *g, long long stage_doubles, int reg_ndof,
                    void *stream);
 
 /*

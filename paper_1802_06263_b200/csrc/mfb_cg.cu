@@ -69,7 +69,14 @@ __device__ __forceinline__ double row_dot_r(const double *__restrict__ B, int nd
 // (stage = sum_i nd_i^2 doubles) and the dof lists are copied to shared
 // memory once, so every iteration's GEMV reads shared memory only; the row's
 // dot product runs with four independent accumulators.
-__global__ void __launch_bounds__(CG_NT_MAX)
+//
+// RN > 0 (register rows): one row per thread and the thread's row of its
+// basis block held in registers for the whole solve (RN >= max ndof, zero
+// padded), so an iteration's GEMV reads only p (shared memory, broadcast
+// within a block's rows) -- the blocks are read from L2 once per point and
+// never staged. Same accumulation order as row_dot_r (ndof % 4 == 0).
+template <int RN>
+__global__ void __launch_bounds__(RN > 0 ? 640 : CG_NT_MAX)
 cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
           const int *__restrict__ dof_ptr, const int *__restrict__ dof_map,
           const int *__restrict__ region, const long long *__restrict__ blk_base,
@@ -92,7 +99,8 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     double *sB = Sp + n_lambda;                                       // staged blocks
     double *rowval = sB + stage;                                      // row results
     double *prow = rowval + nrows;                                    // p in row space
-    int *rb = reinterpret_cast<int *>(prow + (use_prow ? nrows : 0)); // block base + a
+    // prow carries RN zero doubles of padding: a register row reads RN entries
+    int *rb = reinterpret_cast<int *>(prow + (use_prow ? nrows + RN : 0)); // block base + a
     int *rmeta = rb + nrows;                                          // dof offset | nd << 20
     int *sdm = rmeta + nrows;                                         // dof lists (no prow)
     int *sbo = sdm + (use_prow ? 0 : nrows);                          // staged block offsets
@@ -114,6 +122,7 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     if (!use_prow)
         for (int d = tid; d < nrows; d += NT) sdm[d] = dof_map[d];
     for (int d = tid; d < n_lambda; d += NT) { side0[d] = 0x7fffffff; side1[d] = -1; }
+    if (RN > 0 && tid < RN) prow[nrows + tid] = 0.0;
     __syncthreads();
     for (int row = tid; row < nrows; row += NT) {
         atomicMin(&side0[dof_map[row]], row);
@@ -134,6 +143,18 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         }
     }
     __syncthreads();
+    double breg[RN > 0 ? RN : 1];
+    int rd0 = 0;
+    if constexpr (RN > 0) {             // this thread's block row, column by column
+        const int row = tid;
+        const int meta = row < nrows ? rmeta[row] : 0;
+        const int nd = meta >> 20;
+        rd0 = meta & 0xFFFFF;
+        const double *Bp = blocks + (row < nrows ? rb[row] : 0);
+#pragma unroll
+        for (int c = 0; c < RN; ++c)
+            breg[c] = c < nd ? __ldg(Bp + (long long)c * nd) : 0.0;
+    }
     for (int i = wid; i < n_sub; i += NT / 32) {
         const int nd = ndof[i];
         const int loc = region[i] < 0 ? 0 : local_idx[(long long)region[i] * n_real + k];
@@ -173,7 +194,20 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         // its two sides (0 + a + b of basis_apply, order free in IEEE) ------
         __syncthreads();                         // p of the previous iteration
         CGP(1);
-        if (use_prow) {
+        if constexpr (RN > 0) {
+            if (tid < nrows) {
+                const double *pr = prow + rd0;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                for (int c = 0; c < RN; c += 4) {
+                    a0 = fma(breg[c], pr[c], a0);
+                    a1 = fma(breg[c + 1], pr[c + 1], a1);
+                    a2 = fma(breg[c + 2], pr[c + 2], a2);
+                    a3 = fma(breg[c + 3], pr[c + 3], a3);
+                }
+                rowval[tid] = (a0 + a1) + (a2 + a3);
+            }
+        } else if (use_prow) {
             const double *Bs = stage > 0 ? sB : blocks;
             for (int row = tid; row < nrows; row += NT) {
                 const int meta = rmeta[row];
@@ -260,7 +294,7 @@ extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const in
                               const double *hbar, int k0, int n_pts, double tol,
                               int max_iter, double *lam, int *iters, int *status,
                               double *res_hist, int hist_cap, double *g,
-                              long long stage_doubles, void *stream) {
+                              long long stage_doubles, int reg_ndof, void *stream) {
     if (n_pts <= 0) return n_pts == 0 ? MFB_OK : MFB_ERR_ARG;
     // every mortar dof has two sides: the stacked block rows number 2 n_lambda
     const int nrows = 2 * n_lambda;
@@ -275,16 +309,33 @@ extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const in
     int use_prow = smem + (size_t)nrows * 8 <= 200 * 1024;
     smem += use_prow ? (size_t)nrows * 8 : (size_t)nrows * 4;
     long long stage = stage_doubles;
+    // register rows: every row on its own thread (one row per thread, at
+    // most 640 threads for the register budget), max ndof <= 32 and a
+    // multiple of 4; then nothing is staged
+    const int rn = (reg_ndof <= 16 ? 16 : 32);
+    const bool regs = use_prow && reg_ndof > 0 && reg_ndof <= 32 && nrows <= 640;
+    if (regs) {
+        stage = 0;
+        smem += (size_t)rn * 8;
+    }
     if (stage < 0 || smem + (size_t)stage * sizeof(double) > 200 * 1024) stage = 0;
     smem += (size_t)stage * sizeof(double);
     if (smem > 227 * 1024) return MFB_ERR_SMEM;
-    if (cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return MFB_ERR_SMEM;
-    cg_kernel<<<n_pts, nt, smem, mfb_stream(stream)>>>(
-        n_lambda, n_sub, ndof, dof_ptr, dof_map, region, blk_base, h_base, local_idx, n_real,
-        blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, g, stage,
-        use_prow);
+    cudaStream_t st = mfb_stream(stream);
+#define MFB_CG_LAUNCH(R)                                                                    \
+    do {                                                                                    \
+        if (cudaFuncSetAttribute(cg_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)smem) != cudaSuccess)                                 \
+            return MFB_ERR_SMEM;                                                            \
+        cg_kernel<R><<<n_pts, nt, smem, st>>>(                                              \
+            n_lambda, n_sub, ndof, dof_ptr, dof_map, region, blk_base, h_base, local_idx,   \
+            n_real, blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, \
+            g, stage, use_prow);                                                            \
+    } while (0)
+    if (!regs) MFB_CG_LAUNCH(0);
+    else if (rn == 16) MFB_CG_LAUNCH(16);
+    else MFB_CG_LAUNCH(32);
+#undef MFB_CG_LAUNCH
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }

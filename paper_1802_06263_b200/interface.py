@@ -665,8 +665,10 @@ class S3Engine:
     def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False,
                      kernel="auto"):
         """CG over points k0..k0+n_pts-1. kernel: "auto" (multi-point when the
-        blocks exceed shared memory and the points fill the GPU), "cta" (one
-        CTA per point) or "multi" (forced, for tests)."""
+        blocks exceed shared memory and the points fill the GPU, else one CTA
+        per point with register-resident block rows when they fit), "cta"
+        (one CTA per point), "staged" (one CTA per point, blocks staged in
+        shared memory) or "multi" (forced, for tests)."""
         torch, plan, st = self.torch, self.plan, self.st
         n_real = plan.grid.n_real
         n_pts = n_real - k0 if n_pts is None else n_pts
@@ -680,7 +682,8 @@ class S3Engine:
         self.launches += 1
         if self.timing:
             e0 = self._ev()
-        mt = None if kernel == "cta" else self._multi_tables(n_pts, force=kernel == "multi")
+        mt = None if kernel in ("cta", "staged") else self._multi_tables(n_pts,
+                                                                      force=kernel == "multi")
         if mt is not None:
             self.launches += 1
             _lib.check(self.L.mfb_cg_pack(
@@ -699,13 +702,17 @@ class S3Engine:
             if self.timing:
                 self.cg_events.append((e0, self._ev(), n_pts))
             return lam, iters, status, hist, g
+        # block rows in registers when every ndof is a multiple of 4 (the
+        # accumulation order then equals the staged kernel's)
+        reg_ndof = int(plan.ndof.max()) if (kernel != "staged" and len(plan.ndof)
+                                             and not np.any(plan.ndof % 4)) else 0
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
             _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(st.d_cg_local), n_real,
             _ptr(st.blocks), _ptr(st.hbar), k0, n_pts, float(tol), int(max_iter),
             _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
             _ptr(g) if keep_g else None, int(np.sum(plan.ndof.astype(np.int64) ** 2)),
-            self.sp), "mfb_cg_batched")
+            reg_ndof, self.sp), "mfb_cg_batched")
         if self.timing:
             self.cg_events.append((e0, self._ev(), n_pts))
         return lam, iters, status, hist, g

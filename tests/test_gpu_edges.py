@@ -99,7 +99,7 @@ def test_band_solver_zero_pivot_ends_every_cta(gpu, group):
     assert info == 78
 
 
-def _cg(blocks, hbar, nd, n_lambda, max_iter, tol=1e-12, stage=True):
+def _cg(blocks, hbar, nd, n_lambda, max_iter, tol=1e-12, stage=True, regs=False):
     import torch
 
     from paper_1802_06263_b200 import _lib
@@ -122,16 +122,19 @@ def _cg(blocks, hbar, nd, n_lambda, max_iter, tol=1e-12, stage=True):
         n_lambda, n_sub, _ptr(t["ndof"]), _ptr(t["dof_ptr"]), _ptr(t["dof_map"]),
         _ptr(t["region"]), _ptr(t["blk"]), _ptr(t["h"]), _ptr(t["loc"]), 1, _ptr(t["blocks"]),
         _ptr(t["hbar"]), 0, 1, tol, max_iter, _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist),
-        max(max_iter, 1), None, int(sum(k * k for k in nd)) if stage else 0, None),
+        max(max_iter, 1), None, int(sum(k * k for k in nd)) if stage else 0,
+        max(nd) if regs and all(k % 4 == 0 for k in nd) else 0, None),
         "mfb_cg_batched")
     torch.cuda.synchronize()
     return lam.cpu().numpy(), int(iters.item()), int(status.item()), hist.cpu().numpy()
 
 
-@pytest.mark.parametrize("stage", [True, False])
-def test_cg_status_paths(gpu, stage):
+@pytest.mark.parametrize("stage,regs", [(True, False), (False, False), (False, True)])
+def test_cg_status_paths(gpu, stage, regs):
+    """Staged blocks, blocks read from L2, and block rows in registers (the
+    latter needs ndof % 4 == 0)."""
     rng = np.random.default_rng(3)
-    nl = 5
+    nl = 8 if regs else 5
     nd = [nl, nl]                                  # two sides of every dof
     M1 = rng.standard_normal((nl, nl))
     M2 = rng.standard_normal((nl, nl))
@@ -139,19 +142,19 @@ def test_cg_status_paths(gpu, stage):
     blocks = np.concatenate([B1.T.ravel(), B2.T.ravel()])    # column-major storage
     h = rng.standard_normal(2 * nl)
     # converged, against a dense solve of (B1 + B2) lam = h1 + h2
-    lam, it, status, hist = _cg(blocks, h, nd, nl, 50, stage=stage)
+    lam, it, status, hist = _cg(blocks, h, nd, nl, 50, stage=stage, regs=regs)
     ref = np.linalg.solve(B1 + B2, h[:nl] + h[nl:])
     assert status == 0 and 1 <= it <= 50
     assert np.max(np.abs(lam - ref)) / np.max(np.abs(ref)) <= 1e-10
     assert hist[it - 1] <= 1e-12
     # zero rhs: no iterations, lambda = 0 (interface.py:111-113)
-    lam, it, status, _ = _cg(blocks, np.zeros(2 * nl), nd, nl, 50, stage=stage)
+    lam, it, status, _ = _cg(blocks, np.zeros(2 * nl), nd, nl, 50, stage=stage, regs=regs)
     assert status == 3 and it == 0 and not lam.any()
     # breakdown on a negative definite operator (interface.py:123-126)
-    _, it, status, _ = _cg(-blocks, h, nd, nl, 50, stage=stage)
+    _, it, status, _ = _cg(-blocks, h, nd, nl, 50, stage=stage, regs=regs)
     assert status == 1 and it == 1
     # budget exhausted (interface.py:137-139)
-    _, it, status, hist = _cg(blocks, h, nd, nl, 2, stage=stage)
+    _, it, status, hist = _cg(blocks, h, nd, nl, 2, stage=stage, regs=regs)
     assert status == 2 and it == 2 and hist[1] > 1e-12
 
 
@@ -161,7 +164,7 @@ def test_empty_launches_are_noops(gpu):
     z = ctypes.c_void_p(0)
     assert L.mfb_systems_solve(z, 0, z, z, z, z, z, z, z, z, 256, 0, 1, z, None) == 0
     assert L.mfb_cg_batched(4, 1, z, z, z, z, z, z, z, 1, z, z, 0, 0, 1e-9, 10, z, z, z, z, 1,
-                            z, 0, None) == 0
+                            z, 0, 0, None) == 0
     assert L.mfb_systems_solve(z, -1, z, z, z, z, z, z, z, z, 256, 0, 1, z, None) == 1
 
 
