@@ -69,14 +69,7 @@ __device__ __forceinline__ double row_dot_r(const double *__restrict__ B, int nd
 // (stage = sum_i nd_i^2 doubles) and the dof lists are copied to shared
 // memory once, so every iteration's GEMV reads shared memory only; the row's
 // dot product runs with four independent accumulators.
-//
-// RN > 0 (register rows): one row per thread and the thread's row of its
-// basis block held in registers for the whole solve (RN >= max ndof, zero
-// padded), so an iteration's GEMV reads only p (shared memory, broadcast
-// within a block's rows) -- the blocks are read from L2 once per point and
-// never staged. Same accumulation order as row_dot_r (ndof % 4 == 0).
-template <int RN>
-__global__ void __launch_bounds__(RN > 0 ? 640 : CG_NT_MAX)
+__global__ void __launch_bounds__(CG_NT_MAX)
 cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
           const int *__restrict__ dof_ptr, const int *__restrict__ dof_map,
           const int *__restrict__ region, const long long *__restrict__ blk_base,
@@ -99,8 +92,7 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     double *sB = Sp + n_lambda;                                       // staged blocks
     double *rowval = sB + stage;                                      // row results
     double *prow = rowval + nrows;                                    // p in row space
-    // prow carries RN zero doubles of padding: a register row reads RN entries
-    int *rb = reinterpret_cast<int *>(prow + (use_prow ? nrows + RN : 0)); // block base + a
+    int *rb = reinterpret_cast<int *>(prow + (use_prow ? nrows : 0)); // block base + a
     int *rmeta = rb + nrows;                                          // dof offset | nd << 20
     int *sdm = rmeta + nrows;                                         // dof lists (no prow)
     int *sbo = sdm + (use_prow ? 0 : nrows);                          // staged block offsets
@@ -122,7 +114,6 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     if (!use_prow)
         for (int d = tid; d < nrows; d += NT) sdm[d] = dof_map[d];
     for (int d = tid; d < n_lambda; d += NT) { side0[d] = 0x7fffffff; side1[d] = -1; }
-    if (RN > 0 && tid < RN) prow[nrows + tid] = 0.0;
     __syncthreads();
     for (int row = tid; row < nrows; row += NT) {
         atomicMin(&side0[dof_map[row]], row);
@@ -143,18 +134,6 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         }
     }
     __syncthreads();
-    double breg[RN > 0 ? RN : 1];
-    int rd0 = 0;
-    if constexpr (RN > 0) {             // this thread's block row, column by column
-        const int row = tid;
-        const int meta = row < nrows ? rmeta[row] : 0;
-        const int nd = meta >> 20;
-        rd0 = meta & 0xFFFFF;
-        const double *Bp = blocks + (row < nrows ? rb[row] : 0);
-#pragma unroll
-        for (int c = 0; c < RN; ++c)
-            breg[c] = c < nd ? __ldg(Bp + (long long)c * nd) : 0.0;
-    }
     for (int i = wid; i < n_sub; i += NT / 32) {
         const int nd = ndof[i];
         const int loc = region[i] < 0 ? 0 : local_idx[(long long)region[i] * n_real + k];
@@ -194,20 +173,7 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         // its two sides (0 + a + b of basis_apply, order free in IEEE) ------
         __syncthreads();                         // p of the previous iteration
         CGP(1);
-        if constexpr (RN > 0) {
-            if (tid < nrows) {
-                const double *pr = prow + rd0;
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-                for (int c = 0; c < RN; c += 4) {
-                    a0 = fma(breg[c], pr[c], a0);
-                    a1 = fma(breg[c + 1], pr[c + 1], a1);
-                    a2 = fma(breg[c + 2], pr[c + 2], a2);
-                    a3 = fma(breg[c + 3], pr[c + 3], a3);
-                }
-                rowval[tid] = (a0 + a1) + (a2 + a3);
-            }
-        } else if (use_prow) {
+        if (use_prow) {
             const double *Bs = stage > 0 ? sB : blocks;
             for (int row = tid; row < nrows; row += NT) {
                 const int meta = rmeta[row];
@@ -276,6 +242,140 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
 
 
 
+// Register rows, paired: thread 2d + side holds the block row of mortar dof
+// d's lower (side 0) or upper (side 1) subdomain in registers, so S p[d] =
+// row_lower + row_upper is one shuffle inside the warp (basis_apply's
+// ascending-sid scatter from zero; an absent side is an all-zero row), and
+// x, r, p of dof d live in the even thread's registers. Per iteration: one
+// barrier for p, the GEMV from registers against p in row space (shared
+// memory), and the two reductions -- three barriers in all.
+template <int RN>
+__global__ void __launch_bounds__(608)
+cg_pair_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
+               const int *__restrict__ dof_ptr, const int *__restrict__ dof_map,
+               const int *__restrict__ region, const long long *__restrict__ blk_base,
+               const long long *__restrict__ h_base, const int *__restrict__ local_idx,
+               int n_real, const double *__restrict__ blocks, const double *__restrict__ hbar,
+               int k0, double tol, int max_iter, double *__restrict__ lam_out,
+               int *__restrict__ iters_out, int *__restrict__ status_out,
+               double *__restrict__ res_hist, int hist_cap, double *__restrict__ g_out) {
+    extern __shared__ double sm[];
+    __shared__ double red2[2 * (CG_NT_MAX / 32)];
+    int rbuf = 0;
+    const int NT = blockDim.x;
+    const int nrows = dof_ptr[n_sub];
+    double *r0 = sm;                                            // rhs assembly, n_lambda
+    double *prow = r0 + n_lambda;                               // p in row space (+RN pad)
+    long long *rb = reinterpret_cast<long long *>(prow + nrows + RN);   // block row base
+    int *rmeta = reinterpret_cast<int *>(rb + nrows);           // dof offset | nd << 20
+    int *side0 = rmeta + nrows;                                 // rows of dof d
+    int *side1 = side0 + n_lambda;
+    const int pt = blockIdx.x;
+    const int k = k0 + pt;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+
+    for (int d = tid; d < n_lambda; d += NT) { r0[d] = 0.0; side0[d] = 0x7fffffff; side1[d] = -1; }
+    if (tid < RN) prow[nrows + tid] = 0.0;
+    __syncthreads();
+    for (int row = tid; row < nrows; row += NT) {
+        atomicMin(&side0[dof_map[row]], row);
+        atomicMax(&side1[dof_map[row]], row);
+    }
+    for (int i = wid; i < n_sub; i += NT / 32) {
+        const int nd = ndof[i], d0 = dof_ptr[i];
+        const int loc = region[i] < 0 ? 0 : local_idx[(long long)region[i] * n_real + k];
+        const long long bb = blk_base[i] + (long long)loc * nd * nd;
+        for (int a = lane; a < nd; a += 32) {
+            rb[d0 + a] = bb + a;
+            rmeta[d0 + a] = d0 | (nd << 20);
+        }
+        const double *h = hbar + h_base[i] + (long long)loc * nd;
+        const int *dm = dof_map + d0;
+        // 0 + a + b: two contributions per dof, order free in IEEE
+        for (int a = lane; a < nd; a += 32) atomicAdd(&r0[dm[a]], h[a]);
+    }
+    __syncthreads();
+    const int d = tid >> 1, sd = tid & 1;
+    const bool own = d < n_lambda;
+    int row = -1;
+    if (own) {
+        const int s0 = side0[d], s1 = side1[d];
+        row = sd == 0 ? s0 : (s1 != s0 ? s1 : -1);
+    }
+    double breg[RN];
+    int rd0 = 0;
+    {
+        const int meta = row >= 0 ? rmeta[row] : 0;
+        const int nd = row >= 0 ? (meta >> 20) : 0;
+        rd0 = meta & 0xFFFFF;
+        const double *Bp = blocks + (row >= 0 ? rb[row] : 0);
+#pragma unroll
+        for (int c = 0; c < RN; ++c) breg[c] = c < nd ? __ldg(Bp + (long long)c * nd) : 0.0;
+    }
+    const bool head = own && sd == 0;           // the dof's state lives here
+    double x = 0.0, r = 0.0, pd = 0.0;
+    const double g = own ? r0[d] : 0.0;
+    if (head) {
+        r = g;
+        pd = g;
+        if (g_out) g_out[(long long)pt * n_lambda + d] = g;
+    }
+    if (row >= 0) prow[row] = g;
+    double rr = block_sum_alt(head ? g * g : 0.0, red2, rbuf);
+    const double gnorm = sqrt(rr);
+    double *lam = lam_out + (long long)pt * n_lambda;
+    if (gnorm == 0.0) {
+        if (head) lam[d] = 0.0;
+        if (tid == 0) { iters_out[pt] = 0; status_out[pt] = MFB_CG_ZERO_RHS; }
+        return;
+    }
+    double *hist = res_hist + (long long)pt * hist_cap;
+    int status = MFB_CG_MAX_ITER, it_done = max_iter;
+    for (int it = 1; it <= max_iter; ++it) {
+        __syncthreads();                          // p (row space) of this iteration
+        const double *pr = prow + rd0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int c = 0; c < RN; c += 4) {
+            a0 = fma(breg[c], pr[c], a0);
+            a1 = fma(breg[c + 1], pr[c + 1], a1);
+            a2 = fma(breg[c + 2], pr[c + 2], a2);
+            a3 = fma(breg[c + 3], pr[c + 3], a3);
+        }
+        const double v = (a0 + a1) + (a2 + a3);
+        const double vu = __shfl_down_sync(0xffffffffu, v, 1);
+        const double sp = v + vu;                 // lower + upper (even threads)
+        const double pSp = block_sum_alt(head ? pd * sp : 0.0, red2, rbuf);
+        if (!(pSp > 0.0)) {
+            status = MFB_CG_NOT_SPD;
+            it_done = it;
+            break;
+        }
+        const double a = rr / pSp;
+        r -= a * sp;
+        const double rr_new = block_sum_alt(head ? r * r : 0.0, red2, rbuf);
+        x += a * pd;
+        const double rn = sqrt(rr_new);
+        // rn now, rn / gnorm after the loop (keeps the division off the chain)
+        if (tid == 0 && it <= hist_cap) hist[it - 1] = rn;
+        if (rn <= tol * gnorm) {
+            status = MFB_CG_CONVERGED;
+            it_done = it;
+            break;
+        }
+        const double beta = rr_new / rr;
+        pd = r + beta * pd;
+        const double pv = __shfl_sync(0xffffffffu, pd, lane & ~1);
+        if (row >= 0) prow[row] = pv;
+        rr = rr_new;
+    }
+    if (head) lam[d] = x;
+    if (tid == 0) { iters_out[pt] = it_done; status_out[pt] = status; }
+    __syncthreads();                              // tid 0's rn entries
+    const int nh = min(status == MFB_CG_NOT_SPD ? it_done - 1 : it_done, hist_cap);
+    for (int j = tid; j < nh; j += NT) hist[j] = hist[j] / gnorm;
+}
+
 }  // namespace
 
 extern "C" int mfb_debug_cgprof(unsigned long long *out) {
@@ -309,33 +409,43 @@ extern "C" int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const in
     int use_prow = smem + (size_t)nrows * 8 <= 200 * 1024;
     smem += use_prow ? (size_t)nrows * 8 : (size_t)nrows * 4;
     long long stage = stage_doubles;
-    // register rows: every row on its own thread (one row per thread, at
-    // most 640 threads for the register budget), max ndof <= 32 and a
-    // multiple of 4; then nothing is staged
+    // register rows (cg_pair_kernel): one block row per thread, the two
+    // sides of a dof on adjacent lanes, at most 608 threads for the register
+    // budget, max ndof <= 32 and a multiple of 4; nothing is staged
     const int rn = (reg_ndof <= 16 ? 16 : 32);
-    const bool regs = use_prow && reg_ndof > 0 && reg_ndof <= 32 && nrows <= 640;
-    if (regs) {
-        stage = 0;
-        smem += (size_t)rn * 8;
-    }
+    const bool regs = use_prow && reg_ndof > 0 && reg_ndof <= 32 && nrows <= 608;
     if (stage < 0 || smem + (size_t)stage * sizeof(double) > 200 * 1024) stage = 0;
     smem += (size_t)stage * sizeof(double);
     if (smem > 227 * 1024) return MFB_ERR_SMEM;
     cudaStream_t st = mfb_stream(stream);
-#define MFB_CG_LAUNCH(R)                                                                    \
+#define MFB_CG_LAUNCH()                                                                     \
     do {                                                                                    \
-        if (cudaFuncSetAttribute(cg_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+        if (cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
                                  (int)smem) != cudaSuccess)                                 \
             return MFB_ERR_SMEM;                                                            \
-        cg_kernel<R><<<n_pts, nt, smem, st>>>(                                              \
+        cg_kernel<<<n_pts, nt, smem, st>>>(                                                 \
             n_lambda, n_sub, ndof, dof_ptr, dof_map, region, blk_base, h_base, local_idx,   \
             n_real, blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, \
             g, stage, use_prow);                                                            \
     } while (0)
-    if (!regs) MFB_CG_LAUNCH(0);
-    else if (rn == 16) MFB_CG_LAUNCH(16);
-    else MFB_CG_LAUNCH(32);
+#define MFB_CG_PAIR(R)                                                                      \
+    do {                                                                                    \
+        const size_t sm2 = (size_t)n_lambda * 8 + (size_t)(nrows + R) * 8 +                \
+                           (size_t)nrows * (8 + 4) + (size_t)n_lambda * 8 + 64;            \
+        if (cudaFuncSetAttribute(cg_pair_kernel<R>,                                         \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+                                 (int)sm2) != cudaSuccess)                                  \
+            return MFB_ERR_SMEM;                                                            \
+        cg_pair_kernel<R><<<n_pts, nt, sm2, st>>>(                                          \
+            n_lambda, n_sub, ndof, dof_ptr, dof_map, region, blk_base, h_base, local_idx,   \
+            n_real, blocks, hbar, k0, tol, max_iter, lam, iters, status, res_hist, hist_cap, \
+            g);                                                                             \
+    } while (0)
+    if (!regs) MFB_CG_LAUNCH();
+    else if (rn == 16) MFB_CG_PAIR(16);
+    else MFB_CG_PAIR(32);
 #undef MFB_CG_LAUNCH
+#undef MFB_CG_PAIR
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }
