@@ -685,6 +685,7 @@ class S3Engine:
         mt = None if kernel in ("cta", "staged") else self._multi_tables(n_pts,
                                                                       force=kernel == "multi")
         if mt is not None:
+            self.cg_kernel_name = "cg_multi_kernel (8 points per CTA on FP64 mma.m8n8k4)"
             self.launches += 1
             _lib.check(self.L.mfb_cg_pack(
                 mt["n_strips"], _ptr(mt["strips"]), _ptr(plan.d_ndof), _ptr(mt["n_loc"]),
@@ -706,6 +707,10 @@ class S3Engine:
         # accumulation order then equals the staged kernel's)
         reg_ndof = int(plan.ndof.max()) if (kernel != "staged" and len(plan.ndof)
                                              and not np.any(plan.ndof % 4)) else 0
+        self.cg_kernel_name = (
+            "cg_pair_kernel (one CTA per point, block rows in registers)"
+            if 0 < reg_ndof <= 32 and 2 * nl <= 608 else
+            "cg_kernel (one CTA per point, blocks staged in shared memory or read from L2)")
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
             _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(st.d_cg_local), n_real,

@@ -9,7 +9,7 @@ python bench.py > $OUT/bench.json 2> $OUT/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-s2 \
     > $OUT/ncu_launch.log 2>&1
-for k in band_solve cg_kernel condense; do
+for k in band_solve cg_pair condense; do
   ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $OUT/$k \
       python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-s2 > $OUT/ncu_$k.log 2>&1
   python tools/ncu_summary.py $OUT/$k.ncu-rep $OUT/${k}_cfg2_summary.json > /dev/null
