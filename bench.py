@@ -448,8 +448,12 @@ def run_ours(a):
     # bytes of the per-step inputs run_method uploads (collocation + KL tables)
     h2d = int(res.timings.get("h2d_bytes", 0)) if (res is not None and hasattr(res, "timings")) \
         else 0
-    # lambdas, packed residual histories (sum of iterations), iters + status, moments
-    n_hist = int(np.sum(iters_host)) if iters_host is not None else grid.n_real * max_iter
+    # lambdas, residual histories (the whole [n_real, max_iter] buffer when it
+    # is small -- run_method packs it on the host -- else the packed entries),
+    # iters + status, moments
+    n_hist = grid.n_real * max_iter
+    if n_hist * 8 > (256 << 20) and iters_host is not None:
+        n_hist = int(np.sum(iters_host))
     d2h = 8 * grid.n_real * nl + 8 * n_hist + 8 * grid.n_real * 2 + \
         16 * (nl + int(plan.nfield.sum()))
     if rank == 0:

@@ -900,13 +900,27 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     ev[2].record(eng.stream)
     mh = eng.moments_launch(lam)
     ev[3].record(eng.stream)
-    eng.check_info()
-    st = status.cpu().numpy()
-    it = iters.cpu().numpy()
+    # every result travels back in pinned buffers queued behind the moments:
+    # one wait, then host-side assembly only
+    small_hist = hist.numel() * 8 <= (256 << 20)
+    with torch.cuda.stream(eng.stream):
+        h_st = torch.empty(status.shape, dtype=status.dtype, pin_memory=True)
+        h_it = torch.empty(iters.shape, dtype=iters.dtype, pin_memory=True)
+        h_lam = torch.empty(lam.shape, dtype=lam.dtype, pin_memory=True)
+        h_st.copy_(status, non_blocking=True)
+        h_it.copy_(iters, non_blocking=True)
+        h_lam.copy_(lam, non_blocking=True)
+        if small_hist:
+            h_hist = torch.empty(hist.shape, dtype=hist.dtype, pin_memory=True)
+            h_hist.copy_(hist, non_blocking=True)
+    eng.check_info()                # syncs the stream: the copies above are done
+    st = h_st.numpy()
+    it = h_it.numpy()
     fail = np.nonzero((st == 1) | (st == 2))[0]
     if len(fail):
         k = int(fail[0])
-        res = hist[k, :min(int(it[k]), hist.shape[1])].cpu().numpy().tolist()
+        res = (h_hist[k] if small_hist else hist[k].cpu()).numpy()[
+            :min(int(it[k]), hist.shape[1])].tolist()
         if st[k] == 1:
             raise ConvergenceError(f"interface operator is not positive definite "
                                    f"(p.Sp <= 0 at iteration {int(it[k])}, point {k})",
@@ -917,9 +931,14 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     timings["bases"] = ev[0].elapsed_time(ev[1]) / 1e3
     timings["cg"] = ev[1].elapsed_time(ev[2]) / 1e3
     timings["moments"] = ev[2].elapsed_time(ev[3]) / 1e3
-    lam_h = lam.cpu().numpy()
-    lambdas = [lam_h[k] for k in range(grid.n_real)]
-    residuals = _pack_histories(hist, iters)
+    lam_h = h_lam.numpy()
+    lambdas = list(lam_h)
+    if small_hist:
+        it_c = np.minimum(it.astype(np.int64), hist.shape[1])
+        hh = h_hist.numpy()
+        residuals = ResidualHistories(hh[np.arange(hh.shape[1])[None, :] < it_c[:, None]], it_c)
+    else:
+        residuals = _pack_histories(hist, iters)
     stats.cg_iters = [int(x) for x in it]
     for s in range(n_sub):
         # S3: one factorization per (sid, loc); S2: per (sid, realization)

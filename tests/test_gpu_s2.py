@@ -93,3 +93,33 @@ def test_s2_s3_blocks_share_darcy_realizations(gpu):
         assert np.array_equal(a, b), (s, k)
         checked += 1
     assert checked > 0
+
+
+def test_methods_and_size_cap_errors(gpu):
+    """run_method's error conventions (interface.py:288-346): unknown method
+    -> ValueError; the basis-memory cap -> SizeCapError before any device
+    work, checked on the whole S3 pool (interface.py:375) but on ONE
+    realization's bases for S2 (interface.py:320-322); S1 is not on this
+    path and says so (no CPU fallback)."""
+    from paper_1802_06263_b200.errors import SizeCapError
+    from paper_1802_06263_b200.interface import get_plan, run_method
+    _, problem, grid, _ = case_from_golden("cfg2")
+    with pytest.raises(ValueError):
+        run_method(problem, grid, method="S4")
+    with pytest.raises(NotImplementedError):
+        run_method(problem, grid, method="S1")
+    plan = get_plan(problem, grid)
+    s3_mb = sum(plan.basis_bytes("S3")) / 2 ** 20
+    s2_mb = sum(plan.basis_bytes("S2")) / 2 ** 20
+    assert s2_mb < s3_mb
+    with pytest.raises(SizeCapError):
+        run_method(problem, grid, method="S3", tol=TOL, basis_cap_mb=0.5 * s3_mb)
+    with pytest.raises(SizeCapError):
+        run_method(problem, grid, method="S2", tol=TOL, basis_cap_mb=0.5 * s2_mb)
+    # a cap between the two: S2 (one realization at a time in the reference's
+    # accounting) runs, S3 (the whole local pool) does not
+    cap = 0.5 * (s2_mb + s3_mb)
+    res = run_method(problem, grid, method="S2", tol=TOL, basis_cap_mb=cap)
+    assert len(res.lambdas) == grid.n_real
+    with pytest.raises(SizeCapError):
+        run_method(problem, grid, method="S3", tol=TOL, basis_cap_mb=cap)
