@@ -10,6 +10,7 @@
  *   mfb_kl_realize        <- LogPermField.realize / evaluate_log
  *                            (random_field.py:232-243, 125-140)
  *   mfb_kl_realize_ld     <- problem.permeability (problem.py:85-96), S2
+ *   mfb_kl_realize_batched   every table of a sweep in one launch
  *   mfb_systems_solve     <- problem.assemble_subdomain + DarcyOperator /
  *                            StokesOperator factor + the N_dof star solves of
  *                            compute_flux_basis and the bar solve
@@ -126,6 +127,19 @@ const char *mfb_strerror(int code);
 /* K[l*n_cells + c] = exp(mean[c] + sum_j phi[c*n_term + j] * xi[l*n_term + j]) */
 int mfb_kl_realize(const double *phi, const double *mean, int n_cells, int n_term,
                    const double *xi, int n_loc, double *K, void *stream);
+
+/* One KL table of a batched launch: xi holds n_rows + 1 rows of n_term
+ * (row 0 = the mean-field point, written at K + dst0; row l >= 1 at K + dst +
+ * (l - 1) * ld). All pointers are device pointers. */
+typedef struct {
+    const double *phi, *mean, *xi;
+    long long dst0, dst, ld;
+    int n_cells, n_term, n_rows, pad;
+} MfbKlTable;
+
+/* Every table in one launch (max_rows = max n_rows, max_cells = max n_cells). */
+int mfb_kl_realize_batched(int n_tables, const MfbKlTable *tables, int max_rows,
+                           int max_cells, double *K, void *stream);
 
 /* Same with a row stride: K[l*ld + c]. Method S2 writes realization k of a
  * Darcy subdomain into the k-th full-problem K row (problem.permeability(y),

@@ -30,6 +30,11 @@ class MfbPattern(ctypes.Structure):
     ]
 
 
+class MfbKlTable(ctypes.Structure):
+    _fields_ = [("phi", _p), ("mean", _p), ("xi", _p), ("dst0", _ll), ("dst", _ll), ("ld", _ll),
+                ("n_cells", _i), ("n_term", _i), ("n_rows", _i), ("pad", _i)]
+
+
 class MfbHybPattern(ctypes.Structure):
     _fields_ = [
         ("n", _i), ("w", _i), ("ws", _i), ("ndof", _i), ("nfield", _i), ("n_edges", _i),
@@ -50,6 +55,7 @@ _SIGS = {
     "mfb_strerror": ([_i], ctypes.c_char_p),
     "mfb_kl_realize": ([_p, _p, _i, _i, _p, _i, _p, _p], _i),
     "mfb_kl_realize_ld": ([_p, _p, _i, _i, _p, _i, _p, _ll, _p], _i),
+    "mfb_kl_realize_batched": ([_i, _p, _i, _i, _p, _p], _i),
     "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _p], _i),
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,

@@ -26,6 +26,25 @@ __global__ void kl_realize_kernel(const double *__restrict__ phi,
         K[(long long)l * ld + c] = exp(mean[c] + dot);
     }
 }
+// Every KL table of a sweep in one launch: blockIdx.z = table, blockIdx.y =
+// row (row 0 of a table is its mean-field row, written to dst0), grid-stride
+// over the cells.
+__global__ void kl_batched_kernel(const MfbKlTable *__restrict__ tabs, double *__restrict__ K) {
+    __shared__ double s_xi[KL_MAX_TERM];
+    const MfbKlTable T = tabs[blockIdx.z];
+    const int l = blockIdx.y;
+    if (l > T.n_rows) return;
+    if (threadIdx.x < T.n_term) s_xi[threadIdx.x] = T.xi[(long long)l * T.n_term + threadIdx.x];
+    __syncthreads();
+    double *out = l == 0 ? K + T.dst0 : K + T.dst + (long long)(l - 1) * T.ld;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < T.n_cells;
+         c += gridDim.x * blockDim.x) {
+        const double *row = T.phi + (long long)c * T.n_term;
+        double dot = 0.0;
+        for (int j = 0; j < T.n_term; ++j) dot = fma(row[j], s_xi[j], dot);
+        out[c] = exp(T.mean[c] + dot);
+    }
+}
 }  // namespace
 
 extern "C" int mfb_kl_realize_ld(const double *phi, const double *mean, int n_cells,
@@ -48,4 +67,18 @@ extern "C" int mfb_kl_realize(const double *phi, const double *mean, int n_cells
                               int n_term, const double *xi, int n_loc, double *K,
                               void *stream) {
     return mfb_kl_realize_ld(phi, mean, n_cells, n_term, xi, n_loc, K, n_cells, stream);
+}
+
+extern "C" int mfb_kl_realize_batched(int n_tables, const MfbKlTable *tables, int max_rows,
+                                      int max_cells, double *K, void *stream) {
+    if (n_tables < 0 || max_rows < 0 || max_cells < 0) return MFB_ERR_ARG;
+    if (n_tables == 0) return MFB_OK;
+    const int nt = 256;
+    int bx = (max_cells + nt - 1) / nt;
+    if (bx > 64) bx = 64;
+    if (bx < 1) bx = 1;
+    dim3 grid(bx, max_rows + 1, n_tables);
+    kl_batched_kernel<<<grid, nt, 0, mfb_stream(stream)>>>(tables, K);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
 }

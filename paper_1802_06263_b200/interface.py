@@ -273,6 +273,16 @@ class _S3Static:
                             _dev(xi, f64), int(dst), xi.shape[0] - 1, int(ld)))
         self.kl_h2d_bytes = sum(8 * (t[3].numel() + t[4].numel() + t[5].numel())
                                 for t in self.kl)
+        # the same tables as one MfbKlTable array: a single batched KL launch
+        tabs = (_lib.MfbKlTable * max(len(self.kl), 1))()
+        for j, (s_, nc, nt, d_phi, d_mean, d_xi, dst, nrows, ld) in enumerate(self.kl):
+            t = tabs[j]
+            t.phi, t.mean, t.xi = d_phi.data_ptr(), d_mean.data_ptr(), d_xi.data_ptr()
+            t.dst0, t.dst, t.ld = int(plan.k0_off[s_]), int(dst), int(ld)
+            t.n_cells, t.n_term, t.n_rows = int(nc), int(nt), int(nrows)
+        self.kl_tab = torch.frombuffer(bytearray(bytes(tabs)), dtype=torch.uint8).to("cuda")
+        self.kl_max_rows = max([t[7] for t in self.kl], default=0)
+        self.kl_max_cells = max([t[1] for t in self.kl], default=0)
         # CG gather tables: block of subdomain i at point k is loc = table[region_i][k]
         if method == "S2":
             self.d_cg_region = _dev(np.zeros(plan.n_sub, dtype=np.int32), i32)
@@ -572,15 +582,11 @@ class S3Engine:
         """K for every (Darcy sid, loc) system plus the mean-field K0 buffer."""
         st, plan = self.st, self.plan
         K = st.K
-        for s, nc, nt, d_phi, d_mean, d_xi, dst, nrows, ld in st.kl:
-            self.launches += 2
-            _lib.check(self.L.mfb_kl_realize(
-                _ptr(d_phi), _ptr(d_mean), nc, nt, _ptr(d_xi), 1,
-                ctypes.c_void_p(K.data_ptr() + 8 * plan.k0_off[s]), self.sp), "mfb_kl_realize")
-            _lib.check(self.L.mfb_kl_realize_ld(
-                _ptr(d_phi), _ptr(d_mean), nc, nt, ctypes.c_void_p(d_xi.data_ptr() + 8 * nt),
-                nrows, ctypes.c_void_p(K.data_ptr() + 8 * dst), ld, self.sp),
-                "mfb_kl_realize_ld")
+        if st.kl:
+            self.launches += 1
+            _lib.check(self.L.mfb_kl_realize_batched(
+                len(st.kl), _ptr(st.kl_tab), st.kl_max_rows, st.kl_max_cells, _ptr(K), self.sp),
+                "mfb_kl_realize_batched")
         return K
 
     # ------------------------------------------------------- (2) bases ----
