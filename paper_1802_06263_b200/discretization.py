@@ -86,9 +86,9 @@ class Pattern:
     def work_doubles(self):
         # band, rhs rows, BAND_GROUP_MAX + 1 panel-publication slots ((kl + 16)
         # x 16 scaled factors + 32 scales + 16 doubles of pivots/flag), then n reciprocal U
-        # diagonals (mfb_band.cu)
+        # diagonals, then the inverses of the 16 x 16 diagonal U blocks (mfb_band.cu)
         w = (self.ldab * self.n + self.n * (self.ndof + 1) + 1
-             + 17 * ((self.kl + 16) * 16 + 48) + self.n)
+             + 17 * ((self.kl + 16) * 16 + 48) + self.n + 256 * ((self.n + 15) // 16) + 1)
         return w + (w & 1)                 # even: every system's slots stay 16-byte aligned
 
     @property
