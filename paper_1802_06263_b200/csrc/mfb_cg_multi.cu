@@ -95,65 +95,86 @@ __device__ __forceinline__ void reduce_pairs(double &v0, double &v1, double (*re
 // holds the A fragments of its MMAs in lane order: fragment t of lane
 // (g, q) = B[r0 + g][4 t + q] at strip[32 t + lane] (zero-padded), so every
 // A load is one coalesced 256-byte warp access.
+// One pass over a strip for the slots of mask m (block of local realization
+// l): NT4 > 0 is the compile-time fragment count (ndof == 4 NT4, no bounds
+// checks), 0 the generic path.
+template <int NT4>
+__device__ __forceinline__ void strip_pass(const double *__restrict__ Sl, const int *dm, int nd,
+                                           const double *__restrict__ ps, bool all, double bm,
+                                           double &d0, double &d1) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const int nt4 = NT4 > 0 ? NT4 : (nd + 3) >> 2;
+    // Two accumulator chains (even / odd fragments) halve the MMA dependency
+    // chain; their sum is the row product
+    double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+#pragma unroll
+    for (int t0 = 0; t0 < (NT4 > 0 ? NT4 : nt4); t0 += MPF) {
+        double af[MPF];
+        int dv[MPF];
+#pragma unroll
+        for (int t = 0; t < MPF; ++t) {
+            if (NT4 > 0 ? (t0 + t < NT4) : (t0 + t < nt4)) {
+                af[t] = __ldg(Sl + 32 * (t0 + t));
+                const int c = 4 * (t0 + t) + q;
+                dv[t] = (NT4 > 0 || c < nd) ? dm[c] + g : g;
+            }
+        }
+        if (all) {
+#pragma unroll
+            for (int t = 0; t < MPF; t += 2) {
+                if (NT4 > 0 ? (t0 + t >= NT4) : (t0 + t >= nt4)) break;
+                dmma884(e0, e1, af[t], ps[dv[t]]);
+                if (NT4 > 0 ? (t0 + t + 1 < NT4) : (t0 + t + 1 < nt4))
+                    dmma884(o0, o1, af[t + 1], ps[dv[t + 1]]);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < MPF; t += 2) {
+                if (NT4 > 0 ? (t0 + t >= NT4) : (t0 + t >= nt4)) break;
+                dmma884(e0, e1, af[t], ps[dv[t]] * bm);
+                if (NT4 > 0 ? (t0 + t + 1 < NT4) : (t0 + t + 1 < nt4))
+                    dmma884(o0, o1, af[t + 1], ps[dv[t + 1]] * bm);
+            }
+        }
+    }
+    // slots outside the group have e = o = 0 here: d + 0 leaves them
+    d0 += e0 + o0;
+    d1 += e1 + o1;
+}
+
+// acc += the 8-row strip at `soff` of subdomain sid's packed block (slot
+// n's block: local realization of its region) times the slots' p. A strip
+// holds the A fragments of its MMAs in lane order: fragment t of lane
+// (g, q) = B[r0 + g][4 t + q] at strip[32 t + lane] (zero-padded), so every
+// A load is one coalesced 256-byte warp access. The slots are visited by
+// local-realization group (g_cnt / g_loc / g_mask per region, rebuilt when
+// slots are refilled); the frozen Stokes blocks are one group.
 __device__ __forceinline__ void side_mma(const CgMultiArgs &A, int sid, int soff,
                                          const double *__restrict__ ps, const int *sdm,
-                                         const int *s_loc, int live, double &d0, double &d1) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+                                         const int *g_cnt, const int *g_loc, const int *g_mask,
+                                         int live, double &d0, double &d1) {
+    const int lane = threadIdx.x & 31, g = lane >> 2;
     const int nd = A.ndof[sid];
-    const int nt4 = (nd + 3) >> 2;
     const int reg = A.region[sid];
     const int *dm = sdm + A.dof_ptr[sid];       // shared: dof * MP
     const double *base = A.packed + A.pk_base[sid] + soff + lane;
     const int psz = A.pk_size[sid];
-    int rem = live;
-    while (rem) {
-        int m = rem, l = 0;
-        if (reg >= 0) {
-            const int s0 = __ffs(rem) - 1;
-            l = s_loc[reg * MP + s0];
-            m = 0;
-#pragma unroll
-            for (int s = 0; s < MP; ++s)
-                if (((rem >> s) & 1) && s_loc[reg * MP + s] == l) m |= 1 << s;
-        }
-        rem &= ~m;
-        // B column n = slot g; slots outside this realization's group get 0.
-        // Two accumulator chains (even / odd fragments) halve the MMA
-        // dependency chain; their sum is the row product.
+    const int ngrp = reg < 0 ? 1 : g_cnt[reg];
+    for (int gi = 0; gi < ngrp; ++gi) {
+        const int m = reg < 0 ? live : (g_mask[reg * MP + gi] & live);
+        if (!m) continue;
+        const int l = reg < 0 ? 0 : g_loc[reg * MP + gi];
         const bool all = (m == live);
         const double bm = ((m >> g) & 1) ? 1.0 : 0.0;
         const double *Sl = base + (long long)l * psz;
-        double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
-        for (int t0 = 0; t0 < nt4; t0 += MPF) {
-            double af[MPF];
-            int dv[MPF];
-#pragma unroll
-            for (int t = 0; t < MPF; ++t) {
-                if (t0 + t < nt4) {
-                    af[t] = __ldg(Sl + 32 * (t0 + t));
-                    const int c = 4 * (t0 + t) + q;
-                    dv[t] = c < nd ? dm[c] + g : g;
-                }
-            }
-            if (all) {
-#pragma unroll
-                for (int t = 0; t < MPF; t += 2) {
-                    if (t0 + t >= nt4) break;
-                    dmma884(e0, e1, af[t], ps[dv[t]]);
-                    if (t0 + t + 1 < nt4) dmma884(o0, o1, af[t + 1], ps[dv[t + 1]]);
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < MPF; t += 2) {
-                    if (t0 + t >= nt4) break;
-                    dmma884(e0, e1, af[t], ps[dv[t]] * bm);
-                    if (t0 + t + 1 < nt4) dmma884(o0, o1, af[t + 1], ps[dv[t + 1]] * bm);
-                }
-            }
+        switch (nd) {
+        case 16: strip_pass<4>(Sl, dm, nd, ps, all, bm, d0, d1); break;
+        case 24: strip_pass<6>(Sl, dm, nd, ps, all, bm, d0, d1); break;
+        case 32: strip_pass<8>(Sl, dm, nd, ps, all, bm, d0, d1); break;
+        case 48: strip_pass<12>(Sl, dm, nd, ps, all, bm, d0, d1); break;
+        case 64: strip_pass<16>(Sl, dm, nd, ps, all, bm, d0, d1); break;
+        default: strip_pass<0>(Sl, dm, nd, ps, all, bm, d0, d1); break;
         }
-        // slots outside the group have e = o = 0 here: d + 0 leaves them
-        d0 += e0 + o0;
-        d1 += e1 + o1;
     }
 }
 
@@ -184,6 +205,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP];
     __shared__ double s_rr[MP], s_gn[MP], s_a[MP], s_b[MP], s_tot[MP];
     __shared__ int s_loc[MREG * MP];
+    __shared__ int s_gcnt[MREG], s_gloc[MREG * MP], s_gmask[MREG * MP];
     __shared__ double s_red[MW][MP];
     __shared__ int s_any;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -232,6 +254,25 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                     s_loc[e] = A.local_idx[(long long)(e / MP) * A.n_real + A.k0 + s_k[s]];
             }
             __syncthreads();
+            // per region: the distinct local realizations among the slots
+            // holding points, with their slot masks (read after the barriers
+            // of the reduction below)
+            for (int r = tid; r < A.n_regions; r += MNT) {
+                int cnt = 0;
+                for (int s = 0; s < MP; ++s) {
+                    if (s_k[s] < 0) continue;
+                    const int l = s_loc[r * MP + s];
+                    int j = 0;
+                    while (j < cnt && s_gloc[r * MP + j] != l) ++j;
+                    if (j == cnt) {
+                        s_gloc[r * MP + cnt] = l;
+                        s_gmask[r * MP + cnt] = 0;
+                        ++cnt;
+                    }
+                    s_gmask[r * MP + j] |= 1 << s;
+                }
+                s_gcnt[r] = cnt;
+            }
             // g = 0 + h_lower + h_upper (mortar.jump of the bar traces), x = 0
             for (int e = tid; e < npair; e += MNT) {
                 if (!(f0 || f1)) break;
@@ -286,8 +327,8 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                 const int4 T = A.tasks[ti];
                 const int i = T.w & 0xfff, j = ((T.w >> 12) & 0xfff) - 1, R = T.w >> 24;
                 double lo0 = 0.0, lo1 = 0.0, up0 = 0.0, up1 = 0.0;
-                side_mma(A, i, T.y, ps, sdm, s_loc, run, lo0, lo1);
-                if (j >= 0) side_mma(A, j, T.z, ps, sdm, s_loc, run, up0, up1);
+                side_mma(A, i, T.y, ps, sdm, s_gcnt, s_gloc, s_gmask, run, lo0, lo1);
+                if (j >= 0) side_mma(A, j, T.z, ps, sdm, s_gcnt, s_gloc, s_gmask, run, up0, up1);
                 if (g8 < R) {
                     const int d = T.x + g8;
                     const double2 sp = j >= 0 ? make_double2(lo0 + up0, lo1 + up1)
