@@ -136,10 +136,10 @@ def s2_comparison(plan, problem, grid, tol, max_iter, flush, steps=2):
     per subdomain per realization, Stokes included) on the device, device
     time per sweep (CUDA events, L2 flushed) and end to end via run_method."""
     import torch
-    from paper_1802_06263_b200.interface import S3Engine, run_method
+    from paper_1802_06263_b200.interface import SweepEngine, run_method
 
     def sweep():
-        e = S3Engine(plan, method="S2")
+        e = SweepEngine(plan, method="S2")
         e.kl_fields()
         e.build_bases()
         lam, iters, status, hist, _ = e.solve_points(tol, max_iter)
@@ -288,7 +288,7 @@ def run_ours(a):
         torch.cuda.set_device(0)
     from paper_1802_06263_b200 import _build
     from paper_1802_06263_b200.config import load_config
-    from paper_1802_06263_b200.interface import S3Engine, get_plan, run_method
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan, run_method
     _build.build()
     cfg_path = _config_path(a.config)
     problem, grid, _ = load_config(cfg_path)
@@ -323,7 +323,7 @@ def run_ours(a):
             return lam, iters, status, mom
 
         def new_engine():
-            e = S3Engine(plan)
+            e = SweepEngine(plan)
             e.timing = True
             return e
 

@@ -16,7 +16,7 @@ The path shards naturally:
 Every number a rank computes is computed by the same kernel with the same
 inputs as on one GPU, so the N-rank result is bitwise the 1-rank result.
 The collectives are ordinary torch.distributed calls (NCCL on GPUs, gloo in
-the CPU tests), and `Engine` is the device engine (`interface.S3Engine`) or
+the CPU tests), and `Engine` is the device engine (`interface.SweepEngine`) or
 a CPU stand-in used by tests/test_distributed.py.
 """
 
@@ -96,12 +96,12 @@ def run_sharded(engine, n_real, n_lambda, tol, max_iter, dist, rank, world):
 
 
 class DeviceShardEngine:
-    """`run_sharded` engine over the sm_100a S3Engine (one GPU per rank)."""
+    """`run_sharded` engine over the sm_100a SweepEngine (one GPU per rank)."""
 
     def __init__(self, plan):
-        from .interface import S3Engine
+        from .interface import SweepEngine
         self.plan = plan
-        self.eng = S3Engine(plan)
+        self.eng = SweepEngine(plan)
 
     def sid_costs(self):
         p = self.plan

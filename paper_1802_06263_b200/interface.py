@@ -210,7 +210,7 @@ def get_plan(problem, grid):
     return plan
 
 
-class _S3Static:
+class _SweepStatic:
     """Everything a sweep needs that depends only on (problem, grid, method).
 
     Built once per DevicePlan and kept resident: the system list and its
@@ -550,8 +550,8 @@ class _S3Static:
         return int(total)
 
 
-class S3Engine:
-    """Device work of one S3 sweep; methods map 1:1 onto the C ABI calls."""
+class SweepEngine:
+    """Device work of one S3 or S2 sweep; methods map 1:1 onto the C ABI calls."""
 
     def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid", method="S3"):
         import torch
@@ -559,7 +559,7 @@ class S3Engine:
         self.plan = plan
         self.method = method
         self.L = _lib.lib()
-        self.st = plan.s3_static(keep_fields, darcy_kernel, method)
+        self.st = plan.sweep_static(keep_fields, darcy_kernel, method)
         self.stream = torch.cuda.current_stream() if stream is None else stream
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
         self.launches = 0            # kernels launched through the C ABI
@@ -892,7 +892,7 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     plan = get_plan(problem, grid)
     _check_basis_cap(plan.basis_bytes(method), basis_cap_mb)
     timings = {"plan": time.perf_counter() - t0}
-    eng = S3Engine(plan, method=method)
+    eng = SweepEngine(plan, method=method)
     timings["h2d_bytes"] = eng.st.refresh_inputs()
     # everything is queued on the stream first (no host round trips between
     # the phases); the verdicts are checked in the reference's order after:

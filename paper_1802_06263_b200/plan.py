@@ -176,15 +176,15 @@ class DevicePlan:
             out += [(s, l) for l in range(int(self.n_loc[s]))]
         return out
 
-    def s3_static(self, keep_fields=True, darcy_kernel="hybrid", method="S3"):
+    def sweep_static(self, keep_fields=True, darcy_kernel="hybrid", method="S3"):
         """Resident sweep state for `method` ("S3" or "S2"), cached per method."""
         cache = self.__dict__.setdefault("_statics", {})
         st = cache.get(method)
         if (st is None or (keep_fields and not st.keep_fields)
                 or st.darcy_kernel != darcy_kernel):
-            from .interface import _S3Static
+            from .interface import _SweepStatic
             cache.pop(method, None)
-            st = _S3Static(self, keep_fields, darcy_kernel, method)
+            st = _SweepStatic(self, keep_fields, darcy_kernel, method)
             cache[method] = st
         return st
 

@@ -32,9 +32,9 @@ def test_dmma_fragment_layout(gpu):
 
 
 def _engine(problem, grid):
-    from paper_1802_06263_b200.interface import S3Engine, get_plan
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
     plan = get_plan(problem, grid)
-    eng = S3Engine(plan)
+    eng = SweepEngine(plan)
     eng.kl_fields()
     eng.build_bases()
     eng.check_info()
@@ -145,7 +145,7 @@ def test_rhs_and_cg_against_oracle_inputs(gpu, name):
 def test_cfg5_basis_blocks(gpu):
     """Basis-only stress config: 64x64 Darcy, 6-term regions, 729 local points."""
     import torch
-    from paper_1802_06263_b200.interface import S3Engine, get_plan
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
     from paper_1802_06263_b200.collocation import build_tensor_grid
     z = golden("cfg5")
     _, problem, grid, _ = case_from_golden("cfg5")
@@ -154,7 +154,7 @@ def test_cfg5_basis_blocks(gpu):
     grid.local_points = [loc.points.copy() for _ in range(4)]
     grid.local_counts = [729] * 4
     plan = get_plan(problem, grid)
-    eng = S3Engine(plan, keep_fields=False)
+    eng = SweepEngine(plan, keep_fields=False)
     eng.kl_fields()
     eng.build_bases()
     eng.check_info()
@@ -172,10 +172,10 @@ def test_cfg4_basis_blocks(gpu):
     """cfg4 (16x8 subdomains, 8 regions, 289 local realizations): sampled blocks."""
     z = golden("cfg4")
     from conftest import ROOT, case_from_config
-    from paper_1802_06263_b200.interface import S3Engine, get_plan
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
     _, problem, grid, _ = case_from_config(f"{ROOT}/configs/cfg4.json")
     plan = get_plan(problem, grid)
-    eng = S3Engine(plan, keep_fields=False)
+    eng = SweepEngine(plan, keep_fields=False)
     eng.kl_fields()
     eng.build_bases()
     eng.check_info()
@@ -233,10 +233,10 @@ def test_cfg4_points_match_reference(gpu, kernel):
         pytest.skip("cfg4_points.npz not generated")
     z = np.load(path)
     from conftest import ROOT, case_from_config
-    from paper_1802_06263_b200.interface import S3Engine, get_plan
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
     _, problem, grid, _ = case_from_config(f"{ROOT}/configs/cfg4.json")
     plan = get_plan(problem, grid)
-    eng = S3Engine(plan, keep_fields=False)
+    eng = SweepEngine(plan, keep_fields=False)
     eng.kl_fields()
     eng.build_bases()
     eng.check_info()

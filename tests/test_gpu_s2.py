@@ -71,13 +71,13 @@ def test_s2_s3_blocks_share_darcy_realizations(gpu):
     """S2's Darcy block of realization k is S3's block of loc_i(k) (same K,
     same kernel): bitwise, as the reference's S3 == S2 check
     (test_interface.py:129-140) relies on."""
-    from paper_1802_06263_b200.interface import S3Engine, get_plan
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
     _, problem, grid, _ = case_from_golden("cfg1")
     plan = get_plan(problem, grid)
-    e3 = S3Engine(plan, method="S3")
+    e3 = SweepEngine(plan, method="S3")
     e3.kl_fields(); e3.build_bases(); e3.check_info()
     b3 = e3.blocks.cpu().numpy()
-    e2 = S3Engine(plan, method="S2")
+    e2 = SweepEngine(plan, method="S2")
     e2.kl_fields(); e2.build_bases(); e2.check_info()
     b2 = e2.blocks.cpu().numpy()
     sys3 = {sl: i for i, sl in enumerate(e3.systems)}

@@ -16,7 +16,7 @@ import torch  # noqa: E402
 
 from paper_1802_06263_b200.collocation import build_tensor_grid  # noqa: E402
 from paper_1802_06263_b200.config import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 
 def main():
@@ -34,7 +34,7 @@ def main():
     t_plan = time.time() - t
     best = None
     for rep in range(a.reps):
-        eng = S3Engine(plan, keep_fields=False)
+        eng = SweepEngine(plan, keep_fields=False)
         eng.timing = True
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)

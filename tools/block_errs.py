@@ -7,13 +7,13 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(
 import numpy as np  # noqa: E402
 
 from conftest import case_from_golden, golden  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 name = sys.argv[1]
 z = golden(name)
 _, problem, grid, _ = case_from_golden(name)
 plan = get_plan(problem, grid)
-eng = S3Engine(plan)
+eng = SweepEngine(plan)
 eng.kl_fields()
 eng.build_bases()
 blocks = eng.blocks.cpu().numpy()

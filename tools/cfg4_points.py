@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1802_06263_b200.config import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 GOLD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
                     "golden", "cfg4_points.npz")
@@ -25,7 +25,7 @@ def main():
     problem, grid, _ = load_config("configs/cfg4.json")
     plan = get_plan(problem, grid)
     print(f"setup+plan {time.time() - t:.1f} s, n_lambda {plan.n_lambda}, n_real {grid.n_real}")
-    eng = S3Engine(plan, keep_fields=False)
+    eng = SweepEngine(plan, keep_fields=False)
     torch.cuda.synchronize()
     t = time.time()
     eng.kl_fields()

@@ -1,4 +1,4 @@
-"""Host/device split of S3Engine.moments (debug helper)."""
+"""Host/device split of SweepEngine.moments (debug helper)."""
 import os
 import sys
 import time
@@ -8,12 +8,12 @@ import torch  # noqa: E402
 
 from paper_1802_06263_b200 import interface  # noqa: E402
 from paper_1802_06263_b200.config import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 problem, grid, _ = load_config(f"configs/{cfg}.json")
 plan = get_plan(problem, grid)
-eng = S3Engine(plan)
+eng = SweepEngine(plan)
 eng.kl_fields()
 eng.build_bases()
 lam, iters, status, hist, _ = eng.solve_points(1e-11, 10 * plan.n_lambda)

@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 
 from conftest import case_from_golden, golden  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan, run_method  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan, run_method  # noqa: E402
 
 
 def rel(a, b):
@@ -25,7 +25,7 @@ def report(name):
     _, problem, grid, _ = case_from_golden(name)
     out = {"config": name, "n_real": grid.n_real, "n_lambda": problem.space.n_dof}
     plan = get_plan(problem, grid)
-    eng = S3Engine(plan)
+    eng = SweepEngine(plan)
     eng.kl_fields()
     eng.build_bases()
     blocks = eng.blocks.cpu().numpy()

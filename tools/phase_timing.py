@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from paper_1802_06263_b200.config import load_config
-from paper_1802_06263_b200.interface import S3Engine, get_plan
+from paper_1802_06263_b200.interface import SweepEngine, get_plan
 
 
 def main():
@@ -35,7 +35,7 @@ def main():
     print(f"setup {t_setup:.2f}s plan {t_plan:.2f}s n_real {grid.n_real} "
           f"n_lambda {plan.n_lambda} method {a.method}", flush=True)
     for rep in range(a.reps):
-        eng = S3Engine(plan, darcy_kernel=a.darcy, method=a.method)
+        eng = SweepEngine(plan, darcy_kernel=a.darcy, method=a.method)
         eng.timing = True
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()

@@ -12,12 +12,12 @@ from paper_1802_06263_b200 import _lib
 _lib._lib = None
 _lib.load(os.path.join(os.path.dirname(_lib._SO), "_mfb_prof.so"))
 from paper_1802_06263_b200.config import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 problem, grid, _ = load_config(f"configs/{cfg}.json")
 plan = get_plan(problem, grid)
-eng = S3Engine(plan)
+eng = SweepEngine(plan)
 eng.kl_fields()
 eng.build_bases()
 lam, iters, status, hist, _ = eng.solve_points(1e-11, 10 * plan.n_lambda)

@@ -12,14 +12,14 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1802_06263_b200.config import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 n_pts = int(sys.argv[1]) if len(sys.argv) > 1 else 1184
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 which = sys.argv[3] if len(sys.argv) > 3 else "both"
 problem, grid, _ = load_config("configs/cfg4.json")
 plan = get_plan(problem, grid)
-eng = S3Engine(plan, keep_fields=False)
+eng = SweepEngine(plan, keep_fields=False)
 eng.kl_fields()
 eng.build_bases()
 torch.cuda.synchronize()

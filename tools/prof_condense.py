@@ -12,7 +12,7 @@ from paper_1802_06263_b200 import _lib
 _lib._lib = None
 _lib.load(os.path.join(os.path.dirname(_lib._SO), "_mfb_prof.so"))
 from paper_1802_06263_b200.config import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import S3Engine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 band_only = "--band" in sys.argv
@@ -23,7 +23,7 @@ if cfg == "cfg5":
     grid.local_points = [loc.points.copy() for _ in problem.perm.regions]
     grid.local_counts = [loc.n_real] * len(problem.perm.regions)
 plan = get_plan(problem, grid)
-eng = S3Engine(plan, keep_fields=(cfg != "cfg5"))
+eng = SweepEngine(plan, keep_fields=(cfg != "cfg5"))
 eng.kl_fields()
 eng.build_bases()
 torch.cuda.synchronize()
