@@ -200,8 +200,19 @@ def _check_basis_cap(sizes_bytes, cap_mb):
                            f"cap of {cap_mb:.3g} MiB; raise basis_cap_mb or use method S1")
 
 
+def _plan_fingerprint(problem, grid):
+    """What the resident plan was built from: the problem's and grid's
+    component objects (the reference's problem is a mutable dataclass, so a
+    caller may swap `physics`, `bcs`, sources or the permeability model in
+    place between calls; any such swap rebuilds the plan)."""
+    return (id(problem), id(grid), problem.physics, id(problem.bcs), id(problem.perm),
+            id(problem.f_s), id(problem.f_d), id(problem.q_d), id(problem.meshes),
+            id(problem.space), id(problem.layout), id(grid.points), id(grid.weights),
+            grid.n_real, id(grid.local_indices), id(grid.local_points))
+
+
 def get_plan(problem, grid):
-    key = (id(problem), id(grid))
+    key = _plan_fingerprint(problem, grid)
     plan = _PLAN_CACHE.get(key)
     if plan is None or plan.problem is not problem or plan.grid is not grid:
         plan = DevicePlan(problem, grid)

@@ -123,3 +123,19 @@ def test_methods_and_size_cap_errors(gpu):
     assert len(res.lambdas) == grid.n_real
     with pytest.raises(SizeCapError):
         run_method(problem, grid, method="S3", tol=TOL, basis_cap_mb=cap)
+
+
+def test_in_place_problem_changes_rebuild_the_plan(gpu):
+    """The reference's problem is a mutable dataclass: swapping its physics in
+    place between two run_method calls must not reuse the resident plan
+    built for the old physics."""
+    import dataclasses
+    from paper_1802_06263_b200.interface import run_method
+    _, problem, grid, _ = case_from_golden("cfg1")
+    r1 = run_method(problem, grid, method="S3", tol=TOL)
+    problem.physics = dataclasses.replace(problem.physics, alpha=0.0)
+    r2 = run_method(problem, grid, method="S3", tol=TOL)
+    _, fresh, grid0, _ = case_from_golden("cfg1", physics={"alpha": 0.0})
+    r3 = run_method(fresh, grid0, method="S3", tol=TOL)
+    assert not np.array_equal(np.array(r1.lambdas), np.array(r2.lambdas))
+    assert np.array_equal(np.array(r2.lambdas), np.array(r3.lambdas))
