@@ -333,6 +333,9 @@ cg_pair_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     int status = MFB_CG_MAX_ITER, it_done = max_iter;
     for (int it = 1; it <= max_iter; ++it) {
         __syncthreads();                          // p (row space) of this iteration
+        // 1 / rr for this iteration's beta, computed here so that its latency
+        // overlaps the GEMV instead of sitting on the chain after rr_new
+        const double inv_rr = __drcp_rn(rr);
         const double *pr = prow + rd0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
@@ -363,7 +366,7 @@ cg_pair_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             it_done = it;
             break;
         }
-        const double beta = rr_new / rr;
+        const double beta = rr_new * inv_rr;
         pd = r + beta * pd;
         const double pv = __shfl_sync(0xffffffffu, pd, lane & ~1);
         if (row >= 0) prow[row] = pv;
