@@ -838,26 +838,29 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
         unsigned bsphase[2] = {0u, 0u};
         // U(i0..jj-1, jj..jj+pn-1) -> buffer b: a contiguous run of the band per
         // column, started one element early when odd (16-byte aligned ends)
+        // issued by the 16 lanes of warp 0, one column each: lane 0 posts the
+        // transaction count (warp sum of the column byte counts) before any
+        // copy is issued
         auto issue_u = [&](int jj, int b) {
-            if (tid != 0) return;
+            if (tid >= 32) return;
             const int pn = min(NB, n - jj), ii0 = max(0, jj - kl - ku), mr = jj - ii0;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            unsigned tot = 0;
-            const double *srcs[NB];
-            unsigned bytes[NB];
-#pragma unroll
-            for (int k = 0; k < NB; ++k) {
+            const int k = tid;
+            unsigned bytes = 0;
+            const double *src = AB;
+            if (k < NB) {
                 const long long off = (long long)(jj + k) * ldab + (kl + ku + ii0 - (jj + k));
                 const int sh = (int)(off & 1);
                 s_ush[b][k] = sh;
-                srcs[k] = AB + off - sh;
-                bytes[k] = (k < pn && mr > 0) ? (unsigned)(((mr + sh + 1) & ~1) * 8) : 0u;
-                tot += bytes[k];
+                src = AB + off - sh;
+                bytes = (k < pn && mr > 0) ? (unsigned)(((mr + sh + 1) & ~1) * 8) : 0u;
             }
-            mbar_arrive_expect_tx(&s_bsbar[b], tot);
+            unsigned tot = bytes;
 #pragma unroll
-            for (int k = 0; k < NB; ++k)
-                if (bytes[k]) bulk_g2s(Ub2 + (b * NB + k) * LDU, srcs[k], bytes[k], &s_bsbar[b]);
+            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (tid == 0) mbar_arrive_expect_tx(&s_bsbar[b], tot);
+            __syncwarp();
+            if (bytes) bulk_g2s(Ub2 + (b * NB + k) * LDU, src, bytes, &s_bsbar[b]);
         };
         auto u11_load = [&](int jj, double *dst) {        // U11^-1 of the block at jj
             const double *src = u11inv + (long long)(jj / NB) * NB * NB;
