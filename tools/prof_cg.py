@@ -1,4 +1,5 @@
-"""CG phase cycle breakdown (CTA 0, -DMFB_PROFILE build _mfb_prof.so)."""
+"""CG phase cycle breakdown of the staged cg_kernel (CTA 0, -DMFB_PROFILE build
+_mfb_prof.so); the register-row cg_pair_kernel has no phase hooks."""
 import ctypes
 import os
 import sys
@@ -20,7 +21,8 @@ plan = get_plan(problem, grid)
 eng = SweepEngine(plan)
 eng.kl_fields()
 eng.build_bases()
-lam, iters, status, hist, _ = eng.solve_points(1e-11, 10 * plan.n_lambda)
+# the CGP phase hooks live in the staged one-CTA-per-point kernel (cg_kernel)
+lam, iters, status, hist, _ = eng.solve_points(1e-11, 10 * plan.n_lambda, kernel="staged")
 torch.cuda.synchronize()
 out = (ctypes.c_ulonglong * 8)()
 _lib.load().mfb_debug_cgprof(out)
