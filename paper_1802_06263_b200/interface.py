@@ -459,6 +459,8 @@ class _SweepStatic:
                 kshape.append(tuple(shape))
         tab = {"n": len(sel), "pat": _dev(sys_pat, i32), "gptr": _dev(gptr, i32),
                "keys": keys, "key_start": np.array(kstart, dtype=np.int64), "key_shape": kshape,
+               "key_slices": [(k, a, a + int(np.prod(sh)), sh)
+                              for k, a, sh in zip(keys, kstart, kshape)],
                "mem": _dev(mem, i32), "voff": _dev(self._voff[:-1][sel], i64),
                "coff": _dev(self._coff[:-1][sel], i64),
                "moff": _dev(self._moff[:-1][sel], i64),
@@ -849,9 +851,11 @@ class SweepEngine:
             return out
         mvh = allh[nlm:]
         mf, vf = mvh[:nout], mvh[nout:].copy()
-        # moments.py:43-58 for every key at once: per-key scale, warn, clamp
-        keys, starts, shapes = tab["keys"], tab["key_start"], tab["key_shape"]
-        if len(starts):
+        # moments.py:43-58 for every key at once: per-key scale, warn, clamp.
+        # The scale is >= 1, so nothing can warn unless some entry is below
+        # -1e-12: only then are the per-key scales formed.
+        keys, starts = tab["keys"], tab["key_start"]
+        if len(starts) and vf.min(initial=0.0) < -1e-12:
             sumsq = np.abs(vf + mf * mf)
             scale = np.maximum(1.0, np.maximum.reduceat(sumsq, starts))
             sizes = np.diff(np.append(starts, nout))
@@ -862,10 +866,9 @@ class SweepEngine:
                     seg = vf[starts[j]: starts[j] + sizes[j]]
                     log.warning("field %s: %d variance entries below -1e-12*scale (min %.3e), "
                                 "clamping", keys[j], int(nbad[j]), float(seg.min()))
-            np.maximum(vf, 0.0, out=vf)
-        for j, key in enumerate(keys):
-            a, b = starts[j], starts[j] + int(np.prod(shapes[j]))
-            out[key] = (mf[a:b].reshape(shapes[j]), vf[a:b].reshape(shapes[j]))
+        np.maximum(vf, 0.0, out=vf)
+        out.update({key: (mf[a:b].reshape(sh), vf[a:b].reshape(sh))
+                    for key, a, b, sh in tab["key_slices"]})
         return out
 
 
