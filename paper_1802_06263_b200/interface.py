@@ -273,15 +273,33 @@ class _SweepStatic:
                     cur += pb.meshes[s].n_cells
         self.koff, self.sys_first = koff, first
         self.K = torch.empty(max(cur, 1), dtype=f64, device="cuda")
+        # The sweep's inputs (local-index table, weights, KL tables) live in
+        # one device staging buffer (refresh_inputs: one pinned H2D copy);
+        # the KL tables are views into it.
+        self._plan = plan
+        kl_host = [(s, self._kl_tables(plan, s)) for s in plan.darcy]
+        sizes = [4 * int(plan.d_local.numel()), 8 * int(plan.d_weights.numel())]
+        for _, (phi, mean, xi) in kl_host:
+            sizes += [phi.nbytes, mean.nbytes, xi.nbytes]
+        offs = np.concatenate([[0], np.cumsum([(b + 15) // 16 * 16 for b in sizes])])
+        self._stage_offs = offs
+        self._stage_dev = torch.zeros(max(int(offs[-1]), 16), dtype=torch.uint8, device="cuda")
+
+        def view(j, dtype, shape):
+            return self._stage_dev[int(offs[j]):int(offs[j]) + sizes[j]].view(dtype).view(shape)
+
         self.kl = []
-        for s in plan.darcy:
-            phi, mean, xi = self._kl_tables(plan, s)
+        for j, (s, (phi, mean, xi)) in enumerate(kl_host):
             if method == "S2":
                 dst, ld = plan.k0_len + plan.k0_off[s], plan.k0_len
             else:
                 dst, ld = int(koff[first[s]]), len(mean)
-            self.kl.append((s, len(mean), phi.shape[1], _dev(phi, f64), _dev(mean, f64),
-                            _dev(xi, f64), int(dst), xi.shape[0] - 1, int(ld)))
+            d_phi = view(2 + 3 * j, f64, phi.shape)
+            d_mean = view(3 + 3 * j, f64, mean.shape)
+            d_xi = view(4 + 3 * j, f64, xi.shape)
+            self.kl.append((s, len(mean), phi.shape[1], d_phi, d_mean, d_xi, int(dst),
+                            xi.shape[0] - 1, int(ld)))
+        self.refresh_inputs()
         self.kl_h2d_bytes = sum(8 * (t[3].numel() + t[4].numel() + t[5].numel())
                                 for t in self.kl)
         # the same tables as one MfbKlTable array: a single batched KL launch
@@ -300,7 +318,6 @@ class _SweepStatic:
             self.d_cg_local = _dev(np.arange(n_real, dtype=np.int32)[None, :], i32)
         else:
             self.d_cg_region, self.d_cg_local = plan.d_region, plan.d_local
-        self._plan = plan
         # (2) systems: pools and waves
         pats = plan.patterns
         sys_pat = np.array([s for s, _ in systems], dtype=np.int32)
@@ -527,40 +544,38 @@ class _SweepStatic:
         return self._side
 
     def refresh_inputs(self):
-        """Re-upload the sweep's inputs from the host -- collocation weights,
-        local-index tables and the KL tables (Phi, mean, local points) -- in
-        ONE pinned host->device copy, then device-side copies into place.
-        Returns the bytes transferred."""
+        """Re-upload the sweep's inputs from the host -- local-index tables,
+        collocation weights and the KL tables (Phi, mean, local points) -- in
+        ONE pinned host->device copy into the staging buffer the KL kernels
+        read; the plan's local-index table and weights are copied out of it
+        on the device. Returns the bytes transferred."""
         import torch
         plan, grid = self._plan, self._plan.grid
         li = np.stack(grid.local_indices).astype(np.int32) if grid.local_indices else \
             np.zeros((1, grid.n_real), dtype=np.int32)
-        pieces = [(plan.d_local, li), (plan.d_weights, np.ascontiguousarray(grid.weights))]
-        for s_, nc, nt, d_phi, d_mean, d_xi, *_ in self.kl:
-            phi, mean, xi = self._kl_tables(plan, s_)
-            pieces += [(d_phi, phi), (d_mean, mean), (d_xi, xi)]
-        stage = getattr(self, "_stage", None)
-        if stage is None:
-            offs, off = [], 0
-            for _, h in pieces:
-                offs.append(off)
-                off += (h.nbytes + 15) // 16 * 16
-            host = torch.empty(max(off, 16), dtype=torch.uint8, pin_memory=True)
-            dev = torch.empty(max(off, 16), dtype=torch.uint8, device="cuda")
-            stage = self._stage = (offs, off, host, dev)
-        offs, total, host, dev = stage
+        pieces = [li, np.ascontiguousarray(grid.weights)]
+        for s_, *_ in self.kl:
+            pieces += list(self._kl_tables(plan, s_))
+        offs = self._stage_offs
+        host = getattr(self, "_stage_host", None)
+        if host is None:
+            host = self._stage_host = torch.empty(self._stage_dev.numel(), dtype=torch.uint8,
+                                                  pin_memory=True)
         ev = getattr(self, "_stage_ev", None)
         if ev is not None:
             ev.synchronize()                     # the previous upload left the pinned buffer
         hv = host.numpy()
-        for (_, h), o in zip(pieces, offs):
-            hv[o:o + h.nbytes] = np.frombuffer(np.ascontiguousarray(h).tobytes(), dtype=np.uint8)
-        dev.copy_(host, non_blocking=True)
+        for h, o in zip(pieces, offs):
+            b = np.ascontiguousarray(h)
+            hv[int(o):int(o) + b.nbytes] = b.view(np.uint8).ravel()
+        self._stage_dev.copy_(host, non_blocking=True)
         self._stage_ev = torch.cuda.Event()
         self._stage_ev.record()
-        for (d, h), o in zip(pieces, offs):
-            d.view(-1).copy_(dev[o:o + h.nbytes].view(d.dtype))
-        return int(total)
+        n0, n1 = int(plan.d_local.numel()), int(plan.d_weights.numel())
+        plan.d_local.view(-1).copy_(self._stage_dev[:4 * n0].view(torch.int32))
+        plan.d_weights.copy_(
+            self._stage_dev[int(offs[1]):int(offs[1]) + 8 * n1].view(torch.float64))
+        return int(offs[-1])
 
 
 class SweepEngine:
