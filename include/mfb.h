@@ -16,6 +16,8 @@
  *                            compute_flux_basis and the bar solve
  *                            (problem.py:98-112, darcy.py:67-154,
  *                             stokes.py:112-322, interface.py:218-235, 166-177)
+ *   mfb_systems_apply     <- solve_star + side_functionals with stored
+ *                            factors (S1's direct_apply, interface.py:180-194)
  *   mfb_systems_extract   <- compute_flux_basis readout (interface.py:210-235),
  *                            side_functionals (problem.py:132-148),
  *                            postprocess (problem.py:150-158)
@@ -179,6 +181,19 @@ int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
                         double *hbar, const long long *sys_hoff,
                         double *M, const long long *sys_moff,
                         double *Fb, const long long *sys_fboff, void *stream);
+
+/*
+ * Solves with the factors mfb_systems_solve left in the work buffer (Method
+ * S1's star solves): item t applies system item_sys[t] to v = V[t*ldv ..]
+ * (one coefficient per local mortar dof): x = S^-1 (Q v) (rigid-body kernel
+ * projected out like the factorization's own solves) into X[t*ldx ..] (n+nb
+ * entries, may be NULL) and the readout Q^T x into R[t*ldr ..] (ndof
+ * entries, may be NULL). max_n: max n + nb over the items' systems.
+ */
+int mfb_systems_apply(const MfbPattern *pats, int n_items, const int *item_sys,
+                      const int *sys_pat, const double *work, const long long *sys_woff,
+                      const double *V, long long ldv, double *X, long long ldx, double *R,
+                      long long ldr, int max_n, void *stream);
 
 /*
  * Batched interface CG over points k0..k0+n_pts-1 (global indices).

@@ -186,7 +186,8 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
                                            int ldab, int kp, double *__restrict__ slot,
                                            double *__restrict__ udinv, unsigned int *ready,
                                            double *s_cand, double *s_fin,
-                                           unsigned long long *red_k, int *s_fail) {
+                                           unsigned long long *red_k, int *s_fail,
+                                           double *__restrict__ Lp = nullptr) {
     constexpr int NB = BAND_NB, NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int j0 = kp * NB, pnb = min(NB, n - j0);
@@ -350,6 +351,10 @@ __device__ __noinline__ int factor_publish(double *__restrict__ AB, int n, int k
                     const double v = (c < pnb && c < i) ? a[rr][c] * s_fin[2 * NB + c]
                                    : (i < pnb && c >= i) ? a[rr][c] * s_fin[3 * NB + i] : a[rr][c];
                     if (c < pnb && r - col <= kl && col - r <= kl + ku) AB[bidx(r, col, kl, ku, ldab)] = v;
+                    // the whole multiplier panel (rows by final position within
+                    // the panel can sit further than kl below their column:
+                    // the band cannot hold those, later solves need them)
+                    if (Lp && c < pnb && c < i) Lp[(long long)i * NB + c] = v;
                 }
             }
         }
@@ -507,14 +512,27 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     double *udinv = slots + D_MAX * SLOT;          // 1 / U(j, j), written by the panel owners
     // inverses of the diagonal 16 x 16 U blocks (back substitution), 16-byte aligned
     double *u11inv = udinv + n + ((reinterpret_cast<uintptr_t>(udinv + n) & 15) ? 1 : 0);
+    // the panels' pivot positions, kept for later solves with these factors
+    // (mfb_systems_apply: Method S1's matrix-free star solves)
+    int *piv = reinterpret_cast<int *>(u11inv + (long long)NB * NB * ((n + NB - 1) / NB));
+    // the multiplier panels, (kl + NB) x NB each, rows by final position
+    double *Lpan = reinterpret_cast<double *>(piv) + ((n + 1) / 2 + 1);
     unsigned int *ready = bar + gridDim.x / C + s;
     const int NTF = kl + NB <= NT ? 1 : 2;
     auto factor = [&](int kp) -> int {
         double *slot = slots + (kp % D) * SLOT;
-        return NTF == 1 ? factor_publish<NT, 1>(AB, n, kl, ku, ldab, kp, slot, udinv, ready,
-                                                s_cand, s_fin, s_fred_k, &s_ffail)
-                        : factor_publish<NT, 2>(AB, n, kl, ku, ldab, kp, slot, udinv, ready,
-                                                s_cand, s_fin, s_fred_k, &s_ffail);
+        double *Lp = Lpan + (long long)kp * (kl + NB) * NB;
+        const int f = NTF == 1 ? factor_publish<NT, 1>(AB, n, kl, ku, ldab, kp, slot, udinv,
+                                                       ready, s_cand, s_fin, s_fred_k, &s_ffail,
+                                                       Lp)
+                               : factor_publish<NT, 2>(AB, n, kl, ku, ldab, kp, slot, udinv,
+                                                       ready, s_cand, s_fin, s_fred_k, &s_ffail,
+                                                       Lp);
+        if (tid == 0) {          // written by this thread inside factor_publish
+            const int *sp = reinterpret_cast<const int *>(slot + (long long)(kl + NB) * NB + 2 * NB);
+            for (int c = 0; c < NB && kp * NB + c < n; ++c) piv[kp * NB + c] = sp[c];
+        }
+        return f;
     };
 #define OWNB(b) (((b) % C) == rank)
     if (rank == 0) {

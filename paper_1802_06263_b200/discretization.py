@@ -86,9 +86,12 @@ class Pattern:
     def work_doubles(self):
         # band, rhs rows, BAND_GROUP_MAX + 1 panel-publication slots ((kl + 16)
         # x 16 scaled factors + 32 scales + 16 doubles of pivots/flag), then n reciprocal U
-        # diagonals, then the inverses of the 16 x 16 diagonal U blocks (mfb_band.cu)
+        # diagonals, the inverses of the 16 x 16 diagonal U blocks, the n
+        # panel pivot positions (ints) and the (kl + 16) x 16 multiplier
+        # panels (mfb_band.cu)
         w = (self.ldab * self.n + self.n * (self.ndof + 1) + 1
-             + 17 * ((self.kl + 16) * 16 + 48) + self.n + 256 * ((self.n + 15) // 16) + 1)
+             + 17 * ((self.kl + 16) * 16 + 48) + self.n + 256 * ((self.n + 15) // 16) + 1
+             + (self.n + 1) // 2 + 1 + ((self.n + 15) // 16) * (self.kl + 16) * 16)
         return w + (w & 1)                 # even: every system's slots stay 16-byte aligned
 
     @property

@@ -237,9 +237,11 @@ class _SweepStatic:
     own blocks.
     """
 
-    def __init__(self, plan, keep_fields=True, darcy_kernel="hybrid", method="S3"):
+    def __init__(self, plan, keep_fields=True, darcy_kernel="hybrid", method="S3",
+                 keep_factors=False):
         import torch
         self.darcy_kernel = darcy_kernel
+        self.keep_factors = keep_factors
         self.method = method
         pb, grid = plan.problem, plan.grid
         lay = pb.layout
@@ -362,8 +364,11 @@ class _SweepStatic:
                 acc += 8 * (work_d[gen[pos]] + x_d[gen[pos]])
                 grp.append(gen[pos])
                 pos += 1
-            woff = np.concatenate([[0], np.cumsum([work_d[i] for i in grp])])
-            xoff = np.concatenate([[0], np.cumsum([x_d[i] for i in grp])])
+            # keep_factors: every wave gets its own region (the factors and
+            # the solutions stay for later solves); else the waves reuse one
+            wbase, xbase = (wmax, xmax) if keep_factors else (0, 0)
+            woff = wbase + np.concatenate([[0], np.cumsum([work_d[i] for i in grp])])
+            xoff = xbase + np.concatenate([[0], np.cumsum([x_d[i] for i in grp])])
             klmax = max(pats[systems[i][0]].kl for i in grp)
             # one panel row per thread when it fits (384 threads keep 170
             # registers per thread, 512 would cap them at 128 and spill)
@@ -581,13 +586,14 @@ class _SweepStatic:
 class SweepEngine:
     """Device work of one S3 or S2 sweep; methods map 1:1 onto the C ABI calls."""
 
-    def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid", method="S3"):
+    def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid", method="S3",
+                 keep_factors=False):
         import torch
         self.torch = torch
         self.plan = plan
         self.method = method
         self.L = _lib.lib()
-        self.st = plan.sweep_static(keep_fields, darcy_kernel, method)
+        self.st = plan.sweep_static(keep_fields, darcy_kernel, method, keep_factors)
         self.stream = torch.cuda.current_stream() if stream is None else stream
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
         self.launches = 0            # kernels launched through the C ABI

@@ -176,16 +176,20 @@ class DevicePlan:
             out += [(s, l) for l in range(int(self.n_loc[s]))]
         return out
 
-    def sweep_static(self, keep_fields=True, darcy_kernel="hybrid", method="S3"):
-        """Resident sweep state for `method` ("S3" or "S2"), cached per method."""
+    def sweep_static(self, keep_fields=True, darcy_kernel="hybrid", method="S3",
+                     keep_factors=False):
+        """Resident sweep state for `method` ("S3" or "S2"), cached per method.
+        keep_factors: every banded system keeps its own work region (its LU
+        stays for later solves, mfb_systems_apply)."""
         cache = self.__dict__.setdefault("_statics", {})
-        st = cache.get(method)
+        key = (method, keep_factors)
+        st = cache.get(key)
         if (st is None or (keep_fields and not st.keep_fields)
                 or st.darcy_kernel != darcy_kernel):
             from .interface import _SweepStatic
-            cache.pop(method, None)
-            st = _SweepStatic(self, keep_fields, darcy_kernel, method)
-            cache[method] = st
+            cache.pop(key, None)
+            st = _SweepStatic(self, keep_fields, darcy_kernel, method, keep_factors)
+            cache[key] = st
         return st
 
     def basis_bytes(self, method="S3"):
