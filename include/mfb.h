@@ -18,6 +18,9 @@
  *                             stokes.py:112-322, interface.py:218-235, 166-177)
  *   mfb_systems_apply     <- solve_star + side_functionals with stored
  *                            factors (S1's direct_apply, interface.py:180-194)
+ *   mfb_s1_cg_begin/_step <- S1's compute_rhs + cg_solve (interface.py:107-139,
+ *                            166-177), every point in lock step
+ *   mfb_s1_fields         <- S1's recover_fields (interface.py:250-260)
  *   mfb_systems_extract   <- compute_flux_basis readout (interface.py:210-235),
  *                            side_functionals (problem.py:132-148),
  *                            postprocess (problem.py:150-158)
@@ -193,7 +196,43 @@ int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
 int mfb_systems_apply(const MfbPattern *pats, int n_items, const int *item_sys,
                       const int *sys_pat, const double *work, const long long *sys_woff,
                       const double *V, long long ldv, double *X, long long ldx, double *R,
-                      long long ldr, int max_n, void *stream);
+                      long long ldr, int max_n, const int *item_live, void *stream);
+
+/*
+ * Method S1's interface CG (cg_solve with direct_apply, interface.py:107-139,
+ * 180-194) for n_pts points in lock step. Item of (point pt, subdomain s) =
+ * pt*n_sub + s; sides[4d..4d+3] = (i, a_i, j, a_j): mortar dof d is local dof
+ * a_i of subdomain i and a_j of j (j < 0: one side). Per point: x, r, p
+ * [n_lambda] (x ends as lambda), scal [2] (r.r, ||g||), iters, status
+ * (MFB_CG_*; 4 while running). V [items x ldv]: the next apply's input
+ * (p restricted to each item's subdomain; x once the point has finished),
+ * item_live: 0 once the item's point has finished (mfb_systems_apply skips
+ * it), *n_running: points still iterating.
+ *   begin: g from the bar readouts hbar[item_hoff[item] + a] (compute_rhs,
+ *          interface.py:166-177), x = 0, r = p = g (g_out may be NULL);
+ *   step:  Sp from the apply's readouts R[item*ldr + a], then one CG update
+ *          (the relative residual of iteration it goes to
+ *          res_hist[pt*hist_cap + it-1] while it <= hist_cap).
+ */
+int mfb_s1_cg_begin(int n_lambda, int n_pts, int n_sub, const int *sides, const double *hbar,
+                    const long long *item_hoff, double *x, double *r, double *p, double *scal,
+                    int *iters, int *status, double *V, long long ldv, int *item_live,
+                    int *n_running, double *g_out, void *stream);
+int mfb_s1_cg_step(int n_lambda, int n_pts, int n_sub, const int *sides, const double *R,
+                   long long ldr, double tol, int max_iter, double *x, double *r, double *p,
+                   double *scal, int *iters, int *status, double *res_hist, int hist_cap,
+                   double *V, long long ldv, int *item_live, int *n_running, void *stream);
+
+/*
+ * Fields of S1's recovery (recover_fields + postprocess, interface.py:250-260,
+ * problem.py:150-158): item t with star solution X[t*ldx ..] (from
+ * mfb_systems_apply) writes F[item_foff[t] + f] = Fb[sys_fboff[sys] + f] -
+ * (P x)_f for the nfield fields of its system's pattern (x = S^-1 Q v is
+ * minus the reference's star solution: Q carries the readout sign).
+ */
+int mfb_s1_fields(const MfbPattern *pats, int n_items, const int *item_sys, const int *sys_pat,
+                  const double *X, long long ldx, const double *Fb, const long long *sys_fboff,
+                  double *F, const long long *item_foff, void *stream);
 
 /*
  * Batched interface CG over points k0..k0+n_pts-1 (global indices).

@@ -52,12 +52,13 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
                   const int *__restrict__ sys_pat, const double *__restrict__ work,
                   const long long *__restrict__ sys_woff, const double *__restrict__ V,
                   long long ldv, double *__restrict__ Xout, long long ldx,
-                  double *__restrict__ Rout, long long ldr) {
+                  double *__restrict__ Rout, long long ldr, const int *__restrict__ item_live) {
     extern __shared__ double b[];                // n + nb
     __shared__ double red[4];
     __shared__ double s_part[8 * S1_NB];
     __shared__ double s_mu[S1_MAX_NB], s_cr[S1_MAX_NB];
     const int item = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (item_live && !item_live[item]) return;        // its CG point has finished
     const int s = item_sys[item];
     const MfbPattern P = pats[sys_pat[s]];
     const int n = P.n, kl = P.kl, ku = P.ku, ldab = P.ldab, nb = P.nb, nd = P.ndof;
@@ -84,9 +85,6 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
             b[P.q_row[q]] += P.q_val[q] * va;
         __syncthreads();
     }
-#if defined(S1_STOP) && S1_STOP == 1
-    return;
-#endif
     // ---- rigid-body kernel: b_I -= C_I^T (CC^T)^-1 C b -------------------
     if (nb > 0) {
         for (int a = 0; a < nb; ++a) {
@@ -158,9 +156,6 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
         }
         __syncthreads();
     }
-#if defined(S1_STOP) && S1_STOP == 2
-    return;
-#endif
     // ---- backward: b_blk -= U(blk, right) x, x_blk = U11^-1 b_blk -----------
     for (int k = nblk - 1; k >= 0; --k) {
         const int j0 = k * S1_NB, pnb = min(S1_NB, n - j0);
@@ -220,9 +215,6 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
         }
         __syncthreads();
     }
-#if defined(S1_STOP) && S1_STOP == 3
-    return;
-#endif
     // ---- outputs: x and the readout Q^T x --------------------------------
     if (Xout)
         for (int i = tid; i < n + nb; i += S1_NT) Xout[(long long)item * ldx + i] = b[i];
@@ -238,13 +230,156 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Method S1's interface CG (cg_solve, interface.py:107-139, with
+// direct_apply's matrix-free operator): every collocation point of the sweep
+// iterates in lock step, one CTA per point. Iteration = one apply launch
+// (the star solves of every live (point, subdomain) item) + one step launch
+// (the CG update of every running point). sides[4d..4d+3] = (i, a_i, j, a_j):
+// mortar dof d is local dof a_i of subdomain i and a_j of j (j < 0: one
+// side). Item of (point pt, subdomain s) = pt * n_sub + s.
+// scal[2pt] = r.r of the current residual, scal[2pt+1] = ||g||.
+constexpr int S1_CG_NT = 256;
+constexpr int S1_RUNNING = 4;
+
+__device__ __forceinline__ void s1_write_items(const double *__restrict__ src, int n_lambda,
+                                               const int *__restrict__ sides, int pt, int n_sub,
+                                               double *__restrict__ V, long long ldv) {
+    const long long base = (long long)pt * n_sub;
+    for (int d = threadIdx.x; d < n_lambda; d += S1_CG_NT) {
+        const int4 sd = reinterpret_cast<const int4 *>(sides)[d];
+        const double v = src[d];
+        V[(base + sd.x) * ldv + sd.y] = v;
+        if (sd.z >= 0) V[(base + sd.z) * ldv + sd.w] = v;
+    }
+}
+
+__device__ __forceinline__ void s1_finish(int pt, int n_sub, int *item_live, int *n_running) {
+    for (int s = threadIdx.x; s < n_sub; s += S1_CG_NT) item_live[(long long)pt * n_sub + s] = 0;
+    if (threadIdx.x == 0) atomicSub(n_running, 1);
+}
+
+__global__ void __launch_bounds__(S1_CG_NT)
+s1_cg_begin_kernel(int n_lambda, int n_sub, const int *__restrict__ sides,
+                   const double *__restrict__ hbar, const long long *__restrict__ item_hoff,
+                   double *__restrict__ x, double *__restrict__ r, double *__restrict__ p,
+                   double *__restrict__ scal, int *__restrict__ iters, int *__restrict__ status,
+                   double *__restrict__ V, long long ldv, int *__restrict__ item_live,
+                   int *__restrict__ n_running, double *__restrict__ g_out) {
+    __shared__ double red[S1_CG_NT / 32];
+    const int pt = blockIdx.x;
+    const long long o = (long long)pt * n_lambda, base = (long long)pt * n_sub;
+    // g = jump of the bar solutions (compute_rhs, interface.py:166-177)
+    double part = 0.0;
+    for (int d = threadIdx.x; d < n_lambda; d += S1_CG_NT) {
+        const int4 sd = reinterpret_cast<const int4 *>(sides)[d];
+        double g = hbar[item_hoff[base + sd.x] + sd.y];
+        if (sd.z >= 0) g += hbar[item_hoff[base + sd.z] + sd.w];
+        r[o + d] = g;
+        p[o + d] = g;
+        x[o + d] = 0.0;
+        if (g_out) g_out[o + d] = g;
+        part += g * g;
+    }
+    const double rr = block_sum<S1_CG_NT>(part, red);
+    const double gnorm = sqrt(rr);
+    if (threadIdx.x == 0) {
+        scal[2 * pt] = rr;
+        scal[2 * pt + 1] = gnorm;
+        iters[pt] = 0;
+        status[pt] = gnorm == 0.0 ? MFB_CG_ZERO_RHS : S1_RUNNING;
+        if (gnorm != 0.0) atomicAdd(n_running, 1);
+    }
+    for (int s = threadIdx.x; s < n_sub; s += S1_CG_NT) item_live[base + s] = gnorm != 0.0;
+    // the first apply's input: p = g (x = 0 for a zero right-hand side)
+    s1_write_items(p + o, n_lambda, sides, pt, n_sub, V, ldv);
+}
+
+__global__ void __launch_bounds__(S1_CG_NT)
+s1_cg_step_kernel(int n_lambda, int n_sub, const int *__restrict__ sides,
+                  const double *__restrict__ R, long long ldr, double tol, int max_iter,
+                  double *__restrict__ x, double *__restrict__ r, double *__restrict__ p,
+                  double *__restrict__ scal, int *__restrict__ iters, int *__restrict__ status,
+                  double *__restrict__ res_hist, int hist_cap, double *__restrict__ V,
+                  long long ldv, int *__restrict__ item_live, int *__restrict__ n_running) {
+    extern __shared__ double Sp[];                 // n_lambda
+    __shared__ double red[S1_CG_NT / 32];
+    const int pt = blockIdx.x, tid = threadIdx.x;
+    if (status[pt] != S1_RUNNING) return;
+    const long long o = (long long)pt * n_lambda, base = (long long)pt * n_sub;
+    double *xp = x + o, *rp = r + o, *pp = p + o;
+    const int it = iters[pt] + 1;
+    const double rr = scal[2 * pt], gnorm = scal[2 * pt + 1];
+    // Sp = -jump(side functionals of the star solves): each dof adds its
+    // two sides' readouts
+    double part = 0.0;
+    for (int d = tid; d < n_lambda; d += S1_CG_NT) {
+        const int4 sd = reinterpret_cast<const int4 *>(sides)[d];
+        double v = R[(base + sd.x) * ldr + sd.y];
+        if (sd.z >= 0) v += R[(base + sd.z) * ldr + sd.w];
+        Sp[d] = v;
+        part += pp[d] * v;
+    }
+    const double pSp = block_sum<S1_CG_NT>(part, red);
+    if (!(pSp > 0.0)) {
+        if (tid == 0) { status[pt] = MFB_CG_NOT_SPD; iters[pt] = it; }
+        s1_write_items(xp, n_lambda, sides, pt, n_sub, V, ldv);
+        s1_finish(pt, n_sub, item_live, n_running);
+        return;
+    }
+    const double a = rr / pSp;
+    part = 0.0;
+    for (int d = tid; d < n_lambda; d += S1_CG_NT) {
+        xp[d] += a * pp[d];
+        const double rd = rp[d] - a * Sp[d];
+        rp[d] = rd;
+        part += rd * rd;
+    }
+    const double rr_new = block_sum<S1_CG_NT>(part, red);
+    const double rn = sqrt(rr_new);
+    if (tid == 0 && it - 1 < hist_cap) res_hist[(long long)pt * hist_cap + it - 1] = rn / gnorm;
+    const bool conv = rn <= tol * gnorm;
+    if (conv || it >= max_iter) {
+        if (tid == 0) { status[pt] = conv ? MFB_CG_CONVERGED : MFB_CG_MAX_ITER; iters[pt] = it; }
+        __syncthreads();                               // x complete before the item copy
+        s1_write_items(xp, n_lambda, sides, pt, n_sub, V, ldv);   // the recovery's input
+        s1_finish(pt, n_sub, item_live, n_running);
+        return;
+    }
+    const double beta = rr_new / rr;
+    for (int d = tid; d < n_lambda; d += S1_CG_NT) pp[d] = rp[d] + beta * pp[d];
+    if (tid == 0) { scal[2 * pt] = rr_new; iters[pt] = it; }
+    __syncthreads();
+    s1_write_items(pp, n_lambda, sides, pt, n_sub, V, ldv);
+}
+
+// fields of (point, subdomain) item t: F[item_foff[t] + f] =
+// Fb_sys[f] - (P x)_f -- recover_fields + postprocess (interface.py:250-260,
+// problem.py:150-158): the bar fields plus the star solution's. Q carries
+// the readout's sign (B = Q^T S^-1 Q = -restrict(...), interface.py:230),
+// so x = S^-1 Q v is minus the reference's star solution.
+__global__ void __launch_bounds__(128)
+s1_fields_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ item_sys,
+                 const int *__restrict__ sys_pat, const double *__restrict__ X, long long ldx,
+                 const double *__restrict__ Fb, const long long *__restrict__ sys_fboff,
+                 double *__restrict__ F, const long long *__restrict__ item_foff) {
+    const int t = blockIdx.x, s = item_sys[t];
+    const MfbPattern P = pats[sys_pat[s]];
+    const double *xt = X + (long long)t * ldx;
+    for (int f = threadIdx.x; f < P.nfield; f += blockDim.x) {
+        double v = 0.0;
+        for (int q = P.p_ptr[f]; q < P.p_ptr[f + 1]; ++q) v += P.p_val[q] * xt[P.p_col[q]];
+        F[item_foff[t] + f] = Fb[sys_fboff[s] + f] - v;
+    }
+}
+
 }  // namespace
 
 extern "C" int mfb_systems_apply(const MfbPattern *pats, int n_items, const int *item_sys,
                                  const int *sys_pat, const double *work,
                                  const long long *sys_woff, const double *V, long long ldv,
                                  double *X, long long ldx, double *R, long long ldr,
-                                 int max_n, void *stream) {
+                                 int max_n, const int *item_live, void *stream) {
     if (n_items < 0 || max_n < 0) return MFB_ERR_ARG;
     if (n_items == 0) return MFB_OK;
     const size_t smem = (size_t)(max_n + S1_MAX_NB) * sizeof(double);
@@ -253,7 +388,54 @@ extern "C" int mfb_systems_apply(const MfbPattern *pats, int n_items, const int 
                              (int)smem) != cudaSuccess)
         return MFB_ERR_SMEM;
     band_apply_kernel<<<n_items, S1_NT, smem, mfb_stream(stream)>>>(
-        pats, item_sys, sys_pat, work, sys_woff, V, ldv, X, ldx, R, ldr);
+        pats, item_sys, sys_pat, work, sys_woff, V, ldv, X, ldx, R, ldr, item_live);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_s1_cg_begin(int n_lambda, int n_pts, int n_sub, const int *sides,
+                               const double *hbar, const long long *item_hoff, double *x,
+                               double *r, double *p, double *scal, int *iters, int *status,
+                               double *V, long long ldv, int *item_live, int *n_running,
+                               double *g_out, void *stream) {
+    if (n_lambda <= 0 || n_pts < 0 || n_sub <= 0) return MFB_ERR_ARG;
+    if (n_pts == 0) return MFB_OK;
+    cudaStream_t st = mfb_stream(stream);
+    if (cudaMemsetAsync(n_running, 0, sizeof(int), st) != cudaSuccess) return MFB_ERR_LAUNCH;
+    s1_cg_begin_kernel<<<n_pts, S1_CG_NT, 0, st>>>(n_lambda, n_sub, sides, hbar, item_hoff, x,
+                                                   r, p, scal, iters, status, V, ldv,
+                                                   item_live, n_running, g_out);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_s1_cg_step(int n_lambda, int n_pts, int n_sub, const int *sides,
+                              const double *R, long long ldr, double tol, int max_iter,
+                              double *x, double *r, double *p, double *scal, int *iters,
+                              int *status, double *res_hist, int hist_cap, double *V,
+                              long long ldv, int *item_live, int *n_running, void *stream) {
+    if (n_lambda <= 0 || n_pts < 0 || n_sub <= 0 || hist_cap < 1) return MFB_ERR_ARG;
+    if (n_pts == 0) return MFB_OK;
+    const size_t smem = (size_t)n_lambda * sizeof(double);
+    if (smem > 200 * 1024) return MFB_ERR_SMEM;
+    if (cudaFuncSetAttribute(s1_cg_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return MFB_ERR_SMEM;
+    s1_cg_step_kernel<<<n_pts, S1_CG_NT, smem, mfb_stream(stream)>>>(
+        n_lambda, n_sub, sides, R, ldr, tol, max_iter, x, r, p, scal, iters, status, res_hist,
+        hist_cap, V, ldv, item_live, n_running);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
+extern "C" int mfb_s1_fields(const MfbPattern *pats, int n_items, const int *item_sys,
+                             const int *sys_pat, const double *X, long long ldx,
+                             const double *Fb, const long long *sys_fboff, double *F,
+                             const long long *item_foff, void *stream) {
+    if (n_items < 0) return MFB_ERR_ARG;
+    if (n_items == 0) return MFB_OK;
+    s1_fields_kernel<<<n_items, 128, 0, mfb_stream(stream)>>>(pats, item_sys, sys_pat, X, ldx,
+                                                             Fb, sys_fboff, F, item_foff);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }

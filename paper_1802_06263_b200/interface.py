@@ -1,4 +1,4 @@
-"""Drop-in `run_method` for Methods S3 and S2 on one B200.
+"""Drop-in `run_method` for Methods S3, S2 and S1 on one B200.
 
 Same signature, return type and error behaviour as the reference's
 `sdmortar.interface.run_method` (interface.py:288-346): a `RunResult` with
@@ -16,8 +16,11 @@ the device through the C ABI (include/mfb.h):
      per-group shifted statistics)
 
 Method S2 (the deterministic MFB) runs the same kernels
-with one system per (subdomain, global realization). Method S1 is not on
-this path and raises NotImplementedError -- there is no CPU fallback.
+with one system per (subdomain, global realization). Method S1 (matrix-free,
+8f row 2) factors the same per-realization systems, keeps the factors, and
+applies the interface operator by a batched star solve per CG iteration
+(mfb_systems_apply + mfb_s1_cg_step); its moments stream every point's
+fields in realization order. There is no CPU fallback.
 """
 
 import ctypes
@@ -39,6 +42,7 @@ _PLAN_CACHE = {}
 WORK_BUDGET_BYTES = 16 << 30
 N_SMS = 148                 # B200
 BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
+S1_FIELD_BYTES_MAX = 32 << 30   # S1 keeps every realization's fields for the moments
 
 
 @dataclass
@@ -796,6 +800,152 @@ class SweepEngine:
             st._multi = mt
         return mt
 
+    # ------------------------------------------------ (3') S1 CG ------------
+    def _s1_tables(self):
+        """Item tables of Method S1 (cached on the static state). Item of
+        (point k, subdomain s) = k * n_sub + s; its system is the S2 system
+        (s, k) = s * n_real + k, whose factors stay in the work buffer."""
+        st, plan, torch = self.st, self.plan, self.torch
+        t = getattr(st, "_s1", None)
+        if t is not None:
+            return t
+        if st.method != "S2" or st.hwaves or not st.keep_factors or not st.keep_fields:
+            raise ValueError("method S1 runs on an S2 sweep state with every system on the "
+                             "banded path, factors and fields kept")
+        n_real, n_sub = plan.grid.n_real, plan.n_sub
+        i32, i64 = torch.int32, torch.int64
+        woff = np.zeros(len(st.systems), dtype=np.int64)
+        for w in st.waves:
+            woff[w["idx"]] = w["woff"].cpu().numpy()
+        kk, ss = np.meshgrid(np.arange(n_real), np.arange(n_sub), indexing="ij")
+        item_sys = (ss * n_real + kk).ravel()
+        nout = int(st.out_off[-1])
+        item_foff = (kk * nout + st.out_off[:-1][ss]).ravel()
+        _, sides, _, _ = cg_tasks(n_sub, plan.ndof.astype(np.int64), plan.dof_ptr, plan.dof_map,
+                                  plan.n_lambda)
+        t = {"n_items": len(item_sys), "item_sys": _dev(item_sys.astype(np.int32), i32),
+             "item_hoff": _dev(st.sys_hoff[item_sys], i64),
+             "item_foff": _dev(item_foff.astype(np.int64), i64),
+             "sides": _dev(np.ascontiguousarray(sides, dtype=np.int32).ravel(), i32),
+             "woff": _dev(woff, i64), "fboff": _dev(st.sys_fboff, i64), "nout": nout,
+             "max_n": max(int(p.n + p.nb) for p in plan.patterns)}
+        st._s1 = t
+        return t
+
+    def solve_s1(self, tol, max_iter, hist_cap=None, keep_g=False, check_every=16):
+        """Method S1's CG for every point at once (cg_solve with direct_apply,
+        interface.py:107-139, 180-194): each iteration is one batched star
+        solve of every live (point, subdomain) item with the stored factors,
+        then one CG update per point. The host checks the count of running
+        points once per `check_every` iterations, one check behind (no stall).
+        Returns (lam, iters, status, hist, g) like solve_points."""
+        torch, plan, st = self.torch, self.plan, self.st
+        t = self._s1_tables()
+        n_pts, nl, n_sub = plan.grid.n_real, plan.n_lambda, plan.n_sub
+        n_items, ldv = t["n_items"], int(plan.ndof.max())
+        hist_cap = max_iter if hist_cap is None else hist_cap
+        f64, i32 = torch.float64, torch.int32
+        x = torch.empty((n_pts, nl), dtype=f64, device="cuda")
+        r, p = torch.empty_like(x), torch.empty_like(x)
+        scal = torch.empty(2 * n_pts, dtype=f64, device="cuda")
+        iters = torch.empty(n_pts, dtype=i32, device="cuda")
+        status = torch.empty(n_pts, dtype=i32, device="cuda")
+        hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=f64, device="cuda")
+        V = torch.empty((n_items, ldv), dtype=f64, device="cuda")
+        R = torch.empty((n_items, ldv), dtype=f64, device="cuda")
+        live = torch.empty(n_items, dtype=i32, device="cuda")
+        nrun = torch.empty(1, dtype=i32, device="cuda")
+        g = torch.empty((n_pts, nl), dtype=f64, device="cuda") if keep_g else None
+        if self.timing:
+            e0 = self._ev()
+        self.launches += 1
+        _lib.check(self.L.mfb_s1_cg_begin(
+            nl, n_pts, n_sub, _ptr(t["sides"]), _ptr(st.hbar), _ptr(t["item_hoff"]), _ptr(x),
+            _ptr(r), _ptr(p), _ptr(scal), _ptr(iters), _ptr(status), _ptr(V), ldv, _ptr(live),
+            _ptr(nrun), _ptr(g) if keep_g else None, self.sp), "mfb_s1_cg_begin")
+        host = torch.empty(2, dtype=i32, pin_memory=True)
+        evs = [None, None]
+        it, c = 0, 0
+        while it < max_iter:
+            for _ in range(min(check_every, max_iter - it)):
+                _lib.check(self.L.mfb_systems_apply(
+                    _ptr(plan.pat_dev), n_items, _ptr(t["item_sys"]), _ptr(st.d_pat),
+                    _ptr(st.work), _ptr(t["woff"]), _ptr(V), ldv, None, 0, _ptr(R), ldv,
+                    t["max_n"], _ptr(live), self.sp), "mfb_systems_apply")
+                _lib.check(self.L.mfb_s1_cg_step(
+                    nl, n_pts, n_sub, _ptr(t["sides"]), _ptr(R), ldv, float(tol), int(max_iter),
+                    _ptr(x), _ptr(r), _ptr(p), _ptr(scal), _ptr(iters), _ptr(status),
+                    _ptr(hist), max(hist_cap, 1), _ptr(V), ldv, _ptr(live), _ptr(nrun), self.sp),
+                    "mfb_s1_cg_step")
+                self.launches += 2
+                it += 1
+            slot = c & 1
+            with torch.cuda.stream(self.stream):
+                host[slot:slot + 1].copy_(nrun, non_blocking=True)
+            evs[slot] = torch.cuda.Event()
+            evs[slot].record(self.stream)
+            prev = evs[slot ^ 1]
+            if prev is not None:
+                prev.synchronize()
+                if int(host[slot ^ 1]) == 0:
+                    break
+            c += 1
+        if self.timing:
+            self.cg_events.append((e0, self._ev(), n_pts))
+        self._s1_V = V                # every item's lambda restriction (recovery input)
+        self._s1_lam = x
+        return x, iters, status, hist, g
+
+    def s1_moments_launch(self):
+        """S1's recovery (recover_fields, interface.py:250-260): one more
+        batched star solve per (point, subdomain) with the final lambda, the
+        fields bar + star, and the moments of lambda and of every field in
+        realization order (MomentAccumulator, moments.py:25-58). Queued like
+        moments_launch; finish with moments_finish."""
+        torch, plan, st = self.torch, self.plan, self.st
+        t = self._s1_tables()
+        n_real, nl, nout = plan.grid.n_real, plan.n_lambda, t["nout"]
+        ldv, max_n, n_items = int(plan.ndof.max()), t["max_n"], t["n_items"]
+        f64 = torch.float64
+        if 8 * n_real * nout > S1_FIELD_BYTES_MAX:
+            raise SizeCapError(f"method S1 keeps every realization's fields on the device: "
+                               f"{8 * n_real * nout / 2 ** 30:.3g} GiB exceeds "
+                               f"{S1_FIELD_BYTES_MAX / 2 ** 30:.3g} GiB")
+        F = torch.empty((n_real, nout), dtype=f64, device="cuda")
+        chunk = max(1, min(n_items, (1 << 30) // (8 * max_n)))
+        X = torch.empty((chunk, max_n), dtype=f64, device="cuda")
+        V = self._s1_V
+        for a in range(0, n_items, chunk):
+            m = min(chunk, n_items - a)
+            self.launches += 2
+            _lib.check(self.L.mfb_systems_apply(
+                _ptr(plan.pat_dev), m, ctypes.c_void_p(t["item_sys"].data_ptr() + 4 * a),
+                _ptr(st.d_pat), _ptr(st.work), _ptr(t["woff"]),
+                ctypes.c_void_p(V.data_ptr() + 8 * a * ldv), ldv, _ptr(X), max_n, None, 0,
+                max_n, None, self.sp), "mfb_systems_apply")
+            _lib.check(self.L.mfb_s1_fields(
+                _ptr(plan.pat_dev), m, ctypes.c_void_p(t["item_sys"].data_ptr() + 4 * a),
+                _ptr(st.d_pat), _ptr(X), max_n, _ptr(st.Fb), _ptr(t["fboff"]), _ptr(F),
+                ctypes.c_void_p(t["item_foff"].data_ptr() + 8 * a), self.sp), "mfb_s1_fields")
+        x = self._s1_lam
+        res = torch.empty(3 * nl + 3 * nout, dtype=f64, device="cuda")
+        rp = res.data_ptr()
+        self.launches += 2
+        for n, src, off in ((nl, x, 0), (nout, F, 3 * nl)):
+            _lib.check(self.L.mfb_lambda_moments(
+                n, n_real, _ptr(src), _ptr(plan.d_weights), ctypes.c_void_p(rp + 8 * off),
+                ctypes.c_void_p(rp + 8 * (off + n)), ctypes.c_void_p(rp + 8 * (off + 2 * n)),
+                self.sp), "mfb_lambda_moments")
+        keep = 3 * nl + 2 * nout               # the fields' sum of squares stays behind
+        host = torch.empty(keep, dtype=f64, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            host.copy_(res[:keep], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        tab = st.moment_table(list(range(plan.n_sub)))
+        return {"host": host, "res": res, "F": F, "done": done, "tab": tab, "nl": nl,
+                "nlm": 3 * nl, "nout": nout, "ng": tab["n"], "with_lambda": True}
+
     # ----------------------------------------------------- (4) moments ----
     def moments(self, lam, sids=None, with_lambda=True):
         """Moment dict over the "lambda" key (if with_lambda) and the field keys
@@ -912,9 +1062,6 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     """
     if method not in METHODS:
         raise ValueError(f"unknown method {method!r}, expected one of {METHODS}")
-    if method == "S1":
-        raise NotImplementedError(
-            "method S1 (matrix-free) is not on this B200 path (S2/S3 only); no CPU fallback")
     _lib.lib()                      # raises NativeLibraryError: no CPU fallback
     import torch
     t0 = time.perf_counter()
@@ -925,9 +1072,16 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     if max_iter is None:
         max_iter = max(50, 10 * nl)
     plan = get_plan(problem, grid)
-    _check_basis_cap(plan.basis_bytes(method), basis_cap_mb)
+    if method != "S1":              # S1 stores no basis (interface.py:313-330)
+        _check_basis_cap(plan.basis_bytes(method), basis_cap_mb)
     timings = {"plan": time.perf_counter() - t0}
-    eng = SweepEngine(plan, method=method)
+    if method == "S1":
+        # S1 assembles and factors every subdomain per realization like S2
+        # (interface.py:316), every system on the banded LU whose factors
+        # the star solves reuse
+        eng = SweepEngine(plan, method="S2", darcy_kernel="band", keep_factors=True)
+    else:
+        eng = SweepEngine(plan, method=method)
     timings["h2d_bytes"] = eng.st.refresh_inputs()
     # everything is queued on the stream first (no host round trips between
     # the phases); the verdicts are checked in the reference's order after:
@@ -937,9 +1091,12 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     eng.kl_fields()
     eng.build_bases()
     ev[1].record(eng.stream)
-    lam, iters, status, hist, _ = eng.solve_points(tol, max_iter)
+    if method == "S1":
+        lam, iters, status, hist, _ = eng.solve_s1(tol, max_iter)
+    else:
+        lam, iters, status, hist, _ = eng.solve_points(tol, max_iter)
     ev[2].record(eng.stream)
-    mh = eng.moments_launch(lam)
+    mh = eng.s1_moments_launch() if method == "S1" else eng.moments_launch(lam)
     ev[3].record(eng.stream)
     # every result travels back in pinned buffers queued behind the moments:
     # one wait, then host-side assembly only
@@ -981,7 +1138,12 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     else:
         residuals = _pack_histories(hist, iters)
     stats.cg_iters = [int(x) for x in it]
-    for s in range(n_sub):
+    if method == "S1":
+        # per realization and subdomain: one factorization, the bar solve,
+        # one star solve per CG iteration and the recovery (interface.py:14-16)
+        stats.factorizations[:] = grid.n_real
+        stats.backsolves[:] = int(np.sum(it.astype(np.int64))) + 2 * grid.n_real
+    for s in range(n_sub if method != "S1" else 0):
         # S3: one factorization per (sid, loc); S2: per (sid, realization)
         nloc = int(eng.st.n_loc[s])
         stats.factorizations[s] = nloc

@@ -62,7 +62,5 @@ def test_method_and_cap_errors_before_device_work():
     _, problem, grid, _ = case_from_golden("cfg1")
     with pytest.raises(ValueError, match="unknown method"):
         run_method(problem, grid, method="S9")
-    with pytest.raises(NotImplementedError):
-        run_method(problem, grid, method="S1")
     with pytest.raises(SizeCapError, match="basis"):
         _check_basis_cap([8 * 12 * 12], 1e-9)

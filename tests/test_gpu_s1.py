@@ -1,8 +1,16 @@
-"""Solves with stored factors (mfb_systems_apply, the star solves of Method
-S1): applied to unit mortar coefficients they must reproduce the
-factorization's own solution columns X = S^-1 Q and the flux-basis columns
-B = Q^T X, for Darcy (generic band path) and Stokes systems, with and
-without the rigid-body kernel projection."""
+"""Method S1 (matrix-free) on the device.
+
+1. Solves with stored factors (mfb_systems_apply, the star solves of S1):
+   applied to unit mortar coefficients they must reproduce the
+   factorization's own solution columns X = S^-1 Q and the flux-basis
+   columns B = Q^T X, for Darcy (generic band path) and Stokes systems, with
+   and without the rigid-body kernel projection.
+2. The S1 sweep vs the reference's own S1 sweep (tests/golden/
+   make_golden_s1.py): lambda and moments within 1e-8 relative at CG tol
+   1e-11, or 10x the reference's own S1-vs-S2 difference (the same operator
+   applied two ways); iteration counts; the counters in S1 semantics
+   (backsolves = sum_k N_iter(k) + 2 N_real, interface.py:14-16).
+"""
 
 import ctypes
 
@@ -53,7 +61,7 @@ def test_apply_with_stored_factors_reproduces_the_solves(gpu, name):
         d_items = torch.as_tensor(np.array(items, dtype=np.int32), device="cuda")
         _lib.check(L.mfb_systems_apply(
             _ptr(plan.pat_dev), len(items), _ptr(d_items), _ptr(w["pat"]), _ptr(st.work),
-            _ptr(w["woff"]), _ptr(dV), nd_max, _ptr(dX), n_max, _ptr(dR), nd_max, n_max,
+            _ptr(w["woff"]), _ptr(dV), nd_max, _ptr(dX), n_max, _ptr(dR), nd_max, n_max, None,
             ctypes.c_void_p(eng.stream.cuda_stream)), "mfb_systems_apply")
         X = dX.cpu().numpy()
         R = dR.cpu().numpy()
@@ -69,3 +77,74 @@ def test_apply_with_stored_factors_reproduces_the_solves(gpu, name):
             assert np.max(np.abs(R[t, :nd] - bcol)) <= 1e-10 * np.max(np.abs(Bt))
             checked.add((int(pat[j]), int(P.nb) > 0))
     assert any(nbpos for _, nbpos in checked) or name != "cfg2"
+
+
+TOL = 1e-11
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b))
+                 / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "darcy_twoblock", "case1_mini", "cfg2"])
+def test_s1_sweep_matches_reference(gpu, name):
+    from conftest import golden
+    from paper_1802_06263_b200.interface import run_method
+    z = golden(name + "_s1")
+    z2 = golden(name + "_s2")
+    _, problem, grid, _ = case_from_golden(name)
+    res = run_method(problem, grid, method="S1", tol=TOL)
+    L = np.array(res.lambdas)
+    floor = _rel(z2["s2_lambda"], z["s1_lambda"])
+    assert _rel(L, z["s1_lambda"]) <= max(1e-8, 10 * floor), (_rel(L, z["s1_lambda"]), floor)
+    assert set(res.moments) == {k[len("mean__"):] for k in z.files if k.startswith("mean__")}
+    for key in res.moments:
+        m, v = res.moments[key]
+        mg, vg = z[f"mean__{key}"], z[f"var__{key}"]
+        assert m.shape == mg.shape and v.shape == vg.shape, key
+        fm = _rel(z2[f"mean__{key}"], mg)
+        assert (_rel(m, mg) <= max(1e-8, 10 * fm)
+                or np.max(np.abs(m - mg)) <= 1e-12), (key, _rel(m, mg), fm)
+        fv = _rel(z2[f"var__{key}"], vg)
+        scale = max(float(np.max(mg * mg)), 1e-300)
+        assert (_rel(v, vg) <= max(1e-8, 10 * fv)
+                or np.max(np.abs(v - vg)) / scale <= 1e-12), (key, _rel(v, vg), fv)
+    it = np.array(res.stats.cg_iters)
+    itg = z["s1_iters"]
+    assert abs(it.mean() - itg.mean()) <= 0.05 * itg.mean() + 2
+    # residual histories: one entry per iteration, ending below tol
+    assert [len(h) for h in res.residuals] == list(it)
+    assert all(h[-1] <= TOL for h in res.residuals if len(h))
+    # counters in S1 semantics, from our own iteration counts
+    n_real = grid.n_real
+    assert list(res.stats.factorizations) == [n_real] * problem.layout.n_subdomains
+    assert list(res.stats.basis_backsolves) == list(z["stats_basis_backsolves"])
+    assert list(res.stats.backsolves) == [int(it.sum()) + 2 * n_real] * \
+        problem.layout.n_subdomains
+    if np.array_equal(it, itg):
+        assert list(res.stats.backsolves) == list(z["stats_backsolves"])
+
+
+def test_s1_engine_statuses_and_budget(gpu):
+    """The S1 CG's exits: a budget too small ends every point with
+    MFB_CG_MAX_ITER after exactly max_iter iterations (ConvergenceError
+    through run_method, with the residual history), and the solves agree
+    with S2's lambda when converged."""
+    from paper_1802_06263_b200.errors import ConvergenceError
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan, run_method
+    _, problem, grid, _ = case_from_golden("cfg1")
+    with pytest.raises(ConvergenceError) as ei:
+        run_method(problem, grid, method="S1", tol=TOL, max_iter=5)
+    assert len(ei.value.residuals) == 5
+    plan = get_plan(problem, grid)
+    eng = SweepEngine(plan, method="S2", darcy_kernel="band", keep_factors=True)
+    eng.kl_fields()
+    eng.build_bases()
+    lam, iters, status, hist, g = eng.solve_s1(TOL, 500, keep_g=True, check_every=3)
+    assert np.all(status.cpu().numpy() == 0)
+    lam2, it2, st2, _, g2 = eng.solve_points(TOL, 500, keep_g=True)
+    assert np.all(st2.cpu().numpy() == 0)
+    assert _rel(g.cpu().numpy(), g2.cpu().numpy()) <= 1e-14
+    assert _rel(lam.cpu().numpy(), lam2.cpu().numpy()) <= 1e-8
+    assert np.max(np.abs(iters.cpu().numpy() - it2.cpu().numpy())) <= 2

@@ -99,15 +99,13 @@ def test_methods_and_size_cap_errors(gpu):
     """run_method's error conventions (interface.py:288-346): unknown method
     -> ValueError; the basis-memory cap -> SizeCapError before any device
     work, checked on the whole S3 pool (interface.py:375) but on ONE
-    realization's bases for S2 (interface.py:320-322); S1 is not on this
-    path and says so (no CPU fallback)."""
+    realization's bases for S2 (interface.py:320-322); S1 stores no basis
+    and ignores the cap."""
     from paper_1802_06263_b200.errors import SizeCapError
     from paper_1802_06263_b200.interface import get_plan, run_method
     _, problem, grid, _ = case_from_golden("cfg2")
     with pytest.raises(ValueError):
         run_method(problem, grid, method="S4")
-    with pytest.raises(NotImplementedError):
-        run_method(problem, grid, method="S1")
     plan = get_plan(problem, grid)
     s3_mb = sum(plan.basis_bytes("S3")) / 2 ** 20
     s2_mb = sum(plan.basis_bytes("S2")) / 2 ** 20
