@@ -180,6 +180,33 @@ def s2_comparison(plan, problem, grid, tol, max_iter, flush, steps=2):
                     "api": "run_method(problem, grid, 'S2', tol)"}}
 
 
+def s1_comparison(plan, problem, grid, tol, hbm_peak, steps=1):
+    """the same workload swept with Method S1 (matrix-free:
+    per-realization factors, one batched star solve per CG iteration) end to
+    end through run_method. The star solves stream the stored factors from
+    HBM every iteration: algorithmic bytes = sum over points of N_iter(k) x
+    (multiplier panels + U band of every subdomain), over the CG phase."""
+    from paper_1802_06263_b200.interface import run_method
+    run_method(problem, grid, method="S1", tol=tol)
+    t = time.perf_counter()
+    for _ in range(steps):
+        res = run_method(problem, grid, method="S1", tol=tol)
+    e2e = (time.perf_counter() - t) / steps
+    it = np.array(res.stats.cg_iters, dtype=np.int64)
+    per_pt = sum(8 * ((p.n + 15) // 16) * (p.kl + 16) * 16 + 8 * p.n * (p.kl + p.ku)
+                 for p in plan.patterns)
+    cg_s = res.timings["cg"]
+    ach = float(it.sum()) * per_pt / cg_s / 1e9
+    return {"method": "S1 (matrix-free)", "value": grid.n_real / e2e, "unit": "realizations/s",
+            "api": "run_method(problem, grid, 'S1', tol)", "steps": steps,
+            "cg_iters_mean": float(it.mean()), "cg_iters_max": int(it.max()),
+            "phases_s": {"bases": res.timings["bases"], "cg": cg_s,
+                         "recovery_moments": res.timings["moments"]},
+            "star_solve_roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                                    "unit": "GB/s", "frac": ach / hbm_peak if hbm_peak else None,
+                                    "bytes_per_point_iteration": per_pt}}
+
+
 def cpu_baseline(cfg_path, tol, sample_points=None):
     """Reference CPU algorithm (oracle port of sdmortar S3), 1 thread."""
     from threadpoolctl import threadpool_limits
@@ -530,6 +557,10 @@ def run_ours(a):
         }
         if not a.no_s2 and ws == 1:
             line["s2_comparison"] = s2_comparison(plan, problem, grid, a.tol, max_iter, flush)
+        if not a.no_s2 and ws == 1:
+            hbm = float(peaks.get("hbm_copy_gbs", peaks.get("hbm_gbs", 0.0)) or 0.0) \
+                if peaks else 0.0
+            line["s1_comparison"] = s1_comparison(plan, problem, grid, a.tol, hbm or None)
         if not a.no_cpu_baseline and ws == 1:
             cb = cpu_baseline(cfg_path, a.tol)
             line["cpu_baseline"] = {

@@ -192,11 +192,16 @@ int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
  * projected out like the factorization's own solves) into X[t*ldx ..] (n+nb
  * entries, may be NULL) and the readout Q^T x into R[t*ldr ..] (ndof
  * entries, may be NULL). max_n: max n + nb over the items' systems.
+ * item_live (may be NULL): items with item_live[t] == 0 are skipped.
+ * item_list (may be NULL): the launch covers items item_list[0..n_items-1]
+ * instead of 0..n_items-1 (a size class of systems per launch, so the
+ * shared-memory footprint of the short systems is not the longest's).
  */
 int mfb_systems_apply(const MfbPattern *pats, int n_items, const int *item_sys,
                       const int *sys_pat, const double *work, const long long *sys_woff,
                       const double *V, long long ldv, double *X, long long ldx, double *R,
-                      long long ldr, int max_n, const int *item_live, void *stream);
+                      long long ldr, int max_n, const int *item_live, const int *item_list,
+                      void *stream);
 
 /*
  * Method S1's interface CG (cg_solve with direct_apply, interface.py:107-139,

@@ -60,7 +60,8 @@ _SIGS = {
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
                         _p, _p, _p, _p, _i, _p, ctypes.c_longlong, _i, _p], _i),
-    "mfb_systems_apply": ([_p, _i, _p, _p, _p, _p, _p, _ll, _p, _ll, _p, _ll, _i, _p, _p], _i),
+    "mfb_systems_apply": ([_p, _i, _p, _p, _p, _p, _p, _ll, _p, _ll, _p, _ll, _i, _p, _p, _p],
+                          _i),
     "mfb_s1_cg_begin": ([_i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _ll, _p, _p, _p,
                          _p], _i),
     "mfb_s1_cg_step": ([_i, _i, _i, _p, _p, _ll, _d, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p,

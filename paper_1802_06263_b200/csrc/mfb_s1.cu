@@ -52,12 +52,14 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
                   const int *__restrict__ sys_pat, const double *__restrict__ work,
                   const long long *__restrict__ sys_woff, const double *__restrict__ V,
                   long long ldv, double *__restrict__ Xout, long long ldx,
-                  double *__restrict__ Rout, long long ldr, const int *__restrict__ item_live) {
+                  double *__restrict__ Rout, long long ldr, const int *__restrict__ item_live,
+                  const int *__restrict__ item_list) {
     extern __shared__ double b[];                // n + nb
     __shared__ double red[4];
     __shared__ double s_part[8 * S1_NB];
     __shared__ double s_mu[S1_MAX_NB], s_cr[S1_MAX_NB];
-    const int item = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int item = item_list ? item_list[blockIdx.x] : blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (item_live && !item_live[item]) return;        // its CG point has finished
     const int s = item_sys[item];
     const MfbPattern P = pats[sys_pat[s]];
@@ -147,12 +149,19 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
         __syncthreads();
         for (int i = S1_NB + tid; i < nr; i += S1_NT) {
             const double *li = Lk + (long long)i * S1_NB;
-            double a0 = 0.0, a1 = 0.0;
-            for (int c = 0; c < pnb; c += 2) {
-                a0 = fma(li[c], b[j0 + c], a0);
-                if (c + 1 < pnb) a1 = fma(li[c + 1], b[j0 + c + 1], a1);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (pnb == S1_NB) {                 // all 16 loads issued back to back
+#pragma unroll
+                for (int c = 0; c < S1_NB; c += 4) {
+                    a0 = fma(li[c], b[j0 + c], a0);
+                    a1 = fma(li[c + 1], b[j0 + c + 1], a1);
+                    a2 = fma(li[c + 2], b[j0 + c + 2], a2);
+                    a3 = fma(li[c + 3], b[j0 + c + 3], a3);
+                }
+            } else {
+                for (int c = 0; c < pnb; ++c) a0 = fma(li[c], b[j0 + c], a0);
             }
-            b[j0 + i] -= a0 + a1;
+            b[j0 + i] -= (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
     }
@@ -162,10 +171,21 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
         const int c0 = j0 + pnb, c1 = min(n, j0 + S1_NB + kl + ku);
         const int r = tid & (S1_NB - 1), part = tid >> 4;       // 8 parts
         double acc = 0.0;
-        if (r < pnb)
-            for (int col = c0 + part; col < c1; col += 8)
-                if (col - (j0 + r) <= kl + ku)
-                    acc = fma(AB[bidx1(j0 + r, col, kl, ku, ldab)], b[col], acc);
+        if (r < pnb) {
+            // columns of row j0+r inside the band: col - (j0+r) <= kl+ku;
+            // four independent chains keep four loads in flight
+            const int lim = min(c1, j0 + r + kl + ku + 1);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int col = c0 + part;
+            for (; col + 24 < lim; col += 32) {
+                a0 = fma(AB[bidx1(j0 + r, col, kl, ku, ldab)], b[col], a0);
+                a1 = fma(AB[bidx1(j0 + r, col + 8, kl, ku, ldab)], b[col + 8], a1);
+                a2 = fma(AB[bidx1(j0 + r, col + 16, kl, ku, ldab)], b[col + 16], a2);
+                a3 = fma(AB[bidx1(j0 + r, col + 24, kl, ku, ldab)], b[col + 24], a3);
+            }
+            for (; col < lim; col += 8) a0 = fma(AB[bidx1(j0 + r, col, kl, ku, ldab)], b[col], a0);
+            acc = (a0 + a1) + (a2 + a3);
+        }
         s_part[part * S1_NB + r] = acc;
         __syncthreads();
         if (tid < S1_NB) {
@@ -379,7 +399,8 @@ extern "C" int mfb_systems_apply(const MfbPattern *pats, int n_items, const int 
                                  const int *sys_pat, const double *work,
                                  const long long *sys_woff, const double *V, long long ldv,
                                  double *X, long long ldx, double *R, long long ldr,
-                                 int max_n, const int *item_live, void *stream) {
+                                 int max_n, const int *item_live, const int *item_list,
+                                 void *stream) {
     if (n_items < 0 || max_n < 0) return MFB_ERR_ARG;
     if (n_items == 0) return MFB_OK;
     const size_t smem = (size_t)(max_n + S1_MAX_NB) * sizeof(double);
@@ -388,7 +409,7 @@ extern "C" int mfb_systems_apply(const MfbPattern *pats, int n_items, const int 
                              (int)smem) != cudaSuccess)
         return MFB_ERR_SMEM;
     band_apply_kernel<<<n_items, S1_NT, smem, mfb_stream(stream)>>>(
-        pats, item_sys, sys_pat, work, sys_woff, V, ldv, X, ldx, R, ldr, item_live);
+        pats, item_sys, sys_pat, work, sys_woff, V, ldv, X, ldx, R, ldr, item_live, item_list);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }

@@ -823,7 +823,18 @@ class SweepEngine:
         item_foff = (kk * nout + st.out_off[:-1][ss]).ravel()
         _, sides, _, _ = cg_tasks(n_sub, plan.ndof.astype(np.int64), plan.dof_ptr, plan.dof_map,
                                   plan.n_lambda)
+        # size classes: the long systems (Stokes) and the rest get separate
+        # apply launches, each with its own shared-memory footprint, so all
+        # items of an iteration are resident at once
+        size = np.array([int(p.n + p.nb) for p in plan.patterns])[item_sys // n_real]
+        cut = size.max() // 2
+        classes = []
+        for m in (size > cut, size <= cut):
+            ids = np.nonzero(m)[0]
+            if len(ids):
+                classes.append((_dev(ids.astype(np.int32), i32), len(ids), int(size[ids].max())))
         t = {"n_items": len(item_sys), "item_sys": _dev(item_sys.astype(np.int32), i32),
+             "classes": classes,
              "item_hoff": _dev(st.sys_hoff[item_sys], i64),
              "item_foff": _dev(item_foff.astype(np.int64), i64),
              "sides": _dev(np.ascontiguousarray(sides, dtype=np.int32).ravel(), i32),
@@ -868,16 +879,13 @@ class SweepEngine:
         it, c = 0, 0
         while it < max_iter:
             for _ in range(min(check_every, max_iter - it)):
-                _lib.check(self.L.mfb_systems_apply(
-                    _ptr(plan.pat_dev), n_items, _ptr(t["item_sys"]), _ptr(st.d_pat),
-                    _ptr(st.work), _ptr(t["woff"]), _ptr(V), ldv, None, 0, _ptr(R), ldv,
-                    t["max_n"], _ptr(live), self.sp), "mfb_systems_apply")
+                self._s1_apply(t, V, ldv, None, 0, R, live)
                 _lib.check(self.L.mfb_s1_cg_step(
                     nl, n_pts, n_sub, _ptr(t["sides"]), _ptr(R), ldv, float(tol), int(max_iter),
                     _ptr(x), _ptr(r), _ptr(p), _ptr(scal), _ptr(iters), _ptr(status),
                     _ptr(hist), max(hist_cap, 1), _ptr(V), ldv, _ptr(live), _ptr(nrun), self.sp),
                     "mfb_s1_cg_step")
-                self.launches += 2
+                self.launches += 1
                 it += 1
             slot = c & 1
             with torch.cuda.stream(self.stream):
@@ -896,6 +904,25 @@ class SweepEngine:
         self._s1_lam = x
         return x, iters, status, hist, g
 
+    def _s1_apply(self, t, V, ldv, X, ldx, R, live):
+        """One batched star solve of every item: the long size class on the
+        side stream, concurrently with the short one on the engine's."""
+        torch, plan, st = self.torch, self.plan, self.st
+        cls = t["classes"]
+        side = st.side_stream() if len(cls) > 1 else None
+        if side is not None:
+            side.wait_stream(self.stream)
+        for j, (ids, n, max_n) in enumerate(cls):
+            sp = ctypes.c_void_p(side.cuda_stream) if (side is not None and j == 0) else self.sp
+            self.launches += 1
+            _lib.check(self.L.mfb_systems_apply(
+                _ptr(plan.pat_dev), n, _ptr(t["item_sys"]), _ptr(st.d_pat), _ptr(st.work),
+                _ptr(t["woff"]), _ptr(V), ldv, _ptr(X) if X is not None else None, ldx,
+                _ptr(R) if R is not None else None, ldv, max_n,
+                _ptr(live) if live is not None else None, _ptr(ids), sp), "mfb_systems_apply")
+        if side is not None:
+            self.stream.wait_stream(side)
+
     def s1_moments_launch(self):
         """S1's recovery (recover_fields, interface.py:250-260): one more
         batched star solve per (point, subdomain) with the final lambda, the
@@ -907,26 +934,19 @@ class SweepEngine:
         n_real, nl, nout = plan.grid.n_real, plan.n_lambda, t["nout"]
         ldv, max_n, n_items = int(plan.ndof.max()), t["max_n"], t["n_items"]
         f64 = torch.float64
-        if 8 * n_real * nout > S1_FIELD_BYTES_MAX:
-            raise SizeCapError(f"method S1 keeps every realization's fields on the device: "
-                               f"{8 * n_real * nout / 2 ** 30:.3g} GiB exceeds "
+        need = 8 * (n_real * nout + n_items * max_n)
+        if need > S1_FIELD_BYTES_MAX:
+            raise SizeCapError(f"method S1 keeps every realization's fields and star solutions "
+                               f"on the device: {need / 2 ** 30:.3g} GiB exceeds "
                                f"{S1_FIELD_BYTES_MAX / 2 ** 30:.3g} GiB")
         F = torch.empty((n_real, nout), dtype=f64, device="cuda")
-        chunk = max(1, min(n_items, (1 << 30) // (8 * max_n)))
-        X = torch.empty((chunk, max_n), dtype=f64, device="cuda")
-        V = self._s1_V
-        for a in range(0, n_items, chunk):
-            m = min(chunk, n_items - a)
-            self.launches += 2
-            _lib.check(self.L.mfb_systems_apply(
-                _ptr(plan.pat_dev), m, ctypes.c_void_p(t["item_sys"].data_ptr() + 4 * a),
-                _ptr(st.d_pat), _ptr(st.work), _ptr(t["woff"]),
-                ctypes.c_void_p(V.data_ptr() + 8 * a * ldv), ldv, _ptr(X), max_n, None, 0,
-                max_n, None, self.sp), "mfb_systems_apply")
-            _lib.check(self.L.mfb_s1_fields(
-                _ptr(plan.pat_dev), m, ctypes.c_void_p(t["item_sys"].data_ptr() + 4 * a),
-                _ptr(st.d_pat), _ptr(X), max_n, _ptr(st.Fb), _ptr(t["fboff"]), _ptr(F),
-                ctypes.c_void_p(t["item_foff"].data_ptr() + 8 * a), self.sp), "mfb_s1_fields")
+        X = torch.empty((n_items, max_n), dtype=f64, device="cuda")
+        self._s1_apply(t, self._s1_V, ldv, X, max_n, None, None)
+        self.launches += 1
+        _lib.check(self.L.mfb_s1_fields(
+            _ptr(plan.pat_dev), n_items, _ptr(t["item_sys"]), _ptr(st.d_pat), _ptr(X), max_n,
+            _ptr(st.Fb), _ptr(t["fboff"]), _ptr(F), _ptr(t["item_foff"]), self.sp),
+            "mfb_s1_fields")
         x = self._s1_lam
         res = torch.empty(3 * nl + 3 * nout, dtype=f64, device="cuda")
         rp = res.data_ptr()

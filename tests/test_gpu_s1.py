@@ -61,8 +61,8 @@ def test_apply_with_stored_factors_reproduces_the_solves(gpu, name):
         d_items = torch.as_tensor(np.array(items, dtype=np.int32), device="cuda")
         _lib.check(L.mfb_systems_apply(
             _ptr(plan.pat_dev), len(items), _ptr(d_items), _ptr(w["pat"]), _ptr(st.work),
-            _ptr(w["woff"]), _ptr(dV), nd_max, _ptr(dX), n_max, _ptr(dR), nd_max, n_max, None,
-            ctypes.c_void_p(eng.stream.cuda_stream)), "mfb_systems_apply")
+            _ptr(w["woff"]), _ptr(dV), nd_max, _ptr(dX), n_max, _ptr(dR), nd_max, n_max,
+            None, None, ctypes.c_void_p(eng.stream.cuda_stream)), "mfb_systems_apply")
         X = dX.cpu().numpy()
         R = dR.cpu().numpy()
         for t, (j, c) in enumerate(zip(items, cols)):
