@@ -148,3 +148,10 @@ def test_s1_engine_statuses_and_budget(gpu):
     assert _rel(g.cpu().numpy(), g2.cpu().numpy()) <= 1e-14
     assert _rel(lam.cpu().numpy(), lam2.cpu().numpy()) <= 1e-8
     assert np.max(np.abs(iters.cpu().numpy() - it2.cpu().numpy())) <= 2
+    assert np.all(hist.cpu().numpy()[np.arange(grid.n_real), iters.cpu().numpy() - 1] <= TOL)
+    # zero right-hand side (cg_solve's early return, interface.py:111-113):
+    # status MFB_CG_ZERO_RHS, no iterations, lambda = 0
+    eng.st.hbar.zero_()
+    lam0, it0, st0, _, _ = eng.solve_s1(TOL, 500)
+    assert np.all(st0.cpu().numpy() == 3) and np.all(it0.cpu().numpy() == 0)
+    assert not lam0.cpu().numpy().any()
