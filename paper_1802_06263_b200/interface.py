@@ -43,6 +43,7 @@ WORK_BUDGET_BYTES = 16 << 30
 N_SMS = 148                 # B200
 BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 S1_FIELD_BYTES_MAX = 32 << 30   # S1 keeps every realization's fields for the moments
+S1_CHUNK_REALIZATIONS = None    # S1 realizations per chunk (None: as many as fit)
 
 
 @dataclass
@@ -242,7 +243,7 @@ class _SweepStatic:
     """
 
     def __init__(self, plan, keep_fields=True, darcy_kernel="hybrid", method="S3",
-                 keep_factors=False):
+                 keep_factors=False, reals=None):
         import torch
         self.darcy_kernel = darcy_kernel
         self.keep_factors = keep_factors
@@ -251,9 +252,13 @@ class _SweepStatic:
         lay = pb.layout
         f64, i32, i64 = torch.float64, torch.int32, torch.int64
         n_real = grid.n_real
+        # S2 systems of realizations r0..r1-1 only (Method S1's realization
+        # chunks); the K buffer and KL tables still cover every realization
+        self.reals = (0, n_real) if reals is None else (int(reals[0]), int(reals[1]))
         if method == "S2":
-            systems = [(s, k) for s in range(plan.n_sub) for k in range(n_real)]
-            self.n_loc = np.full(plan.n_sub, n_real, dtype=np.int64)
+            r0, r1 = self.reals
+            systems = [(s, k) for s in range(plan.n_sub) for k in range(r0, r1)]
+            self.n_loc = np.full(plan.n_sub, r1 - r0, dtype=np.int64)
         else:
             systems = plan.s3_systems()
             self.n_loc = plan.n_loc.astype(np.int64).copy()
@@ -591,13 +596,13 @@ class SweepEngine:
     """Device work of one S3 or S2 sweep; methods map 1:1 onto the C ABI calls."""
 
     def __init__(self, plan, stream=None, keep_fields=True, darcy_kernel="hybrid", method="S3",
-                 keep_factors=False):
+                 keep_factors=False, reals=None):
         import torch
         self.torch = torch
         self.plan = plan
         self.method = method
         self.L = _lib.lib()
-        self.st = plan.sweep_static(keep_fields, darcy_kernel, method, keep_factors)
+        self.st = plan.sweep_static(keep_fields, darcy_kernel, method, keep_factors, reals)
         self.stream = torch.cuda.current_stream() if stream is None else stream
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
         self.launches = 0            # kernels launched through the C ABI
@@ -812,7 +817,7 @@ class SweepEngine:
         if st.method != "S2" or st.hwaves or not st.keep_factors or not st.keep_fields:
             raise ValueError("method S1 runs on an S2 sweep state with every system on the "
                              "banded path, factors and fields kept")
-        n_real, n_sub = plan.grid.n_real, plan.n_sub
+        n_real, n_sub = st.reals[1] - st.reals[0], plan.n_sub   # points of this state
         i32, i64 = torch.int32, torch.int64
         woff = np.zeros(len(st.systems), dtype=np.int64)
         for w in st.waves:
@@ -852,7 +857,7 @@ class SweepEngine:
         Returns (lam, iters, status, hist, g) like solve_points."""
         torch, plan, st = self.torch, self.plan, self.st
         t = self._s1_tables()
-        n_pts, nl, n_sub = plan.grid.n_real, plan.n_lambda, plan.n_sub
+        n_pts, nl, n_sub = st.reals[1] - st.reals[0], plan.n_lambda, plan.n_sub
         n_items, ldv = t["n_items"], int(plan.ndof.max())
         hist_cap = max_iter if hist_cap is None else hist_cap
         f64, i32 = torch.float64, torch.int32
@@ -923,35 +928,33 @@ class SweepEngine:
         if side is not None:
             self.stream.wait_stream(side)
 
-    def s1_moments_launch(self):
-        """S1's recovery (recover_fields, interface.py:250-260): one more
-        batched star solve per (point, subdomain) with the final lambda, the
-        fields bar + star, and the moments of lambda and of every field in
-        realization order (MomentAccumulator, moments.py:25-58). Queued like
-        moments_launch; finish with moments_finish."""
+    def s1_fields(self, F):
+        """S1's recovery (recover_fields, interface.py:250-260) for this
+        state's points: one more batched star solve per (point, subdomain)
+        with the final lambda, then the fields bar + star into the rows of
+        F (points x every field of every subdomain, rows in point order)."""
         torch, plan, st = self.torch, self.plan, self.st
         t = self._s1_tables()
-        n_real, nl, nout = plan.grid.n_real, plan.n_lambda, t["nout"]
         ldv, max_n, n_items = int(plan.ndof.max()), t["max_n"], t["n_items"]
-        f64 = torch.float64
-        need = 8 * (n_real * nout + n_items * max_n)
-        if need > S1_FIELD_BYTES_MAX:
-            raise SizeCapError(f"method S1 keeps every realization's fields and star solutions "
-                               f"on the device: {need / 2 ** 30:.3g} GiB exceeds "
-                               f"{S1_FIELD_BYTES_MAX / 2 ** 30:.3g} GiB")
-        F = torch.empty((n_real, nout), dtype=f64, device="cuda")
-        X = torch.empty((n_items, max_n), dtype=f64, device="cuda")
+        X = torch.empty((n_items, max_n), dtype=torch.float64, device="cuda")
         self._s1_apply(t, self._s1_V, ldv, X, max_n, None, None)
         self.launches += 1
         _lib.check(self.L.mfb_s1_fields(
             _ptr(plan.pat_dev), n_items, _ptr(t["item_sys"]), _ptr(st.d_pat), _ptr(X), max_n,
             _ptr(st.Fb), _ptr(t["fboff"]), _ptr(F), _ptr(t["item_foff"]), self.sp),
             "mfb_s1_fields")
-        x = self._s1_lam
+
+    def s1_moments(self, lam, F):
+        """Moments of lambda and of every field over all realizations, in
+        realization order (MomentAccumulator, moments.py:25-58), queued like
+        moments_launch; finish with moments_finish."""
+        torch, plan, st = self.torch, self.plan, self.st
+        n_real, nl, nout = plan.grid.n_real, plan.n_lambda, int(st.out_off[-1])
+        f64 = torch.float64
         res = torch.empty(3 * nl + 3 * nout, dtype=f64, device="cuda")
         rp = res.data_ptr()
         self.launches += 2
-        for n, src, off in ((nl, x, 0), (nout, F, 3 * nl)):
+        for n, src, off in ((nl, lam, 0), (nout, F, 3 * nl)):
             _lib.check(self.L.mfb_lambda_moments(
                 n, n_real, _ptr(src), _ptr(plan.d_weights), ctypes.c_void_p(rp + 8 * off),
                 ctypes.c_void_p(rp + 8 * (off + n)), ctypes.c_void_p(rp + 8 * (off + 2 * n)),
@@ -965,6 +968,15 @@ class SweepEngine:
         tab = st.moment_table(list(range(plan.n_sub)))
         return {"host": host, "res": res, "F": F, "done": done, "tab": tab, "nl": nl,
                 "nlm": 3 * nl, "nout": nout, "ng": tab["n"], "with_lambda": True}
+
+    def s1_moments_launch(self):
+        """Recovery and moments of a single-state S1 sweep (every point)."""
+        torch, plan = self.torch, self.plan
+        n_real, nout = plan.grid.n_real, int(self.st.out_off[-1])
+        _s1_check_fields(n_real, nout)
+        F = torch.empty((n_real, nout), dtype=torch.float64, device="cuda")
+        self.s1_fields(F)
+        return self.s1_moments(self._s1_lam, F)
 
     # ----------------------------------------------------- (4) moments ----
     def moments(self, lam, sids=None, with_lambda=True):
@@ -1063,6 +1075,13 @@ class SweepEngine:
         return out
 
 
+def _s1_check_fields(n_real, nout):
+    need = 8 * n_real * nout
+    if need > S1_FIELD_BYTES_MAX:
+        raise SizeCapError(f"method S1 keeps every realization's fields on the device: "
+                           f"{need / 2 ** 30:.3g} GiB exceeds {S1_FIELD_BYTES_MAX / 2 ** 30:.3g} GiB")
+
+
 def _finalize(key, mean, var, sumsq):
     """Clamp tiny negative variances like moments.py:43-58."""
     scale = max(1.0, float(np.max(np.abs(sumsq), initial=0.0)))
@@ -1098,7 +1117,18 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     if method == "S1":
         # S1 assembles and factors every subdomain per realization like S2
         # (interface.py:316), every system on the banded LU whose factors
-        # the star solves reuse
+        # the star solves reuse: all of them stay resident
+        per_real = 8 * sum(int(p.work_doubles + p.x_doubles) for p in plan.patterns)
+        cached = plan.__dict__.get("_statics", {}).get(("S2", True))
+        if cached is None or cached.darcy_kernel != "band":
+            chunk = S1_CHUNK_REALIZATIONS
+            if chunk is None:
+                free = torch.cuda.mem_get_info()[0]
+                chunk = int(0.8 * free // max(per_real, 1))
+            if chunk < grid.n_real:
+                # too many factors for the device at once: realization chunks
+                return _run_s1_chunked(problem, grid, plan, tol, max_iter, stats, timings, t0,
+                                       max(chunk, 1))
         eng = SweepEngine(plan, method="S2", darcy_kernel="band", keep_factors=True)
     else:
         eng = SweepEngine(plan, method=method)
@@ -1172,3 +1202,62 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     stats.wall_seconds[:] = (time.perf_counter() - t0) / max(n_sub, 1)
     timings["total"] = time.perf_counter() - t0
     return RunResult(moments, stats, lambdas, residuals, grid, timings)
+
+
+def _run_s1_chunked(problem, grid, plan, tol, max_iter, stats, timings, t0, chunk):
+    """Method S1 in realization chunks when the factors of every (subdomain,
+    realization) do not fit on the device at once: each chunk assembles and
+    factors its realizations (an S2 state restricted to them), runs their
+    CG and recovery, and writes its rows of lambda and of the fields; the
+    moments run once over all rows in realization order, so the result does
+    not depend on the chunking. Verdicts in the reference's order: the first
+    chunk holding a singular operator or a failed point raises."""
+    import torch
+    n_real, nl = grid.n_real, plan.n_lambda
+    nout = int(np.sum(plan.nfield.astype(np.int64)))
+    _s1_check_fields(n_real, nout)
+    f64 = torch.float64
+    lam_all = torch.empty((n_real, nl), dtype=f64, device="cuda")
+    F = torch.empty((n_real, nout), dtype=f64, device="cuda")
+    it_all = np.zeros(n_real, dtype=np.int64)
+    hists = []
+    timings["chunks"] = 0
+    eng = None
+    for r0 in range(0, n_real, chunk):
+        r1 = min(n_real, r0 + chunk)
+        eng = None                              # the previous chunk's factors go first
+        torch.cuda.empty_cache()
+        eng = SweepEngine(plan, method="S2", darcy_kernel="band", keep_factors=True,
+                          reals=(r0, r1))
+        eng.kl_fields()
+        eng.build_bases()
+        lam, iters, status, hist, _ = eng.solve_s1(tol, max_iter)
+        eng.check_info()                        # syncs: singular operators first
+        st_h, it_h = status.cpu().numpy(), iters.cpu().numpy()
+        fail = np.nonzero((st_h == 1) | (st_h == 2))[0]
+        if len(fail):
+            j = int(fail[0])
+            res = hist[j].cpu().numpy()[:min(int(it_h[j]), hist.shape[1])].tolist()
+            k = r0 + j
+            if st_h[j] == 1:
+                raise ConvergenceError(f"interface operator is not positive definite "
+                                       f"(p.Sp <= 0 at iteration {int(it_h[j])}, point {k})",
+                                       res[:int(it_h[j]) - 1])
+            raise ConvergenceError(f"CG did not reach tol {tol:g} in {max_iter} iterations "
+                                   f"(last residual {res[-1]:.3e}, point {k})", res)
+        lam_all[r0:r1].copy_(lam)
+        eng.s1_fields(F[r0:r1])
+        it_all[r0:r1] = it_h
+        hists.append(_pack_histories(hist, iters))
+        timings["chunks"] += 1
+    mh = eng.s1_moments(lam_all, F)
+    moments = eng.moments_finish(mh)
+    flat = np.concatenate([h.array(j) for h in hists for j in range(len(h))]) \
+        if n_real else np.zeros(0)
+    residuals = ResidualHistories(flat, np.minimum(it_all, max_iter))
+    stats.cg_iters = [int(x) for x in it_all]
+    stats.factorizations[:] = n_real
+    stats.backsolves[:] = int(it_all.sum()) + 2 * n_real
+    stats.wall_seconds[:] = (time.perf_counter() - t0) / max(plan.n_sub, 1)
+    timings["total"] = time.perf_counter() - t0
+    return RunResult(moments, stats, list(lam_all.cpu().numpy()), residuals, grid, timings)

@@ -177,10 +177,15 @@ class DevicePlan:
         return out
 
     def sweep_static(self, keep_fields=True, darcy_kernel="hybrid", method="S3",
-                     keep_factors=False):
+                     keep_factors=False, reals=None):
         """Resident sweep state for `method` ("S3" or "S2"), cached per method.
         keep_factors: every banded system keeps its own work region (its LU
-        stays for later solves, mfb_systems_apply)."""
+        stays for later solves, mfb_systems_apply). reals = (r0, r1): an S2
+        state for realizations r0..r1-1 only, built fresh and not cached
+        (Method S1's realization chunks)."""
+        if reals is not None:
+            from .interface import _SweepStatic
+            return _SweepStatic(self, keep_fields, darcy_kernel, method, keep_factors, reals)
         cache = self.__dict__.setdefault("_statics", {})
         key = (method, keep_factors)
         st = cache.get(key)

@@ -155,3 +155,26 @@ def test_s1_engine_statuses_and_budget(gpu):
     lam0, it0, st0, _, _ = eng.solve_s1(TOL, 500)
     assert np.all(st0.cpu().numpy() == 3) and np.all(it0.cpu().numpy() == 0)
     assert not lam0.cpu().numpy().any()
+
+
+@pytest.mark.parametrize("name,chunk", [("cfg1", 4), ("case1_mini", 7)])
+def test_s1_realization_chunks_give_the_same_sweep(gpu, name, chunk, monkeypatch):
+    """When the factors of every realization do not fit at once, S1 runs in
+    realization chunks (cfg3 would need ~1 TB); every point's solve is its
+    own and the moments run once over all rows in realization order, so the
+    chunked sweep is bitwise the single-state one."""
+    import paper_1802_06263_b200.interface as itf
+    _, problem, grid, _ = case_from_golden(name)
+    ref = itf.run_method(problem, grid, method="S1", tol=TOL)
+    monkeypatch.setattr(itf, "S1_CHUNK_REALIZATIONS", chunk)
+    itf.get_plan(problem, grid).__dict__.get("_statics", {}).pop(("S2", True), None)
+    res = itf.run_method(problem, grid, method="S1", tol=TOL)
+    assert res.timings["chunks"] == -(-grid.n_real // chunk)
+    assert np.array_equal(np.array(res.lambdas), np.array(ref.lambdas))
+    assert set(res.moments) == set(ref.moments)
+    for key in ref.moments:
+        assert np.array_equal(res.moments[key][0], ref.moments[key][0]), key
+        assert np.array_equal(res.moments[key][1], ref.moments[key][1]), key
+    assert [list(h) for h in res.residuals] == [list(h) for h in ref.residuals]
+    assert list(res.stats.backsolves) == list(ref.stats.backsolves)
+    assert list(res.stats.factorizations) == list(ref.stats.factorizations)
