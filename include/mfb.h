@@ -163,13 +163,16 @@ int mfb_kl_realize_ld(const double *phi, const double *mean, int n_cells, int n_
  * threads: 256 or 384 per CTA (panel rows <= 2 x threads); smem_doubles: Pattern.smem_doubles of
  * the widest pattern. group: CTAs per system (>1: cooperative launch of
  * n_sys*group CTAs that split the trailing and rhs columns; `bar` is a
- * device scratch of n_sys counters, zeroed by the call).
+ * device scratch of n_sys counters, zeroed by the call). keep_factors != 0:
+ * the panels' pivot positions and multiplier panels are also stored in the
+ * workspace for later solves (mfb_systems_apply, Method S1).
  */
 int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *sys_pat,
                       const double *Kbuf, const long long *sys_koff,
                       double *work, const long long *sys_woff,
                       double *X, const long long *sys_xoff, int *info,
                       int threads, int smem_doubles, int group, unsigned int *bar,
+                      int keep_factors,
                       void *stream);
 
 /*

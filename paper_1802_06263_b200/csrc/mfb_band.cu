@@ -369,7 +369,7 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
                   const double *__restrict__ Kbuf, const long long *__restrict__ sys_koff,
                   double *__restrict__ work, const long long *__restrict__ sys_woff,
                   double *__restrict__ Xout, const long long *__restrict__ sys_xoff,
-                  int *__restrict__ info, int C, unsigned int *__restrict__ bar) {
+                  int *__restrict__ info, int C, unsigned int *__restrict__ bar, int keep) {
     constexpr int NB = BAND_NB;
     constexpr int PST = NB + 1;          // odd stride: lane-varying rows hit distinct banks
     constexpr int NW = NT / 32;
@@ -521,14 +521,14 @@ band_solve_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ s
     const int NTF = kl + NB <= NT ? 1 : 2;
     auto factor = [&](int kp) -> int {
         double *slot = slots + (kp % D) * SLOT;
-        double *Lp = Lpan + (long long)kp * (kl + NB) * NB;
+        double *Lp = keep ? Lpan + (long long)kp * (kl + NB) * NB : nullptr;
         const int f = NTF == 1 ? factor_publish<NT, 1>(AB, n, kl, ku, ldab, kp, slot, udinv,
                                                        ready, s_cand, s_fin, s_fred_k, &s_ffail,
                                                        Lp)
                                : factor_publish<NT, 2>(AB, n, kl, ku, ldab, kp, slot, udinv,
                                                        ready, s_cand, s_fin, s_fred_k, &s_ffail,
                                                        Lp);
-        if (tid == 0) {          // written by this thread inside factor_publish
+        if (keep && tid == 0) {  // written by this thread inside factor_publish
             const int *sp = reinterpret_cast<const int *>(slot + (long long)(kl + NB) * NB + 2 * NB);
             for (int c = 0; c < NB && kp * NB + c < n; ++c) piv[kp * NB + c] = sp[c];
         }
@@ -1065,7 +1065,7 @@ template <int NT>
 static int launch_band(int n_sys, int C, size_t smem, cudaStream_t st, const MfbPattern *pats,
                        const int *sys_pat, const double *Kbuf, const long long *sys_koff,
                        double *work, const long long *sys_woff, double *X,
-                       const long long *sys_xoff, int *info, unsigned int *bar) {
+                       const long long *sys_xoff, int *info, unsigned int *bar, int keep) {
     if (cudaFuncSetAttribute(band_solve_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return MFB_ERR_SMEM;
@@ -1074,13 +1074,14 @@ static int launch_band(int n_sys, int C, size_t smem, cudaStream_t st, const Mfb
         return MFB_ERR_LAUNCH;
     if (C == 1) {
         band_solve_kernel<NT><<<n_sys, NT, smem, st>>>(pats, sys_pat, Kbuf, sys_koff, work,
-                                                       sys_woff, X, sys_xoff, info, C, bar);
+                                                       sys_woff, X, sys_xoff, info, C, bar,
+                                                       keep);
     } else {
         // the C CTAs of a system wait on one another: cooperative launch
         // guarantees they are co-resident
         void *args[] = {(void *)&pats, (void *)&sys_pat, (void *)&Kbuf, (void *)&sys_koff,
                         (void *)&work, (void *)&sys_woff, (void *)&X, (void *)&sys_xoff,
-                        (void *)&info, (void *)&C, (void *)&bar};
+                        (void *)&info, (void *)&C, (void *)&bar, (void *)&keep};
         if (cudaLaunchCooperativeKernel((const void *)band_solve_kernel<NT>, dim3(n_sys * C),
                                         dim3(NT), args, smem, st) != cudaSuccess)
             return MFB_ERR_LAUNCH;
@@ -1093,16 +1094,19 @@ extern "C" int mfb_systems_solve(const MfbPattern *pats, int n_sys, const int *s
                                  const double *Kbuf, const long long *sys_koff,
                                  double *work, const long long *sys_woff, double *X,
                                  const long long *sys_xoff, int *info, int threads,
-                                 int smem_doubles, int group, unsigned int *bar, void *stream) {
+                                 int smem_doubles, int group, unsigned int *bar,
+                                 int keep_factors, void *stream) {
     if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
     if (group < 1 || group > BAND_GROUP_MAX || bar == nullptr) return MFB_ERR_ARG;
     const size_t smem = (size_t)smem_doubles * sizeof(double);
     cudaStream_t st = mfb_stream(stream);
     switch (threads) {
         case 256: return launch_band<256>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
-                                          work, sys_woff, X, sys_xoff, info, bar);
+                                          work, sys_woff, X, sys_xoff, info, bar,
+                                          keep_factors);
         case 384: return launch_band<384>(n_sys, group, smem, st, pats, sys_pat, Kbuf, sys_koff,
-                                          work, sys_woff, X, sys_xoff, info, bar);
+                                          work, sys_woff, X, sys_xoff, info, bar,
+                                          keep_factors);
         default: return MFB_ERR_ARG;
     }
 }

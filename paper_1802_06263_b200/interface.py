@@ -658,7 +658,8 @@ class SweepEngine:
             _lib.check(self.L.mfb_systems_solve(
                 _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
                 _ptr(st.work), _ptr(w["woff"]), _ptr(st.X), _ptr(w["xoff"]), _ptr(w["info"]),
-                w["nt"], st.smem, w["group"], _ptr(st.bar), sp_b), "mfb_systems_solve")
+                w["nt"], st.smem, w["group"], _ptr(st.bar), int(st.keep_factors), sp_b),
+                "mfb_systems_solve")
             if self.timing:
                 self.solve_events.append(("band", e0, self._ev(bs), w["flops"], w["flops"]))
             self.launches += 2

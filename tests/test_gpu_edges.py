@@ -69,7 +69,7 @@ def _solve_band(A, rows, cols, vals, kl, ku, rhs, group):
     L = _lib.lib()
     _lib.check(L.mfb_systems_solve(_ptr(pats), 1, _ptr(sys_pat), _ptr(K), _ptr(zero64),
                                    _ptr(work), _ptr(zero64), _ptr(X), _ptr(zero64), _ptr(info),
-                                   256, host.smem_doubles, group, _ptr(bar), None),
+                                   256, host.smem_doubles, group, _ptr(bar), 0, None),
                "mfb_systems_solve")
     torch.cuda.synchronize()
     return X.cpu().numpy().reshape(n, ndof + 1), int(info.item())
@@ -162,10 +162,10 @@ def test_empty_launches_are_noops(gpu):
     from paper_1802_06263_b200 import _lib
     L = _lib.lib()
     z = ctypes.c_void_p(0)
-    assert L.mfb_systems_solve(z, 0, z, z, z, z, z, z, z, z, 256, 0, 1, z, None) == 0
+    assert L.mfb_systems_solve(z, 0, z, z, z, z, z, z, z, z, 256, 0, 1, z, 0, None) == 0
     assert L.mfb_cg_batched(4, 1, z, z, z, z, z, z, z, 1, z, z, 0, 0, 1e-9, 10, z, z, z, z, 1,
                             z, 0, 0, None) == 0
-    assert L.mfb_systems_solve(z, -1, z, z, z, z, z, z, z, z, 256, 0, 1, z, None) == 1
+    assert L.mfb_systems_solve(z, -1, z, z, z, z, z, z, z, z, 256, 0, 1, z, 0, None) == 1
 
 
 def test_run_method_raises_convergence_error_with_history(gpu):
