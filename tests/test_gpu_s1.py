@@ -178,3 +178,27 @@ def test_s1_realization_chunks_give_the_same_sweep(gpu, name, chunk, monkeypatch
     assert [list(h) for h in res.residuals] == [list(h) for h in ref.residuals]
     assert list(res.stats.backsolves) == list(ref.stats.backsolves)
     assert list(res.stats.factorizations) == list(ref.stats.factorizations)
+
+
+def test_s1_equals_s2_on_the_device(gpu):
+    """Method equivalence (the reference's CRITERION, test_acceptance.py:
+    124-141): S1 and S2 solve the same per-realization interface problem --
+    lambda and every moment agree to 1e-8 at CG tol 1e-11, and the counters
+    keep their identities (S2: N_dof + 2 backsolves per realization and
+    subdomain; S1: sum_k N_iter(k) + 2 N_real)."""
+    from paper_1802_06263_b200.interface import run_method
+    _, problem, grid, _ = case_from_golden("cfg2")
+    r1 = run_method(problem, grid, method="S1", tol=TOL)
+    r2 = run_method(problem, grid, method="S2", tol=TOL)
+    assert _rel(np.array(r1.lambdas), np.array(r2.lambdas)) <= 1e-8
+    assert set(r1.moments) == set(r2.moments)
+    for key in r2.moments:
+        m1, v1 = r1.moments[key]
+        m2, v2 = r2.moments[key]
+        assert _rel(m1, m2) <= 1e-8 or np.max(np.abs(m1 - m2)) <= 1e-12, key
+        scale = max(float(np.max(m2 * m2)), 1e-300)
+        assert _rel(v1, v2) <= 1e-8 or np.max(np.abs(v1 - v2)) / scale <= 1e-12, key
+    n_real = grid.n_real
+    assert int(np.sum(r1.stats.basis_backsolves)) == 0
+    assert all(int(b) == int(np.sum(r1.stats.cg_iters)) + 2 * n_real for b in r1.stats.backsolves)
+    assert list(r1.stats.factorizations) == list(r2.stats.factorizations)
