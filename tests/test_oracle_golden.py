@@ -81,3 +81,21 @@ def test_oracle_s2_matches_reference(name):
         scale = max(float(np.max(mg ** 2)), 1e-300)
         assert (_rel(v, vg) <= max(1e-8, 10 * float(z[f"floor_var__{key}"]))
                 or np.max(np.abs(v - vg)) / scale <= 1e-12), key
+
+
+@pytest.mark.parametrize("name", ["cfg1", "darcy_twoblock"])
+def test_oracle_s1_matches_reference(name):
+    """The oracle's Method S1 (matrix-free: a star solve per subdomain per
+    CG iteration) against the reference's own S1 sweep
+    (tests/golden/make_golden_s1.py)."""
+    from oracle import s3_cpu
+    z = golden(name + "_s1")
+    _, problem, grid, _ = case_from_golden(name)
+    r = s3_cpu.run_s1(problem, grid, tol=TOL)
+    assert _rel(np.array(r["lambdas"]), z["s1_lambda"]) <= 1e-9
+    assert abs(np.mean(r["iters"]) - np.mean(z["s1_iters"])) <= 0.05 * np.mean(z["s1_iters"]) + 1
+    for key, (m, v) in r["moments"].items():
+        mg, vg = z[f"mean__{key}"], z[f"var__{key}"]
+        assert _rel(m, mg) <= 1e-8 or np.max(np.abs(m - mg)) <= 1e-12, key
+        scale = max(float(np.max(mg ** 2)), 1e-300)
+        assert _rel(v, vg) <= 1e-8 or np.max(np.abs(v - vg)) / scale <= 1e-12, key
