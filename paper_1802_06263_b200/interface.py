@@ -103,10 +103,30 @@ class ResidualHistories(Sequence):
     ~13k iterations) at 8 bytes per entry instead of a Python float each.
     """
 
-    def __init__(self, flat, iters):
+    def __init__(self, flat, iters, padded=None):
         self.flat = flat
         self.iters = np.asarray(iters, dtype=np.int64)
         self.offsets = np.concatenate([[0], np.cumsum(self.iters)])
+        self._padded = padded
+
+    @classmethod
+    def from_padded(cls, padded, iters):
+        """Histories left in the [points, cap] array the device wrote (row k
+        valid up to iters[k]): no repacking; `flat` is built on first use."""
+        h = cls.__new__(cls)
+        h.iters = np.asarray(iters, dtype=np.int64)
+        h._padded = padded
+        h._flat = None
+        return h
+
+    def __getattr__(self, name):          # lazy flat/offsets of a padded store
+        if name in ("flat", "offsets") and self.__dict__.get("_padded") is not None:
+            it = self.iters
+            mask = np.arange(self._padded.shape[1])[None, :] < it[:, None]
+            self.flat = self._padded[mask]
+            self.offsets = np.concatenate([[0], np.cumsum(it)])
+            return self.__dict__[name]
+        raise AttributeError(name)
 
     def __len__(self):
         return len(self.iters)
@@ -115,10 +135,12 @@ class ResidualHistories(Sequence):
         if isinstance(k, slice):
             return [self[j] for j in range(*k.indices(len(self)))]
         k = range(len(self))[k]
-        return self.flat[self.offsets[k]:self.offsets[k + 1]].tolist()
+        return self.array(k).tolist()
 
     def array(self, k):
         """Point k's history as a numpy view (no copy)."""
+        if self.__dict__.get("_padded") is not None:
+            return self._padded[k, :self.iters[k]]
         return self.flat[self.offsets[k]:self.offsets[k + 1]]
 
 
@@ -1184,8 +1206,7 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     lambdas = list(lam_h)
     if small_hist:
         it_c = np.minimum(it.astype(np.int64), hist.shape[1])
-        hh = h_hist.numpy()
-        residuals = ResidualHistories(hh[np.arange(hh.shape[1])[None, :] < it_c[:, None]], it_c)
+        residuals = ResidualHistories.from_padded(h_hist.numpy(), it_c)
     else:
         residuals = _pack_histories(hist, iters)
     stats.cg_iters = [int(x) for x in it]

@@ -76,3 +76,19 @@ def test_residual_histories_behave_like_lists():
     assert np.shares_memory(h.array(2), flat)
     with pytest.raises(IndexError):
         h[3]
+
+
+def test_residual_histories_from_the_padded_device_array():
+    """run_method keeps the [points, cap] history array the device wrote
+    (no host repacking on the end-to-end path); rows, views and the lazily
+    built flat storage behave as the flat-built histories."""
+    from paper_1802_06263_b200.interface import ResidualHistories
+    pad = np.array([[0.5, 0.25, 1e-12, 9.0], [9.0] * 4, [0.75, 1e-13, 9.0, 9.0]])
+    h = ResidualHistories.from_padded(pad, [3, 0, 2])
+    ref = ResidualHistories(np.array([0.5, 0.25, 1e-12, 0.75, 1e-13]), [3, 0, 2])
+    assert len(h) == 3 and [h[k] for k in range(3)] == [ref[k] for k in range(3)]
+    assert h[-1] == ref[-1] and h[0:2] == ref[0:2]
+    assert np.shares_memory(h.array(2), pad)
+    assert np.array_equal(h.flat, ref.flat) and np.array_equal(h.offsets, ref.offsets)
+    with pytest.raises(IndexError):
+        h[3]
