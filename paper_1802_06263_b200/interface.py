@@ -590,9 +590,19 @@ class _SweepStatic:
         li = np.stack(grid.local_indices).astype(np.int32) if grid.local_indices else \
             np.zeros((1, grid.n_real), dtype=np.int32)
         pieces = [li, np.ascontiguousarray(grid.weights)]
-        for s_, *_ in self.kl:
-            pieces += list(self._kl_tables(plan, s_))
         offs = self._stage_offs
+        # the KL tables (evaluated once per plan, _kl_tables) as one byte image
+        kl_img = getattr(self, "_kl_image", None)
+        if kl_img is None:
+            kl_img = np.zeros(int(offs[-1]) - int(offs[2]), dtype=np.uint8)
+            j = 2
+            for s_, *_ in self.kl:
+                for h in self._kl_tables(plan, s_):
+                    b = np.ascontiguousarray(h).view(np.uint8).ravel()
+                    a = int(offs[j]) - int(offs[2])
+                    kl_img[a:a + b.nbytes] = b
+                    j += 1
+            self._kl_image = kl_img
         host = getattr(self, "_stage_host", None)
         if host is None:
             host = self._stage_host = torch.empty(self._stage_dev.numel(), dtype=torch.uint8,
@@ -604,6 +614,7 @@ class _SweepStatic:
         for h, o in zip(pieces, offs):
             b = np.ascontiguousarray(h)
             hv[int(o):int(o) + b.nbytes] = b.view(np.uint8).ravel()
+        hv[int(offs[2]):int(offs[2]) + kl_img.nbytes] = kl_img
         self._stage_dev.copy_(host, non_blocking=True)
         self._stage_ev = torch.cuda.Event()
         self._stage_ev.record()
