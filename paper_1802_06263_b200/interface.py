@@ -576,7 +576,9 @@ class _SweepStatic:
         """Second stream for the banded (Stokes) waves of build_bases."""
         if getattr(self, "_side", None) is None:
             import torch
-            self._side = torch.cuda.Stream()
+            # high priority: the work put here (the Stokes systems) is the
+            # critical path, its CTAs are dispatched ahead of the other stream's
+            self._side = torch.cuda.Stream(priority=-1)
         return self._side
 
     def refresh_inputs(self):
