@@ -147,21 +147,32 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
             if (r < pnb) b[j0 + r] = br;
         }
         __syncthreads();
-        for (int i = S1_NB + tid; i < nr; i += S1_NT) {
-            const double *li = Lk + (long long)i * S1_NB;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            if (pnb == S1_NB) {                 // all 16 loads issued back to back
+        // L21: a half-warp per row (16 lanes = the panel's 16 columns), so
+        // every load instruction reads whole 128-byte rows -- no reliance on
+        // L1 hits between the 16 column loads of a row; four row pairs per
+        // warp in flight, then 16-lane shuffle sums
+        {
+            const int c = lane & 15, half = lane >> 4;
+            const double bc = c < pnb ? b[j0 + c] : 0.0;
+            constexpr int NW = S1_NT / 32, STEP = 2 * NW;
+            for (int base = S1_NB + 2 * wid + half; base - half < nr; base += 4 * STEP) {
+                double v[4];
 #pragma unroll
-                for (int c = 0; c < S1_NB; c += 4) {
-                    a0 = fma(li[c], b[j0 + c], a0);
-                    a1 = fma(li[c + 1], b[j0 + c + 1], a1);
-                    a2 = fma(li[c + 2], b[j0 + c + 2], a2);
-                    a3 = fma(li[c + 3], b[j0 + c + 3], a3);
+                for (int u = 0; u < 4; ++u) {
+                    const int i = base + u * STEP;
+                    v[u] = (i < nr && c < pnb) ? Lk[(long long)i * S1_NB + c] : 0.0;
                 }
-            } else {
-                for (int c = 0; c < pnb; ++c) a0 = fma(li[c], b[j0 + c], a0);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    double t = v[u] * bc;
+                    t += __shfl_xor_sync(0xffffffffu, t, 8);
+                    t += __shfl_xor_sync(0xffffffffu, t, 4);
+                    t += __shfl_xor_sync(0xffffffffu, t, 2);
+                    t += __shfl_xor_sync(0xffffffffu, t, 1);
+                    const int i = base + u * STEP;
+                    if (c == 0 && i < nr) b[j0 + i] -= t;
+                }
             }
-            b[j0 + i] -= (a0 + a1) + (a2 + a3);
         }
         __syncthreads();
     }
