@@ -121,10 +121,11 @@ band_apply_kernel(const MfbPattern *__restrict__ pats, const int *__restrict__ i
     for (int k = 0; k < nblk; ++k) {
         const int j0 = k * S1_NB, pnb = min(S1_NB, n - j0);
         const int nr = min(n, j0 + pnb + kl) - j0;
-        if (tid == 0) {
+        if (wid == 0) {         // the panel's pivots loaded at once, swapped in order
+            const int pv = lane < pnb ? piv[j0 + lane] : lane;
             for (int c = 0; c < pnb; ++c) {
-                const int p = piv[j0 + c];
-                if (p != c) {
+                const int p = __shfl_sync(0xffffffffu, pv, c);
+                if (lane == 0 && p != c) {
                     const double t = b[j0 + c];
                     b[j0 + c] = b[j0 + p];
                     b[j0 + p] = t;
