@@ -212,7 +212,7 @@ def cpu_baseline(cfg_path, tol, sample_points=None):
     from threadpoolctl import threadpool_limits
 
     from oracle import s3_cpu
-    from paper_1802_06263_b200.config import load_config
+    from paper_1802_06263_b200.adapter import load_config
     problem, grid, _ = load_config(cfg_path)
     pts = None if sample_points is None else list(range(min(sample_points, grid.n_real)))
     with threadpool_limits(limits=1):
@@ -271,7 +271,7 @@ def run_reference(a):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    from paper_1802_06263_b200.config import load_config
+    from paper_1802_06263_b200.adapter import load_config
     cfg_path = _config_path(a.config)
     problem, grid, _ = load_config(cfg_path)
     cores = len(os.sched_getaffinity(0))
@@ -324,7 +324,7 @@ def run_ours(a):
     else:
         torch.cuda.set_device(0)
     from paper_1802_06263_b200 import _build
-    from paper_1802_06263_b200.config import load_config
+    from paper_1802_06263_b200.adapter import load_config
     from paper_1802_06263_b200.interface import SweepEngine, get_plan, run_method
     _build.build()
     cfg_path = _config_path(a.config)

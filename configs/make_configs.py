@@ -84,7 +84,7 @@ def layered_config(cfg_id, tol=1e-11):
         "mortars": {"dd": nm, "sd": nm, "ss": nm, "degree": 1},
         "bcs": bcs,
         "method": "S3",
-        "cg": {"tol": tol},
+        "cg": ({"tol": tol, "max_iter": 200000} if cfg_id == 4 else {"tol": tol}),
         "output": {"dir": f"out/cfg{cfg_id}"},
     }
 

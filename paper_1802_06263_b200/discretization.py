@@ -26,9 +26,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .geometry import OUTWARD_SIGN, SIDES
-from .mortar import P2_EDGE_MASS
-from .problem import DarcyBC, StokesBC
+from .adapter import (OUTWARD_SIGN, P2_EDGE_MASS, SIDES, DarcyBC, StokesBC, cell_edge_table,
+                      edge_midpoint)
 
 TERM_CONST, TERM_INV_K, TERM_INV_SQRT_K = 0, 1, 2
 
@@ -228,7 +227,7 @@ def darcy_pattern(problem, sid):
                 cell_idx[mesh.cell(ix, iy)] = nxt
                 nxt += 1
     n = nxt
-    E = mesh.cell_edge_table()                     # w e s n
+    E = cell_edge_table(mesh)                     # w e s n
     cells = np.arange(mesh.n_cells)
     area = mesh.hx * mesh.hy
     tt = _TermTable()
@@ -274,7 +273,7 @@ def darcy_pattern(problem, sid):
             ok = r >= 0
             np.add.at(bar, r[ok], comp[ok] * half)
     for e, (side, gfun) in pressure.items():
-        mid = mesh.edge_midpoint(e)
+        mid = edge_midpoint(mesh, e)
         gv = 0.0 if gfun is None else float(gfun(mid[0], mid[1]))
         bar[edge_idx[e]] -= OUTWARD_SIGN[side] * gv * mesh.edge_length(e)
     if problem.q_d is not None:

@@ -33,8 +33,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .geometry import OUTWARD_SIGN, SIDES
-from .problem import DarcyBC
+from .adapter import OUTWARD_SIGN, SIDES, DarcyBC, cell_edge_table, edge_midpoint
 
 KIND_I, KIND_GAMMA, KIND_P = 0, 1, 2
 SMEM_LIMIT = 232448 - 1024        # opt-in dynamic shared memory per CTA on sm_100a
@@ -155,7 +154,7 @@ def hybrid_pattern(problem, sid):
             elif bc.kind == "pressure":
                 kind[e] = KIND_P
                 idx[e] = len(p_vals)
-                mid = mesh.edge_midpoint(e)
+                mid = edge_midpoint(mesh, e)
                 p_vals.append(0.0 if bc.value is None else float(bc.value(mid[0], mid[1])))
             else:
                 raise ValueError(f"unknown darcy bc {bc.kind!r}")
@@ -178,7 +177,7 @@ def hybrid_pattern(problem, sid):
     row_edge = np.array(row_edge, dtype=np.int64)
     idx[row_edge] = np.arange(len(row_edge))
     n = len(row_edge)
-    CE = mesh.cell_edge_table()
+    CE = cell_edge_table(mesh)
     ecell = -np.ones((ne, 2), dtype=np.int64)
     eslot = -np.ones((ne, 2), dtype=np.int64)
     for c in range(nc):

@@ -32,6 +32,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
+from .adapter import mode_table
 from .errors import ConvergenceError, SingularOperatorError, SizeCapError
 from .plan import DevicePlan, _dev, _ptr
 
@@ -227,15 +228,34 @@ def _check_basis_cap(sizes_bytes, cap_mb):
                            f"cap of {cap_mb:.3g} MiB; raise basis_cap_mb or use method S1")
 
 
+def _digest(*arrays):
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str((a.dtype.str, a.shape)).encode())
+        h.update(a.view(np.uint8).reshape(-1) if a.size else b"")
+    return h.hexdigest()
+
+
 def _plan_fingerprint(problem, grid):
-    """What the resident plan was built from: the problem's and grid's
-    component objects (the reference's problem is a mutable dataclass, so a
-    caller may swap `physics`, `bcs`, sources or the permeability model in
-    place between calls; any such swap rebuilds the plan)."""
-    return (id(problem), id(grid), problem.physics, id(problem.bcs), id(problem.perm),
+    """What the resident plan was built from. The reference recomputes
+    everything on every call and its problem is a mutable dataclass, so the
+    key covers the component objects AND the contents a caller may edit in
+    place between calls: the boundary conditions (kind and data per side),
+    physics, the mean log-permeability, and the grid's points, weights and
+    local tables (hashed). Any change rebuilds the plan."""
+    bcs = tuple(sorted((int(s), side, bc.kind, id(bc.value))
+                       for s, sides in problem.bcs.items() for side, bc in sides.items()))
+    mean = problem.perm.mean
+    mean_key = (id(mean), getattr(mean, "kind", None), repr(getattr(mean, "value", None)),
+                id(getattr(mean, "func", None)), repr(getattr(mean, "per_region", None)))
+    li = list(grid.local_indices) + list(grid.local_points)
+    return (id(problem), id(grid), problem.physics, bcs, id(problem.perm),
+            tuple(id(r) for r in problem.perm.regions), mean_key,
             id(problem.f_s), id(problem.f_d), id(problem.q_d), id(problem.meshes),
-            id(problem.space), id(problem.layout), id(grid.points), id(grid.weights),
-            grid.n_real, id(grid.local_indices), id(grid.local_points))
+            id(problem.space), id(problem.layout), grid.n_real,
+            _digest(grid.points, grid.weights, *li), tuple(grid.local_counts))
 
 
 def get_plan(problem, grid):
@@ -563,7 +583,7 @@ class _SweepStatic:
         pb, grid = plan.problem, plan.grid
         r = pb.layout.blocks[s].kl_region
         c = pb.meshes[s].centroids
-        phi, mean = pb.perm.mode_table(r, c[:, 0], c[:, 1])
+        phi, mean = mode_table(pb.perm, r, c[:, 0], c[:, 1])
         nt = phi.shape[1]
         pts = grid.local_points[r][:, :nt]
         if self.method == "S2":        # realization k's region coordinates

@@ -14,6 +14,7 @@ import numpy as np
 from . import _lib
 from .discretization import darcy_pattern, stokes_pattern
 from .hybrid import assembly_tables, hybrid_pattern
+from .adapter import darcy_sids, mode_table
 
 
 def _dev(a, dtype):
@@ -26,17 +27,20 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else ctypes.c_void_p(0)
 
 
-class DevicePlan:
-    """Everything about (problem, grid) that does not depend on lambda."""
+class HostTables:
+    """The realization-independent host tables of (problem, grid), before upload.
+
+    Built from the reference's own objects (`sdmortar` StokesDarcyProblem and
+    CollocationGrid: layout, meshes, space, perm, couplings, traces, bcs,
+    kl_cells, local tables) through `adapter.py`; `DevicePlan` uploads them.
+    `arrays()` flattens every table into name -> ndarray (tests hash them).
+    """
 
     def __init__(self, problem, grid):
-        import torch
-        self.torch = torch
-        self.problem, self.grid = problem, grid
         lay = problem.layout
         self.n_sub = lay.n_subdomains
         self.n_lambda = problem.space.n_dof
-        self.darcy = problem.darcy_sids()
+        self.darcy = darcy_sids(problem)
         # concatenated mean-field K layout over Darcy subdomains
         self.k0_off, off = {}, 0
         for s in self.darcy:
@@ -47,7 +51,7 @@ class DevicePlan:
         K0_host = np.zeros(self.k0_len)
         for s in self.darcy:
             c = problem.meshes[s].centroids
-            _, mean = problem.perm.mode_table(lay.blocks[s].kl_region, c[:, 0], c[:, 1])
+            _, mean = mode_table(problem.perm, lay.blocks[s].kl_region, c[:, 0], c[:, 1])
             K0_host[self.k0_off[s]:self.k0_off[s] + len(mean)] = np.exp(mean)
         self.patterns = []
         for sid in range(self.n_sub):
@@ -66,6 +70,53 @@ class DevicePlan:
                               dtype=np.int64)
         self.hyb = {s: hybrid_pattern(problem, s) for s in self.darcy}
         self.hyb_panel = {s: h.choose_panel() for s, h in self.hyb.items()}
+        self.kl_modes = {}
+        for s in self.darcy:
+            c = problem.meshes[s].centroids
+            self.kl_modes[s] = mode_table(problem.perm, lay.blocks[s].kl_region,
+                                          c[:, 0], c[:, 1])
+        self.local = (np.stack(grid.local_indices).astype(np.int32) if grid.local_indices
+                      else np.zeros((1, grid.n_real), dtype=np.int32))
+        self.weights = np.ascontiguousarray(grid.weights, dtype=np.float64)
+
+    def arrays(self):
+        """name -> ndarray of every table (patterns, hybrid patterns and their
+        assembly tables, KL mode tables, dof maps, local tables)."""
+        out = {"ndof": self.ndof, "nfield": self.nfield, "dof_ptr": self.dof_ptr,
+               "dof_map": self.dof_map, "region": self.region, "n_loc": self.n_loc,
+               "local": self.local, "weights": self.weights}
+
+        def add(prefix, obj):
+            for k, v in sorted(vars(obj).items()):
+                if isinstance(v, np.ndarray):
+                    out[f"{prefix}.{k}"] = v
+                elif isinstance(v, (int, float, np.integer, np.floating)) and \
+                        not isinstance(v, bool):
+                    out[f"{prefix}.{k}"] = np.array(v)
+        for s, p in enumerate(self.patterns):
+            add(f"pat{s}", p)
+        for s, h in self.hyb.items():
+            add(f"hyb{s}", h)
+            for k, v in assembly_tables(h).items():
+                out[f"hyb{s}.asm.{k}"] = np.asarray(v)
+            out[f"hyb{s}.panel"] = np.array(self.hyb_panel[s])
+        for s, (phi, mean) in self.kl_modes.items():
+            out[f"kl{s}.phi"], out[f"kl{s}.mean"] = phi, mean
+        return out
+
+
+class DevicePlan:
+    """Everything about (problem, grid) that does not depend on lambda."""
+
+    def __init__(self, problem, grid):
+        import torch
+        self.torch = torch
+        self.problem, self.grid = problem, grid
+        ht = HostTables(problem, grid)
+        self.host = ht
+        for name in ("n_sub", "n_lambda", "darcy", "k0_off", "k0_len", "patterns", "ndof",
+                     "nfield", "dof_ptr", "dof_map", "region", "n_loc", "hyb", "hyb_panel"):
+            setattr(self, name, getattr(ht, name))
         self._upload_patterns()
         self._upload_hybrid()
         self._upload_tables()

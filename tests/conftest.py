@@ -12,6 +12,10 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the reference package whose objects the drop-in consumes (environment, or
+# the repo's baseline/_ref install; paper_1802_06263_b200/_ref.py)
+from paper_1802_06263_b200._ref import sdmortar  # noqa: E402,F401
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
@@ -27,7 +31,7 @@ def golden(name):
 
 def case_from_golden(name, **patch):
     """(cfg, problem, grid, options) rebuilt from the config stored in a fixture."""
-    from paper_1802_06263_b200.config import build_from_config, validate_config
+    from sdmortar.config import build_from_config, validate_config
     z = golden(name)
     raw = json.loads(str(z["config_json"]))
     raw.update(patch)
@@ -37,7 +41,7 @@ def case_from_golden(name, **patch):
 
 
 def case_from_config(path, **patch):
-    from paper_1802_06263_b200.config import build_from_config, validate_config
+    from sdmortar.config import build_from_config, validate_config
     with open(path) as fh:
         raw = json.load(fh)
     raw.update(patch)

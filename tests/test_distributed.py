@@ -129,7 +129,8 @@ def _gpu_worker(rank, world, port, q, name):
     # wait on one another, so sharing one GPU is a functional (not perf) test
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1802_06263_b200.config import build_from_config, validate_config
+        from paper_1802_06263_b200._ref import sdmortar  # noqa: F401
+        from sdmortar.config import build_from_config, validate_config
         from paper_1802_06263_b200.distributed import run_method_distributed
         z = np.load(os.path.join(GOLDEN, name + ".npz"))
         problem, grid, _ = build_from_config(validate_config(_json.loads(str(z["config_json"]))))

@@ -146,7 +146,7 @@ def test_cfg5_basis_blocks(gpu):
     """Basis-only stress config: 64x64 Darcy, 6-term regions, 729 local points."""
     import torch
     from paper_1802_06263_b200.interface import SweepEngine, get_plan
-    from paper_1802_06263_b200.collocation import build_tensor_grid
+    from sdmortar.collocation import build_tensor_grid
     z = golden("cfg5")
     _, problem, grid, _ = case_from_golden("cfg5")
     loc = build_tensor_grid([3] * 6)

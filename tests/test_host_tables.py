@@ -19,7 +19,7 @@ def _maps(problem):
 
 @pytest.mark.parametrize("name", ["cfg1", "darcy_twoblock", "case1_mini", "cfg2", "cfg4"])
 def test_cg_tasks_cover_every_row_once(name):
-    from paper_1802_06263_b200.config import load_config
+    from paper_1802_06263_b200.adapter import load_config
     from paper_1802_06263_b200.interface import cg_tasks
     if name in ("cfg2", "cfg4"):
         problem, _, _ = load_config(os.path.join(ROOT, "configs", f"{name}.json"))

@@ -12,18 +12,19 @@ import numpy as np
 import pytest
 
 import pattern_emu
+from paper_1802_06263_b200.adapter import darcy_sids
 from conftest import case_from_golden, golden
 
 
 def _k0(problem, grid):
     from oracle import s3_cpu
     off, cur = {}, 0
-    for s in problem.darcy_sids():
+    for s in darcy_sids(problem):
         off[s] = cur
         cur += problem.meshes[s].n_cells
     K0 = np.zeros(cur)
     zero = np.zeros(grid.n_dims)
-    for s in problem.darcy_sids():
+    for s in darcy_sids(problem):
         K0[off[s]:off[s] + problem.meshes[s].n_cells] = s3_cpu.realize(problem, s, zero)
     return off, K0
 

@@ -1,8 +1,12 @@
-"""Host setup vs the reference (golden fixtures): bit-exact grids and index maps.
+"""Host setup vs the golden fixtures: bit-exact grids and index maps.
 
-The collocation nodes/weights, per-region local-index tables, interface list
-and mortar dof maps must be bit-for-bit the reference's (BASELINE.json
-north_star); they drive which basis block every point uses.
+The drop-in consumes the caller's sdmortar objects (adapter.py), so the
+collocation nodes/weights, per-region local-index tables, interface list and
+mortar dof maps ARE the reference's. This pins that the sdmortar + scipy of
+the running environment (here, and the GPU box's baseline/_ref install)
+reproduce, bit for bit, the setup the golden fixtures were generated with
+(BASELINE.json north_star: grids and index maps bit-exact); the device
+tables derived from them are pinned by test_adapter.py.
 """
 
 import hashlib
@@ -58,18 +62,6 @@ def test_cfg4_grid_hashes_bit_exact():
     assert problem.space.n_dof == 2720
 
 
-def test_gauss_hermite_known_values():
-    """Known nodes/weights (reference tests/test_collocation.py:14-24)."""
-    from paper_1802_06263_b200.collocation import gauss_hermite_rule
-    x, w = gauss_hermite_rule(2)
-    assert np.allclose(x, [-1.0, 1.0], atol=1e-14)
-    assert np.allclose(w, [0.5, 0.5], atol=1e-14)
-    x, w = gauss_hermite_rule(3)
-    assert np.allclose(x, [-np.sqrt(3), 0.0, np.sqrt(3)], atol=1e-14)
-    assert np.allclose(w, [1 / 6, 2 / 3, 1 / 6], atol=1e-14)
-    assert np.array_equal(x, -x[::-1])
-
-
 def test_case1_sizes():
     """Sizes the reference pins for case1_mini (test_config.py:248-258)."""
     _, problem, grid, _ = case_from_golden("case1_mini")
@@ -77,17 +69,3 @@ def test_case1_sizes():
     assert problem.space.n_dof == 48
     assert [len(problem.space.sub_dofs(lay, s)) for s in range(6)] == [12, 12, 20, 20, 16, 16]
     assert list(grid.local_counts) == [4, 8]
-
-
-def test_config_errors_are_collected():
-    from paper_1802_06263_b200.config import validate_config
-    from paper_1802_06263_b200.errors import ConfigError
-    with pytest.raises(ConfigError) as err:
-        validate_config({"domain": {"blocks": [{"rect": [0, 0, 1], "physics": "x",
-                                                "mesh": [0, 1]}]}, "bogus": 1})
-    assert len(err.value.messages) >= 3
-    with open(f"{ROOT}/configs/cfg2.json") as fh:
-        raw = json.load(fh)
-    raw["collocation"] = {"kind": "sparse", "level": -1}
-    with pytest.raises(ConfigError):
-        validate_config(raw)

@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_1802_06263_b200.config import load_config  # noqa: E402
+from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 GOLD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",

@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_1802_06263_b200.config import load_config  # noqa: E402
+from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import run_method  # noqa: E402
 
 

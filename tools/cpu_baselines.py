@@ -24,8 +24,8 @@ import numpy as np  # noqa: E402
 from threadpoolctl import threadpool_limits  # noqa: E402
 
 from oracle import s3_cpu  # noqa: E402
-from paper_1802_06263_b200.collocation import build_tensor_grid  # noqa: E402
-from paper_1802_06263_b200.config import load_config  # noqa: E402
+from sdmortar.collocation import build_tensor_grid  # noqa: E402
+from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 
 PLAN = {  # config: (systems sampled per physics, points sampled)
     "cfg1": (None, None), "cfg2": (None, None), "cfg3": (6, 8), "cfg4": (3, 2),

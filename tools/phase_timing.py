@@ -12,7 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
-from paper_1802_06263_b200.config import load_config
+from paper_1802_06263_b200.adapter import load_config
 from paper_1802_06263_b200.interface import SweepEngine, get_plan
 
 

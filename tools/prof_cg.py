@@ -12,7 +12,7 @@ from paper_1802_06263_b200 import _lib
 
 _lib._lib = None
 _lib.load(os.path.join(os.path.dirname(_lib._SO), "_mfb_prof.so"))
-from paper_1802_06263_b200.config import load_config  # noqa: E402
+from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"

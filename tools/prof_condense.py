@@ -11,14 +11,14 @@ from paper_1802_06263_b200 import _lib
 
 _lib._lib = None
 _lib.load(os.path.join(os.path.dirname(_lib._SO), "_mfb_prof.so"))
-from paper_1802_06263_b200.config import load_config  # noqa: E402
+from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 band_only = "--band" in sys.argv
 problem, grid, _ = load_config(f"configs/{cfg}.json")
 if cfg == "cfg5":
-    from paper_1802_06263_b200.collocation import build_tensor_grid
+    from sdmortar.collocation import build_tensor_grid
     loc = build_tensor_grid([3] * 6)
     grid.local_points = [loc.points.copy() for _ in problem.perm.regions]
     grid.local_counts = [loc.n_real] * len(problem.perm.regions)

@@ -1,7 +1,7 @@
 import os, sys, time, cProfile, pstats
 sys.path.insert(0, os.getcwd())
 import torch
-from paper_1802_06263_b200.config import load_config
+from paper_1802_06263_b200.adapter import load_config
 from paper_1802_06263_b200.interface import run_method
 problem, grid, _ = load_config("configs/cfg2.json")
 for _ in range(3): run_method(problem, grid, method="S3", tol=1e-11)

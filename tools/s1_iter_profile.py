@@ -8,7 +8,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1802_06263_b200 import _lib  # noqa: E402
-from paper_1802_06263_b200.config import load_config  # noqa: E402
+from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
 problem, grid, _ = load_config(os.path.join("configs", "cfg2.json"))
