@@ -277,7 +277,8 @@ int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
  * side). packed: the blocks in strip order (mfb_cg_pack), block of
  * (sid, loc) at pk_base[sid] + loc * pk_size[sid]. scratch:
  * mfb_cg_multi_scratch_doubles(n_lambda, n_cta) doubles (x, r and S p of
- * the points in flight).
+ * the points in flight). seg_tab != NULL: residual histories in segments of
+ * hist_cap entries, as mfb_cg_cluster's (res_hist = the pool).
  */
 long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta);
 int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int *dof_ptr,
@@ -287,7 +288,47 @@ int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int
                  double tol, int max_iter, double *lam, int *iters, int *status,
                  double *res_hist, int hist_cap, double *g, const int *tasks, int n_tasks,
                  const int *sides, const double *packed, const long long *pk_base,
-                 const int *pk_size, int n_cta, double *scratch, int *counter, void *stream);
+                 const int *pk_size, int n_cta, double *scratch, int *counter, int *seg_tab,
+                 int max_segs, long long seg_cap, int *seg_counter, void *stream);
+
+/*
+ * Same contract again, on thread-block clusters of C CTAs (C <= 8) holding
+ * NP (8 or 16) points in flight per cluster (csrc/mfb_cg_cluster.cu): the
+ * subdomains are split into C parts, CTA `rank` applies its part's blocks
+ * (packed fragment strips, mfb_cg_pack) and keeps p, S p and r of the mortar
+ * dofs it owns on chip; the two dot products are all-gathered over DSMEM.
+ * hdr[12 C] / tab: per-rank tables (paper_1802_06263_b200/cgcluster.py:
+ * owned dofs, halo peers, tasks, column maps, cut rows); n_own_max,
+ * n_used_max, n_cut_max, n_cm_max, n_unit_max, n_strip_max: their largest
+ * owned / used / cut row, column-map, unit and strip counts (every rank uses
+ * the same shared-memory layout, sized by
+ * these); flags bit 0 / bit 1: r / x of the owned rows in shared memory
+ * (else in rs / xs: n_clusters * C * n_own_max * NP doubles each); bit 2:
+ * S p in ss (same size) instead of shared memory; smem >=
+ * mfb_cg_cluster_smem(...) bytes of dynamic shared memory.
+ * Residual histories go to a segmented pool: the history of point k, entry
+ * i, is hist[seg_tab[k * max_segs + i / seg] * seg + i % seg]; segments are
+ * drawn from seg_counter (reset by the call); a segment index >= seg_cap is
+ * not stored (seg_tab entry -1) and the final seg_counter says how many
+ * segments the sweep needed. max_segs >= ceil(max_iter / seg).
+ * mfb_cg_cluster_max_clusters: co-resident clusters for (C, NP, n_own_max,
+ * smem) on this device (negative: MFB_ERR_* code).
+ */
+int mfb_cg_cluster_max_clusters(int C, int NP, int n_own_max, long long smem);
+int mfb_debug_cluster(int stop_at);   /* debug: stop the cluster CG at a phase (0: off; 100: phase clocks) */
+int mfb_debug_cluster_prof(long long *out, int n);   /* per-CTA phase clocks of the last run */
+long long mfb_cg_cluster_smem(int NP, int n_used_max, int n_own_max, int n_cut_max,
+                              int n_cm_max, int n_unit_max, int n_strip_max, int n_regions,
+                              int flags);
+int mfb_cg_cluster(int n_lambda, int C, int NP, const int *hdr, const int *tab, int n_own_max,
+                   int n_used_max, int n_cut_max, int n_cm_max, int n_unit_max,
+                   int n_strip_max, int flags, long long smem,
+                   const int *ndof, const int *region, int n_regions, const long long *h_base,
+                   const int *local_idx, int n_real, const double *hbar, const int *sides,
+                   const double *packed, int k0, int n_pts, double tol, int max_iter,
+                   double *lam, int *iters, int *status, double *g, double *xs, double *rs,
+                   double *ss, int n_clusters, int *counter, double *hist, int seg, long long seg_cap,
+                   int *seg_tab, int max_segs, int *seg_counter, void *stream);
 
 /*
  * Repack the basis pool for mfb_cg_multi: strips[4 * n_strips] = {sid, first

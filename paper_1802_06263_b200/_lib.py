@@ -69,8 +69,16 @@ _SIGS = {
     "mfb_s1_fields": ([_p, _i, _p, _p, _p, _ll, _p, _p, _p, _p, _p], _i),
     "mfb_cg_multi_scratch_doubles": ([_i, _i], _ll),
     "mfb_cg_multi": ([_i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
-                      _p, _p, _p, _p, _i, _p, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p], _i),
+                      _p, _p, _p, _p, _i, _p, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _ll,
+                      _p, _p], _i),
     "mfb_cg_pack": ([_i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p], _i),
+    "mfb_debug_cluster": ([_i], _i),
+    "mfb_debug_cluster_prof": ([_p, _i], _i),
+    "mfb_cg_cluster_max_clusters": ([_i, _i, _i, _ll], _i),
+    "mfb_cg_cluster_smem": ([_i, _i, _i, _i, _i, _i, _i, _i, _i], _ll),
+    "mfb_cg_cluster": ([_i, _i, _i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _ll, _p, _p, _i, _p, _p, _i, _p,
+                        _p, _p, _i, _i, _d, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _ll,
+                        _p, _i, _p, _p], _i),
     "mfb_group_stats": ([_i, _p, _p, _p, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p, _p, _p,
                          _p], _i),
     "mfb_group_fields": ([_i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,

@@ -57,6 +57,9 @@ struct CgMultiArgs {
     const int *pk_size;
     const int4 *sides;           // per dof {i, a_i, j, a_j} (j = -1: one side)
     double *lam, *res_hist, *g, *scratch;
+    int *seg_tab, *seg_next;       // segmented histories (seg_tab != NULL; hist_cap = segment)
+    int max_segs;
+    long long seg_cap;
     int *iters, *status, *next;
 };
 
@@ -202,7 +205,7 @@ enum { SLOT_RUN = 0, SLOT_NEW = 1, SLOT_DONE = 2 };
 
 __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     extern __shared__ double ps[];                 // [n_lambda][MP], then the dof lists
-    __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP];
+    __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP], s_seg[MP];
     __shared__ double s_rr[MP], s_gn[MP], s_a[MP], s_b[MP], s_tot[MP];
     __shared__ int s_loc[MREG * MP];
     __shared__ int s_gcnt[MREG], s_gloc[MREG * MP], s_gmask[MREG * MP];
@@ -384,8 +387,19 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
             const double rr_new = s_tot[tid];
             const double rn = sqrt(rr_new);
             const int it = s_it[tid];
-            if (it <= A.hist_cap)
+            if (A.seg_tab) {
+                const int idx = it - 1;
+                if (idx % A.hist_cap == 0) {
+                    const long long sg = atomicAdd(A.seg_next, 1);
+                    s_seg[tid] = sg < A.seg_cap ? (int)sg : -1;
+                    A.seg_tab[(long long)s_k[tid] * A.max_segs + idx / A.hist_cap] = s_seg[tid];
+                }
+                if (s_seg[tid] >= 0)
+                    A.res_hist[(long long)s_seg[tid] * A.hist_cap + idx % A.hist_cap] =
+                        rn / s_gn[tid];
+            } else if (it <= A.hist_cap) {
                 A.res_hist[(long long)s_k[tid] * A.hist_cap + it - 1] = rn / s_gn[tid];
+            }
             if (rn <= A.tol * s_gn[tid]) {
                 s_state[tid] = SLOT_DONE;
                 s_stat[tid] = MFB_CG_CONVERGED;
@@ -455,10 +469,12 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
                             int hist_cap, double *g, const int *tasks, int n_tasks,
                             const int *sides, const double *packed, const long long *pk_base,
                             const int *pk_size, int n_cta, double *scratch, int *counter,
+                            int *seg_tab, int max_segs, long long seg_cap, int *seg_counter,
                             void *stream) {
     if (n_pts <= 0) return n_pts == 0 ? MFB_OK : MFB_ERR_ARG;
     if (n_lambda <= 0 || n_sub <= 0 || n_sub >= 4095 || n_rows <= 0 || n_regions > MREG || n_cta <= 0 ||
-        max_iter < 1 || hist_cap < 1 || n_tasks <= 0)
+        max_iter < 1 || hist_cap < 1 || n_tasks <= 0 ||
+        (seg_tab && (max_segs < (max_iter + hist_cap - 1) / hist_cap || !seg_counter)))
         return MFB_ERR_ARG;
     const size_t smem = (size_t)n_lambda * MP * sizeof(double) + (size_t)n_rows * sizeof(int);
     if (smem > 220 * 1024) return MFB_ERR_SMEM;
@@ -479,6 +495,9 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
     A.packed = packed; A.pk_base = pk_base; A.pk_size = pk_size;
     A.lam = lam; A.res_hist = res_hist; A.g = g; A.scratch = scratch;
     A.iters = iters; A.status = status; A.next = counter;
+    A.seg_tab = seg_tab; A.seg_next = seg_counter; A.max_segs = max_segs; A.seg_cap = seg_cap;
+    if (seg_tab && cudaMemsetAsync(seg_counter, 0, sizeof(int), st) != cudaSuccess)
+        return MFB_ERR_LAUNCH;
     cg_multi_kernel<<<n_cta, MNT, smem, st>>>(A);
     MFB_CHECK_LAUNCH();
     return MFB_OK;

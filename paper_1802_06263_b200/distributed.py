@@ -122,7 +122,8 @@ class DeviceShardEngine:
 
     def solve(self, k0, n, tol, max_iter):
         lam, iters, status, hist, _ = self.eng.solve_points(tol, max_iter, k0=k0, n_pts=n)
-        return lam, iters, status, hist
+        from .interface import hist_padded
+        return lam, iters, status, hist_padded(hist, iters)
 
     def moments(self, lam_all, sids, with_lambda):
         return self.eng.moments(lam_all, sids=sids, with_lambda=with_lambda)

@@ -33,7 +33,7 @@ import numpy as np
 
 from . import _lib
 from .adapter import mode_table
-from .errors import ConvergenceError, SingularOperatorError, SizeCapError
+from .errors import ConvergenceError, NativeLibraryError, SingularOperatorError, SizeCapError
 from .plan import DevicePlan, _dev, _ptr
 
 log = logging.getLogger(__name__)
@@ -45,6 +45,8 @@ N_SMS = 148                 # B200
 BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 S1_FIELD_BYTES_MAX = 32 << 30   # S1 keeps every realization's fields for the moments
 S1_CHUNK_REALIZATIONS = None    # S1 realizations per chunk (None: as many as fit)
+CLUSTER_SHAPES = ((4, 16), (8, 16), (2, 8), (4, 8))   # (CTAs per cluster, points) to try
+HIST_SEG = 1024             # residual-history segment (cluster CG)
 
 
 @dataclass
@@ -120,7 +122,23 @@ class ResidualHistories(Sequence):
         h._flat = None
         return h
 
-    def __getattr__(self, name):          # lazy flat/offsets of a padded store
+    @classmethod
+    def from_segments(cls, pool, seg_tab, iters, seg):
+        """Histories in the segment pool the cluster CG wrote: point k's
+        entry i at pool[seg_tab[k, i // seg] * seg + i % seg]."""
+        h = cls.__new__(cls)
+        h.iters = np.asarray(iters, dtype=np.int64)
+        h._padded = None
+        h._seg = (pool, seg_tab, int(seg))
+        return h
+
+    def __getattr__(self, name):          # lazy flat/offsets of a padded or segmented store
+        if name in ("flat", "offsets") and self.__dict__.get("_seg") is not None:
+            it = self.iters
+            self.offsets = np.concatenate([[0], np.cumsum(it)])
+            self.flat = (np.concatenate([self.array(k) for k in range(len(it))])
+                         if len(it) else np.zeros(0))
+            return self.__dict__[name]
         if name in ("flat", "offsets") and self.__dict__.get("_padded") is not None:
             it = self.iters
             mask = np.arange(self._padded.shape[1])[None, :] < it[:, None]
@@ -142,7 +160,67 @@ class ResidualHistories(Sequence):
         """Point k's history as a numpy view (no copy)."""
         if self.__dict__.get("_padded") is not None:
             return self._padded[k, :self.iters[k]]
+        if self.__dict__.get("_seg") is not None:
+            pool, tab, seg = self._seg
+            n = int(self.iters[k])
+            ids = tab[k, :(n + seg - 1) // seg].astype(np.int64)
+            if len(ids) == 1:
+                return pool[ids[0] * seg:ids[0] * seg + n]
+            return (pool.reshape(-1, seg)[ids].reshape(-1)[:n] if len(ids)
+                    else pool[:0])
         return self.flat[self.offsets[k]:self.offsets[k + 1]]
+
+
+class SegmentedHist:
+    """Residual histories of the cluster CG, still on the device: a pool of
+    `seg`-entry segments and per point the table of its segments
+    (mfb_cg_cluster). `counter` = segments the sweep asked for; when it
+    exceeds `cap` some were not stored and the solve must be rerun with
+    cap = needed() (the results are deterministic, only histories differ)."""
+
+    def __init__(self, pool, seg_tab, seg, counter, cap):
+        self.pool, self.seg_tab, self.seg, self.counter, self.cap = pool, seg_tab, seg, counter, cap
+
+    def needed(self):
+        return int(self.counter.item())
+
+    def complete(self):
+        return self.needed() <= self.cap
+
+    def to_host(self, iters, n_seg=None):
+        """ResidualHistories over host copies of the used segments."""
+        n_seg = min(self.needed() if n_seg is None else n_seg, self.cap)
+        pool = self.pool[:n_seg * self.seg].cpu().numpy()
+        return ResidualHistories.from_segments(pool, self.seg_tab.cpu().numpy(), iters, self.seg)
+
+    def padded(self, iters, width=None):
+        """Device [n_pts, width] tensor of the histories (zeros past each
+        point's iterations): the padded layout of the small-interface kernels."""
+        import torch
+        it = torch.as_tensor(iters, device=self.pool.device).to(torch.int64)
+        width = int(it.max().item()) if width is None and it.numel() else int(width or 0)
+        width = max(width, 1)
+        i = torch.arange(width, device=self.pool.device)
+        seg_i = torch.clamp(i // self.seg, max=self.seg_tab.shape[1] - 1)
+        sid = self.seg_tab[:, seg_i].to(torch.int64)            # [n_pts, width]
+        valid = (i[None, :] < it[:, None]) & (sid >= 0)
+        idx = torch.where(valid, sid * self.seg + (i % self.seg)[None, :], 0)
+        out = self.pool[idx.clamp(max=max(self.pool.numel() - 1, 0))] if self.pool.numel() \
+            else torch.zeros(idx.shape, dtype=torch.float64, device=self.pool.device)
+        return torch.where(valid, out, torch.zeros((), dtype=out.dtype, device=out.device))
+
+    def row(self, k, n):
+        """Point k's first n entries (host list)."""
+        nseg = (int(n) + self.seg - 1) // self.seg
+        ids = self.seg_tab[k, :nseg].cpu().numpy()
+        out = [self.pool[int(i) * self.seg:(int(i) + 1) * self.seg].cpu().numpy() for i in ids]
+        return (np.concatenate(out)[:int(n)] if out else np.zeros(0)).tolist()
+
+
+def hist_padded(hist, iters):
+    """[n_pts, width] device tensor of residual histories from either history
+    form a CG launch returns (padded tensor or SegmentedHist)."""
+    return hist.padded(iters) if isinstance(hist, SegmentedHist) else hist
 
 
 def _pack_histories(hist, iters):
@@ -768,12 +846,16 @@ class SweepEngine:
 
     # ---------------------------------------------------------- (3) CG ----
     def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False,
-                     kernel="auto"):
+                     kernel="auto", cluster_shape=None, hist_segments=None, check_hist=False):
         """CG over points k0..k0+n_pts-1. kernel: "auto" (multi-point when the
         blocks exceed shared memory and the points fill the GPU, else one CTA
         per point with register-resident block rows when they fit), "cta"
         (one CTA per point), "staged" (one CTA per point, blocks staged in
-        shared memory) or "multi" (forced, for tests)."""
+        shared memory), "multi" (8 points per CTA, forced, for tests) or
+        "cluster" (NP points per thread-block cluster, forced; the "auto"
+        choice is "multi" for large interfaces). The multi and cluster kernels
+        return their residual histories as a SegmentedHist, the others as
+        [n_pts, hist_cap]."""
         torch, plan, st = self.torch, self.plan, self.st
         n_real = plan.grid.n_real
         n_pts = n_real - k0 if n_pts is None else n_pts
@@ -782,32 +864,70 @@ class SweepEngine:
         lam = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda")
         iters = torch.empty(n_pts, dtype=torch.int32, device="cuda")
         status = torch.empty(n_pts, dtype=torch.int32, device="cuda")
-        hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=torch.float64, device="cuda")
         g = torch.empty((n_pts, nl), dtype=torch.float64, device="cuda") if keep_g else None
         self.launches += 1
         if self.timing:
             e0 = self._ev()
-        mt = None if kernel in ("cta", "staged") else self._multi_tables(n_pts,
-                                                                      force=kernel == "multi")
-        if mt is not None:
-            self.cg_kernel_name = "cg_multi_kernel (8 points per CTA on FP64 mma.m8n8k4)"
-            self.launches += 1
-            _lib.check(self.L.mfb_cg_pack(
-                mt["n_strips"], _ptr(mt["strips"]), _ptr(plan.d_ndof), _ptr(mt["n_loc"]),
-                mt["max_loc"], _ptr(st.d_blk), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
-                _ptr(st.blocks), _ptr(mt["packed"]), self.sp), "mfb_cg_pack")
-            _lib.check(self.L.mfb_cg_multi(
-                nl, plan.n_sub, int(plan.dof_ptr[-1]), _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
-                _ptr(st.d_cg_region), int(st.d_cg_local.shape[0]), _ptr(st.d_blk), _ptr(st.d_h),
-                _ptr(st.d_cg_local), n_real, _ptr(st.blocks), _ptr(st.hbar), k0, n_pts,
-                float(tol), int(max_iter), _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist),
-                max(hist_cap, 1), _ptr(g) if keep_g else None, _ptr(mt["tasks"]), mt["n_tasks"],
-                _ptr(mt["sides"]), _ptr(mt["packed"]), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
-                mt["n_cta"], _ptr(mt["scratch"]),
-                _ptr(mt["counter"]), self.sp), "mfb_cg_multi")
+        ct = None
+        if kernel == "cluster":
+            ct = self._cluster_tables(n_pts, force=True, shape=cluster_shape)
+            if ct is None:
+                raise NativeLibraryError("no cluster shape fits this interface")
+        mt = None
+        if ct is None and kernel not in ("cta", "staged"):
+            mt = self._multi_tables(n_pts, force=kernel == "multi")
+        if ct is not None or mt is not None:
+            # the large-interface kernels keep residual histories in segments
+            # (device memory ~ the iterations run, not n_pts x max_iter)
+            mt = self._pack_tables() if mt is None else mt
+            self._repack(mt)
+            seg = HIST_SEG
+            max_segs = (int(max_iter) + seg - 1) // seg
+            cap = hist_segments
+            if cap is None:
+                free = torch.cuda.mem_get_info()[0]
+                cap = int(min(n_pts * max_segs, max(free // 8, 1 << 28) // (8 * seg)))
+            counter = ct["seg_counter"] if ct is not None else mt["seg_counter"]
+            while True:
+                pool = torch.empty(int(cap) * seg, dtype=torch.float64, device="cuda")
+                seg_tab = torch.empty((n_pts, max_segs), dtype=torch.int32, device="cuda")
+                self.launches += 1
+                if ct is not None:
+                    C, NP = ct["C"], ct["NP"]
+                    self.cg_kernel_name = (f"cg_cluster_kernel<{NP}> ({NP} points per cluster "
+                                           f"of {C} CTAs, FP64 mma.m8n8k4, vectors on chip)")
+                    _lib.check(self.L.mfb_cg_cluster(
+                        nl, C, NP, _ptr(ct["d_hdr"]), _ptr(ct["d_tab"]), ct["n_own_max"],
+                        ct["n_used_max"], ct["n_cut_max"], ct["n_cm_max"], ct["n_unit_max"],
+                        ct["n_strip_max"], ct["flags"], ct["smem"], _ptr(plan.d_ndof),
+                        _ptr(st.d_cg_region), int(st.d_cg_local.shape[0]), _ptr(st.d_h),
+                        _ptr(st.d_cg_local), n_real, _ptr(st.hbar), _ptr(mt["sides"]),
+                        _ptr(mt["packed"]), k0, n_pts, float(tol), int(max_iter), _ptr(lam),
+                        _ptr(iters), _ptr(status), _ptr(g) if keep_g else None, _ptr(ct["xs"]),
+                        _ptr(ct["rs"]), _ptr(ct["ss"]), ct["n_clusters"], _ptr(mt["counter"]),
+                        _ptr(pool), seg, int(cap), _ptr(seg_tab), max_segs, _ptr(counter),
+                        self.sp), "mfb_cg_cluster")
+                else:
+                    self.cg_kernel_name = "cg_multi_kernel (8 points per CTA on FP64 mma.m8n8k4)"
+                    _lib.check(self.L.mfb_cg_multi(
+                        nl, plan.n_sub, int(plan.dof_ptr[-1]), _ptr(plan.d_ndof),
+                        _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map), _ptr(st.d_cg_region),
+                        int(st.d_cg_local.shape[0]), _ptr(st.d_blk), _ptr(st.d_h),
+                        _ptr(st.d_cg_local), n_real, _ptr(st.blocks), _ptr(st.hbar), k0, n_pts,
+                        float(tol), int(max_iter), _ptr(lam), _ptr(iters), _ptr(status),
+                        _ptr(pool), seg, _ptr(g) if keep_g else None, _ptr(mt["tasks"]),
+                        mt["n_tasks"], _ptr(mt["sides"]), _ptr(mt["packed"]),
+                        _ptr(mt["pk_base"]), _ptr(mt["pk_size"]), mt["n_cta"],
+                        _ptr(mt["scratch"]), _ptr(mt["counter"]), _ptr(seg_tab), max_segs,
+                        int(cap), _ptr(counter), self.sp), "mfb_cg_multi")
+                hist = SegmentedHist(pool, seg_tab, seg, counter, cap)
+                if not check_hist or hist.complete():   # complete() syncs the stream
+                    break
+                cap = hist.needed()          # rerun once with the exact pool size
             if self.timing:
                 self.cg_events.append((e0, self._ev(), n_pts))
             return lam, iters, status, hist, g
+        hist = torch.empty((n_pts, max(hist_cap, 1)), dtype=torch.float64, device="cuda")
         # block rows in registers when every ndof is a multiple of 4 (the
         # accumulation order then equals the staged kernel's)
         reg_ndof = int(plan.ndof.max()) if (kernel != "staged" and len(plan.ndof)
@@ -827,39 +947,115 @@ class SweepEngine:
             self.cg_events.append((e0, self._ev(), n_pts))
         return lam, iters, status, hist, g
 
-    def _multi_tables(self, n_pts, force=False):
-        """Work tables of the multi-point CG (mfb_cg_multi), or None when the
-        one-CTA-per-point kernel is the right one: the point's blocks fit in
-        shared memory (staged once per point), there are too few points to
-        keep 8 per SM in flight, or the dof runs are not 16-byte aligned."""
+    def _pack_tables(self):
+        """Task / strip tables of the multi-point CG kernels and the packed
+        basis pool (cached on the static state; the pool is repacked by
+        mfb_cg_pack on every solve, after the bases)."""
         torch, st, plan = self.torch, self.st, self.plan
-        nd = plan.ndof.astype(np.int64)
-        nl, n_rows = int(plan.n_lambda), int(plan.dof_ptr[-1])
-        staged = 8 * (int(np.sum(nd * nd)) + 6 * nl + 2 * n_rows) <= 200 * 1024
-        if (8 * 8 * nl + 4 * n_rows > 220 * 1024 or int(st.d_cg_local.shape[0]) > 64
-                or plan.n_sub >= 4095):
-            return None
-        if not force and (staged or n_pts < 4 * N_SMS):
-            return None
         mt = getattr(st, "_multi", None)
         if mt is None:
+            nd = plan.ndof.astype(np.int64)
+            nl = int(plan.n_lambda)
             tab, sides, strips, pk_size = cg_tasks(plan.n_sub, nd, plan.dof_ptr, plan.dof_map,
                                                    nl)
             n_loc = st.n_loc.astype(np.int64)
             pk_base = np.concatenate([[0], np.cumsum(pk_size.astype(np.int64) * n_loc)])
-            n_cta = N_SMS
-            scratch = int(self.L.mfb_cg_multi_scratch_doubles(nl, n_cta))
             mt = {"tasks": _dev(tab.ravel(), torch.int32), "n_tasks": int(len(tab)),
-                  "sides": _dev(sides.ravel(), torch.int32), "n_cta": n_cta,
+                  "sides": _dev(sides.ravel(), torch.int32),
                   "strips": _dev(strips.ravel(), torch.int32), "n_strips": int(len(strips)),
                   "pk_size": _dev(pk_size, torch.int32), "pk_base": _dev(pk_base[:-1], torch.int64),
                   "n_loc": _dev(n_loc.astype(np.int32), torch.int32),
                   "max_loc": int(n_loc.max()),
                   "packed": torch.empty(int(pk_base[-1]), dtype=torch.float64, device="cuda"),
-                  "scratch": torch.empty(scratch, dtype=torch.float64, device="cuda"),
-                  "counter": torch.zeros(1, dtype=torch.int32, device="cuda")}
+                  "counter": torch.zeros(1, dtype=torch.int32, device="cuda"),
+                  "seg_counter": torch.zeros(1, dtype=torch.int32, device="cuda"),
+                  "host": {"tasks": tab, "sides": sides, "strips": strips, "pk_size": pk_size,
+                           "pk_base": pk_base[:-1]}}
             st._multi = mt
         return mt
+
+    def _repack(self, mt):
+        plan, st = self.plan, self.st
+        self.launches += 1
+        _lib.check(self.L.mfb_cg_pack(
+            mt["n_strips"], _ptr(mt["strips"]), _ptr(plan.d_ndof), _ptr(mt["n_loc"]),
+            mt["max_loc"], _ptr(st.d_blk), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
+            _ptr(st.blocks), _ptr(mt["packed"]), self.sp), "mfb_cg_pack")
+
+    def _multi_wanted(self, n_pts, force=False):
+        """True when the blocks exceed shared memory and enough points fill
+        the GPU for a multi-point kernel (or it is forced)."""
+        st, plan = self.st, self.plan
+        nd = plan.ndof.astype(np.int64)
+        nl, n_rows = int(plan.n_lambda), int(plan.dof_ptr[-1])
+        if int(st.d_cg_local.shape[0]) > 64 or plan.n_sub >= 4095:
+            return False
+        if force:
+            return True
+        staged = 8 * (int(np.sum(nd * nd)) + 6 * nl + 2 * n_rows) <= 200 * 1024
+        return not staged and n_pts >= 4 * N_SMS
+
+    def _multi_tables(self, n_pts, force=False):
+        """Work tables of the 8-points-per-CTA CG (mfb_cg_multi), or None when
+        its shared-memory vectors do not fit or the kernel is not wanted."""
+        plan, torch = self.plan, self.torch
+        nl, n_rows = int(plan.n_lambda), int(plan.dof_ptr[-1])
+        if 8 * 8 * nl + 4 * n_rows > 220 * 1024 or not self._multi_wanted(n_pts, force):
+            return None
+        mt = self._pack_tables()
+        if "scratch" not in mt:
+            mt["n_cta"] = N_SMS
+            n = int(self.L.mfb_cg_multi_scratch_doubles(nl, N_SMS))
+            mt["scratch"] = torch.empty(n, dtype=torch.float64, device="cuda")
+        return mt
+
+    def _cluster_tables(self, n_pts, force=False, shape=None):
+        """Tables of the cluster CG (mfb_cg_cluster, cgcluster.py) for the
+        first (C, NP) of `shape` (default CLUSTER_SHAPES) whose on-chip
+        vectors fit, or None."""
+        from . import cgcluster
+        torch, st, plan = self.torch, self.st, self.plan
+        if not self._multi_wanted(n_pts, force):
+            return None
+        mt = self._pack_tables()
+        cache = st.__dict__.setdefault("_cluster", {})
+        for C, NP in (shape or CLUSTER_SHAPES):
+            if (C, NP) in cache:
+                if cache[(C, NP)] is not None:
+                    return cache[(C, NP)]
+                continue
+            h = mt["host"]
+            lay = plan.problem.layout
+            centers = np.array([[(b.rect[0] + b.rect[2]) / 2, (b.rect[1] + b.rect[3]) / 2]
+                                for b in lay.blocks])
+            ct = cgcluster.cluster_tables(plan.n_sub, plan.ndof, plan.dof_ptr, plan.dof_map,
+                                          plan.n_lambda, plan.region, centers, C, NP,
+                                          h["tasks"], h["sides"], h["pk_base"], h["pk_size"])
+            ncl, nr = -1, int(st.d_cg_local.shape[0])
+            for flags in (3, 1, 0, 7, 5, 4):   # bit 0 / 1: r / x on chip, bit 2: S p in global
+                smem = int(self.L.mfb_cg_cluster_smem(NP, ct["n_used_max"], ct["n_own_max"],
+                                                      ct["n_cut_max"], ct["n_cm_max"],
+                                                      ct["n_unit_max"], ct["n_strip_max"], nr,
+                                                      flags))
+                if smem > 220 * 1024:
+                    continue
+                ncl = int(self.L.mfb_cg_cluster_max_clusters(C, NP, ct["n_own_max"], smem))
+                if ncl > 0:
+                    break
+            if ncl <= 0:
+                cache[(C, NP)] = None
+                continue
+            nv = ncl * C * ct["n_own_max"] * NP
+            ct.update(n_clusters=ncl, flags=flags, smem=smem,
+                      d_hdr=_dev(ct["hdr"].ravel(), torch.int32),
+                      d_tab=_dev(ct["tab"], torch.int32),
+                      xs=None if flags & 2 else torch.empty(nv, dtype=torch.float64, device="cuda"),
+                      rs=None if flags & 1 else torch.empty(nv, dtype=torch.float64, device="cuda"),
+                      ss=None if not flags & 4 else torch.empty(nv, dtype=torch.float64, device="cuda"),
+                      seg_counter=torch.zeros(1, dtype=torch.int32, device="cuda"))
+            cache[(C, NP)] = ct
+            return ct
+        return None
 
     # ------------------------------------------------ (3') S1 CG ------------
     def _s1_tables(self):
@@ -1206,7 +1402,8 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     ev[3].record(eng.stream)
     # every result travels back in pinned buffers queued behind the moments:
     # one wait, then host-side assembly only
-    small_hist = hist.numel() * 8 <= (256 << 20)
+    seg_hist = isinstance(hist, SegmentedHist)
+    small_hist = (not seg_hist) and hist.numel() * 8 <= (256 << 20)
     with torch.cuda.stream(eng.stream):
         h_st = torch.empty(status.shape, dtype=status.dtype, pin_memory=True)
         h_it = torch.empty(iters.shape, dtype=iters.dtype, pin_memory=True)
@@ -1217,14 +1414,24 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
         if small_hist:
             h_hist = torch.empty(hist.shape, dtype=hist.dtype, pin_memory=True)
             h_hist.copy_(hist, non_blocking=True)
+        if seg_hist:
+            h_cnt = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            h_cnt.copy_(hist.counter, non_blocking=True)
     eng.check_info()                # syncs the stream: the copies above are done
     st = h_st.numpy()
     it = h_it.numpy()
+    if seg_hist and int(h_cnt[0]) > hist.cap:
+        # the history pool overflowed (results are complete): rerun the
+        # deterministic CG once with the exact pool for the histories
+        _, _, _, hist, _ = eng.solve_points(tol, max_iter, hist_segments=int(h_cnt[0]))
     fail = np.nonzero((st == 1) | (st == 2))[0]
     if len(fail):
         k = int(fail[0])
-        res = (h_hist[k] if small_hist else hist[k].cpu()).numpy()[
-            :min(int(it[k]), hist.shape[1])].tolist()
+        if seg_hist:
+            res = hist.row(k, int(it[k]))
+        else:
+            res = (h_hist[k] if small_hist else hist[k].cpu()).numpy()[
+                :min(int(it[k]), hist.shape[1])].tolist()
         if st[k] == 1:
             raise ConvergenceError(f"interface operator is not positive definite "
                                    f"(p.Sp <= 0 at iteration {int(it[k])}, point {k})",
@@ -1237,7 +1444,9 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     timings["moments"] = ev[2].elapsed_time(ev[3]) / 1e3
     lam_h = h_lam.numpy()
     lambdas = list(lam_h)
-    if small_hist:
+    if seg_hist:
+        residuals = hist.to_host(it.astype(np.int64))
+    elif small_hist:
         it_c = np.minimum(it.astype(np.int64), hist.shape[1])
         residuals = ResidualHistories.from_padded(h_hist.numpy(), it_c)
     else:

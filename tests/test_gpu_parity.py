@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from conftest import case_from_golden, golden
+from paper_1802_06263_b200.interface import hist_padded
 
 pytestmark = pytest.mark.gpu
 
@@ -136,7 +137,7 @@ def test_rhs_and_cg_against_oracle_inputs(gpu, name):
     g = g.cpu().numpy()
     assert np.max(np.abs(g - z["s3_g"])) <= 1e-10 * np.max(np.abs(z["s3_g"]))
     assert np.all(status.cpu().numpy() == 0)
-    hist = hist.cpu().numpy()
+    hist = hist_padded(hist, iters).cpu().numpy()
     it = iters.cpu().numpy()
     for k in range(grid.n_real):
         assert hist[k, it[k] - 1] <= TOL
@@ -210,7 +211,7 @@ def test_multi_point_cg_matches_reference(gpu, name):
         gg = g.cpu().numpy()[keep]
         assert np.max(np.abs(gg - z["s3_g"])) <= 1e-10 * np.max(np.abs(z["s3_g"]))
     it = iters.cpu().numpy()
-    h = hist.cpu().numpy()
+    h = hist_padded(hist, iters).cpu().numpy()
     assert all(h[k, it[k] - 1] <= TOL for k in range(grid.n_real))
     assert abs(it.mean() - z["s3_iters"].mean()) <= 0.05 * z["s3_iters"].mean() + 2
     # the point's arithmetic does not depend on its slot / CTA / neighbours:
@@ -242,12 +243,12 @@ def test_cfg4_points_match_reference(gpu, kernel):
     eng.check_info()
     max_iter = max(50, 10 * plan.n_lambda)
     for j, k in enumerate(z["points"]):
-        lam, it, st, hist, g = eng.solve_points(TOL, max_iter, k0=int(k), n_pts=1,
+        lam, it_t, st, hist, g = eng.solve_points(TOL, max_iter, k0=int(k), n_pts=1,
                                                 keep_g=True, kernel=kernel)
         gg = g.cpu().numpy()[0]
         assert np.max(np.abs(gg - z["g"][j])) <= 1e-10 * np.max(np.abs(z["g"][j]))
-        st, it = int(st.cpu()[0]), int(it.cpu()[0])
-        h = hist.cpu().numpy()[0]
+        st, it = int(st.cpu()[0]), int(it_t.cpu()[0])
+        h = hist_padded(hist, it_t).cpu().numpy()[0]
         # unpreconditioned CG at this conditioning amplifies roundoff: the
         # histories agree closely only over the first iterations
         head = z["res_head"][j]
@@ -260,3 +261,33 @@ def test_cfg4_points_match_reference(gpu, kernel):
             assert abs(it - int(z["iters"][j])) <= 0.1 * int(z["iters"][j])
         else:
             assert st == 2 and it == max_iter       # MFB_CG_MAX_ITER, like the reference
+
+
+@pytest.mark.parametrize("name", ["cfg1", "case1_mini", "cfg2"])
+@pytest.mark.parametrize("shape", [(2, 8), (4, 16)])
+def test_cluster_cg_matches_reference(gpu, name, shape):
+    """The thread-block-cluster CG (mfb_cg_cluster, cgcluster.py: C CTAs share
+    NP points, vectors of owned dofs on chip, dot products all-gathered over
+    DSMEM) forced on the configs with reference goldens: lambda within 1e-8,
+    g equal to the recorded rhs, every history ends at tol, and a point solved
+    alone gives the same bits as inside a full cluster."""
+    z = golden(name)
+    _, problem, grid, _ = case_from_golden(name)
+    plan, eng = _engine(problem, grid)
+    max_iter = max(50, 10 * plan.n_lambda)
+    lam, iters, status, hist, g = eng.solve_points(TOL, max_iter, keep_g=True, kernel="cluster",
+                                                  cluster_shape=[shape])
+    assert np.all(status.cpu().numpy() == 0)
+    L = lam.cpu().numpy()
+    keep = z["s3_points"]
+    assert _rel(L[keep], z["s3_lambda"]) <= 1e-8
+    gg = g.cpu().numpy()[keep]
+    assert np.max(np.abs(gg - z["s3_g"])) <= 1e-10 * np.max(np.abs(z["s3_g"]))
+    it = iters.cpu().numpy()
+    H = hist.to_host(it)
+    assert all(H.array(k)[-1] <= TOL and len(H[k]) == it[k] for k in range(grid.n_real))
+    assert abs(it.mean() - z["s3_iters"].mean()) <= 0.05 * z["s3_iters"].mean() + 2
+    k = int(grid.n_real // 2)
+    lam1, it1, _, _, _ = eng.solve_points(TOL, max_iter, k0=k, n_pts=1, kernel="cluster",
+                                          cluster_shape=[shape])
+    assert np.array_equal(lam1.cpu().numpy()[0], L[k]) and int(it1.cpu()[0]) == int(it[k])

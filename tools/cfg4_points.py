@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1802_06263_b200.adapter import load_config  # noqa: E402
-from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
+from paper_1802_06263_b200.interface import SweepEngine, get_plan, hist_padded  # noqa: E402
 
 GOLD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
                     "golden", "cfg4_points.npz")
@@ -45,7 +45,7 @@ def main():
             dt = time.time() - t
             lam = lam.cpu().numpy()[0]
             it, st = int(iters.cpu().numpy()[0]), int(status.cpu().numpy()[0])
-            h = hist.cpu().numpy()[0]
+            h = hist_padded(hist, iters).cpu().numpy()[0]
             msg = f"[{kern}] point {k}: {it} iterations, status {st}, {1e3 * dt:.0f} ms"
             if z is not None and k in list(z["points"]):
                 j = list(z["points"]).index(k)
