@@ -40,6 +40,7 @@ log = logging.getLogger(__name__)
 
 METHODS = ("S1", "S2", "S3")
 _PLAN_CACHE = {}
+PLAN_CACHE_SIZE = 8         # device plans kept (least recently used evicted)
 WORK_BUDGET_BYTES = 16 << 30
 N_SMS = 148                 # B200
 BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
@@ -338,11 +339,12 @@ def _plan_fingerprint(problem, grid):
 
 def get_plan(problem, grid):
     key = _plan_fingerprint(problem, grid)
-    plan = _PLAN_CACHE.get(key)
+    plan = _PLAN_CACHE.pop(key, None)
     if plan is None or plan.problem is not problem or plan.grid is not grid:
         plan = DevicePlan(problem, grid)
-        _PLAN_CACHE.clear()
-        _PLAN_CACHE[key] = plan
+    _PLAN_CACHE[key] = plan                 # most recently used last
+    while len(_PLAN_CACHE) > PLAN_CACHE_SIZE:
+        _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
     return plan
 
 
@@ -1442,6 +1444,8 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     timings["bases"] = ev[0].elapsed_time(ev[1]) / 1e3
     timings["cg"] = ev[1].elapsed_time(ev[2]) / 1e3
     timings["moments"] = ev[2].elapsed_time(ev[3]) / 1e3
+    timings["device"] = ev[0].elapsed_time(ev[3]) / 1e3
+    timings["launches"] = eng.launches
     lam_h = h_lam.numpy()
     lambdas = list(lam_h)
     if seg_hist:
