@@ -29,6 +29,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 import numpy as np  # noqa: E402
 
@@ -340,7 +341,7 @@ def _ncu_cg_traffic():
             unit = str(m["dram__bytes_read.sum"]).split()[1]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
             pit = float(m.get("point_iterations", 1184 * 100))
-            return (rd + wr) * scale / pit, path
+            return (rd + wr) * scale / pit, os.path.relpath(path, ROOT)
     return None, None
 
 
@@ -416,10 +417,13 @@ def run_ours(a):
         torch.cuda.set_device(0)
     from paper_1802_06263_b200 import _build
     from paper_1802_06263_b200.adapter import load_config
+    from paper_1802_06263_b200 import interface
     from paper_1802_06263_b200.interface import _PLAN_CACHE, get_plan, run_method
     _build.build()
+    interface.SHARE_SCRATCH = True          # the batch plans share one set of sweep buffers
     cfg_path = _config_path(a.config)
-    problem, grid, _ = load_config(cfg_path)
+    problem, grid, opts = load_config(cfg_path)
+    max_iter = opts.get("max_iter")         # cfg4: 200,000 (configs/cfg4.json cg.max_iter)
     nl = problem.space.n_dof
     B = a.batches if a.batches else (4 if a.config == "cfg4" else 1)
     batches = _batch_grids(grid, B)
@@ -435,7 +439,7 @@ def run_ours(a):
         if ws > 1:
             torch.distributed.barrier()
         t = time.perf_counter()
-        res = run_method(problem, g, method="S3", tol=a.tol)
+        res = run_method(problem, g, method="S3", tol=a.tol, max_iter=max_iter)
         torch.cuda.synchronize()
         return g.n_real, time.perf_counter() - t, res
 
@@ -526,7 +530,8 @@ def run_ours(a):
                                 f"KL, every basis, CG, moments)") if B > 1 else
                                "one run_method S3 sweep over the whole grid",
                        "batches": B, "points_per_step": n_tot / len(rows),
-                       "tol": a.tol, "max_iter": int(max(50, 10 * nl)),
+                       "tol": a.tol,
+                       "max_iter": int(max_iter) if max_iter else int(max(50, 10 * nl)),
                        "parallelism": (f"x{ws} GPUs: each rank sweeps its own batch, no "
                                        f"collective") if ws > 1 else "single",
                        "l2": "flushed (256 MB write) before every step; the step's working "

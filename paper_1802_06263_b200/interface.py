@@ -41,6 +41,47 @@ log = logging.getLogger(__name__)
 METHODS = ("S1", "S2", "S3")
 _PLAN_CACHE = {}
 PLAN_CACHE_SIZE = 8         # device plans kept (least recently used evicted)
+# Sweep states of different plans may share their large device buffers (the
+# basis pool, field responses, factor work, K): sweeps that go through
+# run_method rebuild them in every call, so plans of the same problem on
+# different grids (e.g. batches of one collocation grid) then cost one set of
+# buffers instead of one each. Off by default: a caller holding two engines'
+# results at once must keep them separate. A sweep that would read a buffer
+# another state has since overwritten raises NativeLibraryError instead.
+SHARE_SCRATCH = False
+_SHARED = {}
+_OWNER = {}
+
+
+def _scratch(name, numel, dtype):
+    """Device buffer for a sweep state: its own, or with SHARE_SCRATCH a view
+    of one buffer per (name, dtype) shared by every state."""
+    import torch
+    numel = int(numel)
+    if not SHARE_SCRATCH:
+        return torch.empty(numel, dtype=dtype, device="cuda")
+    t = _SHARED.get((name, dtype))
+    if t is None or t.numel() < numel:
+        _SHARED.pop((name, dtype), None)
+        t = torch.empty(numel, dtype=dtype, device="cuda")
+        _SHARED[(name, dtype)] = t
+    return t[:numel]
+
+
+def _claim(st, *names):
+    """st's results now live in the shared buffers `names`."""
+    if SHARE_SCRATCH:
+        for n in names:
+            _OWNER[n] = st
+
+
+def _check_owner(st, *names):
+    if SHARE_SCRATCH:
+        for n in names:
+            if _OWNER.get(n, st) is not st:
+                raise NativeLibraryError(
+                    f"shared sweep buffer '{n}' holds another sweep's results "
+                    f"(SHARE_SCRATCH): rebuild this engine's bases first")
 WORK_BUDGET_BYTES = 16 << 30
 N_SMS = 148                 # B200
 BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
@@ -405,7 +446,7 @@ class _SweepStatic:
                     koff[idx] = cur
                     cur += pb.meshes[s].n_cells
         self.koff, self.sys_first = koff, first
-        self.K = torch.empty(max(cur, 1), dtype=f64, device="cuda")
+        self.K = _scratch("K", max(cur, 1), f64)
         # The sweep's inputs (local-index table, weights, KL tables) live in
         # one device staging buffer (refresh_inputs: one pinned H2D copy);
         # the KL tables are views into it.
@@ -461,10 +502,10 @@ class _SweepStatic:
         moff = np.concatenate([[0], np.cumsum(nf * nd)])
         fboff = np.concatenate([[0], np.cumsum(nf)])
         self.keep_fields = keep_fields
-        self.blocks = torch.empty(int(boff[-1]), dtype=f64, device="cuda")
-        self.hbar = torch.empty(int(hoff[-1]), dtype=f64, device="cuda")
-        self.M = torch.empty(int(moff[-1]) if keep_fields else 0, dtype=f64, device="cuda")
-        self.Fb = torch.empty(int(fboff[-1]) if keep_fields else 0, dtype=f64, device="cuda")
+        self.blocks = _scratch("blocks", int(boff[-1]), f64)
+        self.hbar = _scratch("hbar", int(hoff[-1]), f64)
+        self.M = _scratch("M", int(moff[-1]) if keep_fields else 0, f64)
+        self.Fb = _scratch("Fb", int(fboff[-1]) if keep_fields else 0, f64)
         self.sys_boff, self.sys_hoff = boff[:-1], hoff[:-1]
         self.sys_moff, self.sys_fboff = moff[:-1], fboff[:-1]
         self.d_pat = _dev(sys_pat, i32)
@@ -547,12 +588,12 @@ class _SweepStatic:
                          survey_flops=sum(pats[systems[i][0]].algorithmic_flops for i in grp))
                 self.hwaves.append(w)
                 lmax, hxmax = max(lmax, int(loff[-1])), max(hxmax, int(hxoff[-1]))
-        self.work = torch.empty(max(wmax, 1), dtype=f64, device="cuda")
+        self.work = _scratch("work", max(wmax, 1), f64)
         # per system: group-barrier counter and panel-ready counter (mfb_band.cu)
         self.bar = torch.zeros(2 * max(len(systems), 1), dtype=torch.int32, device="cuda")
-        self.X = torch.empty(max(xmax, 1), dtype=f64, device="cuda")
-        self.Lstore = torch.empty(max(lmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
-        self.HX = torch.empty(max(hxmax, 1) if keep_fields else 1, dtype=f64, device="cuda")
+        self.X = _scratch("X", max(xmax, 1), f64)
+        self.Lstore = _scratch("Lstore", max(lmax, 1) if keep_fields else 1, f64)
+        self.HX = _scratch("HX", max(hxmax, 1) if keep_fields else 1, f64)
         self.blk_base = np.array([boff[first[s]] for s in range(plan.n_sub)], dtype=np.int64)
         self.h_base = np.array([hoff[first[s]] for s in range(plan.n_sub)], dtype=np.int64)
         self.d_blk, self.d_h = _dev(self.blk_base, i64), _dev(self.h_base, i64)
@@ -758,6 +799,7 @@ class SweepEngine:
     # ------------------------------------------------------------ (1) KL --
     def kl_fields(self):
         """K for every (Darcy sid, loc) system plus the mean-field K0 buffer."""
+        _claim(self.st, "K")
         st, plan = self.st, self.plan
         K = st.K
         if st.kl:
@@ -776,6 +818,8 @@ class SweepEngine:
         the engine's stream waits for the side stream before returning."""
         torch = self.torch
         st, plan = self.st, self.plan
+        _check_owner(st, "K")
+        _claim(st, "blocks", "hbar", "M", "Fb", "work", "X", "Lstore", "HX")
         waves, hwaves = st.waves_for(sids)
         self._last_waves = list(waves) + list(hwaves)
         if self.timing:
@@ -859,6 +903,7 @@ class SweepEngine:
         return their residual histories as a SegmentedHist, the others as
         [n_pts, hist_cap]."""
         torch, plan, st = self.torch, self.plan, self.st
+        _check_owner(st, "blocks", "hbar")
         n_real = plan.grid.n_real
         n_pts = n_real - k0 if n_pts is None else n_pts
         nl = plan.n_lambda
@@ -888,7 +933,9 @@ class SweepEngine:
             cap = hist_segments
             if cap is None:
                 free = torch.cuda.mem_get_info()[0]
-                cap = int(min(n_pts * max_segs, max(free // 8, 1 << 28) // (8 * seg)))
+                # room for a mean of 64 segments (65k iterations) per point,
+                # within an eighth of free memory; an overflow reruns exactly
+                cap = int(min(n_pts * min(max_segs, 64), max(free // 8, 1 << 28) // (8 * seg)))
             counter = ct["seg_counter"] if ct is not None else mt["seg_counter"]
             while True:
                 pool = torch.empty(int(cap) * seg, dtype=torch.float64, device="cuda")
@@ -1241,6 +1288,7 @@ class SweepEngine:
     def moments_launch(self, lam, sids=None, with_lambda=True):
         """Queue the moment kernels and the device->host copy of their
         results; moments_finish() waits and builds the dict."""
+        _check_owner(self.st, "M", "Fb")
         torch, plan, st = self.torch, self.plan, self.st
         nl, n_real = plan.n_lambda, plan.grid.n_real
         f64 = torch.float64
