@@ -278,7 +278,9 @@ int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
  * (sid, loc) at pk_base[sid] + loc * pk_size[sid]. scratch:
  * mfb_cg_multi_scratch_doubles(n_lambda, n_cta) doubles (x, r and S p of
  * the points in flight). seg_tab != NULL: residual histories in segments of
- * hist_cap entries, as mfb_cg_cluster's (res_hist = the pool).
+ * hist_cap entries, as mfb_cg_cluster's (res_hist = the pool). trec[12 *
+ * n_tasks]: per task its run (as tasks[]), per side nd | (region + 1) << 16,
+ * dof_ptr, packed strip base (loc 0) and packed block size.
  */
 long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta);
 int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int *dof_ptr,
@@ -289,7 +291,8 @@ int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int
                  double *res_hist, int hist_cap, double *g, const int *tasks, int n_tasks,
                  const int *sides, const double *packed, const long long *pk_base,
                  const int *pk_size, int n_cta, double *scratch, int *counter, int *seg_tab,
-                 int max_segs, long long seg_cap, int *seg_counter, void *stream);
+                 int max_segs, long long seg_cap, int *seg_counter, const int *trec,
+                 void *stream);
 
 /*
  * Same contract again, on thread-block clusters of C CTAs (C <= 8) holding
@@ -317,6 +320,7 @@ int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int
 int mfb_cg_cluster_max_clusters(int C, int NP, int n_own_max, long long smem);
 int mfb_debug_cluster(int stop_at);   /* debug: stop the cluster CG at a phase (0: off; 100: phase clocks) */
 int mfb_debug_cluster_prof(long long *out, int n);   /* per-CTA phase clocks of the last run */
+int mfb_debug_multi(int on, long long *out);   /* multi CG phase clocks: on/off, or read (out) */
 long long mfb_cg_cluster_smem(int NP, int n_used_max, int n_own_max, int n_cut_max,
                               int n_cm_max, int n_unit_max, int n_strip_max, int n_regions,
                               int flags);

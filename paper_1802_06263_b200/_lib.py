@@ -9,7 +9,7 @@ import os
 
 from .errors import NativeLibraryError
 
-_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_mfb.so")
+_SO = os.environ.get("MFB_LIBRARY") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_mfb.so")
 _lib = None
 
 _p = ctypes.c_void_p
@@ -70,9 +70,10 @@ _SIGS = {
     "mfb_cg_multi_scratch_doubles": ([_i, _i], _ll),
     "mfb_cg_multi": ([_i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
                       _p, _p, _p, _p, _i, _p, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _ll,
-                      _p, _p], _i),
+                      _p, _p, _p], _i),
     "mfb_cg_pack": ([_i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p], _i),
     "mfb_debug_cluster": ([_i], _i),
+    "mfb_debug_multi": ([_i, _p], _i),
     "mfb_debug_cluster_prof": ([_p, _i], _i),
     "mfb_cg_cluster_max_clusters": ([_i, _i, _i, _ll], _i),
     "mfb_cg_cluster_smem": ([_i, _i, _i, _i, _i, _i, _i, _i, _i], _ll),

@@ -52,6 +52,7 @@ struct CgMultiArgs {
     const long long *blk_base, *h_base;
     const double *blocks, *hbar;
     const int4 *tasks;           // {d0, strip lower, strip upper, i | (j + 1) << 12 | R << 24}
+    const int4 *trec;            // per task 3 int4: the run, side metadata, side strips
     const double *packed;        // blocks as MMA-fragment strips (mfb_cg_pack)
     const long long *pk_base;    // per sid: packed block of loc l at pk_base + l * pk_size
     const int *pk_size;
@@ -103,7 +104,7 @@ __device__ __forceinline__ void reduce_pairs(double &v0, double &v1, double (*re
 // checks), 0 the generic path.
 template <int NT4>
 __device__ __forceinline__ void strip_pass(const double *__restrict__ Sl, const int *dm, int nd,
-                                           const double *__restrict__ ps, bool all, double bm,
+                                           const double *__restrict__ ps, int m,
                                            double &d0, double &d1) {
     const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
     const int nt4 = NT4 > 0 ? NT4 : (nd + 3) >> 2;
@@ -122,27 +123,19 @@ __device__ __forceinline__ void strip_pass(const double *__restrict__ Sl, const 
                 dv[t] = (NT4 > 0 || c < nd) ? dm[c] + g : g;
             }
         }
-        if (all) {
 #pragma unroll
-            for (int t = 0; t < MPF; t += 2) {
-                if (NT4 > 0 ? (t0 + t >= NT4) : (t0 + t >= nt4)) break;
-                dmma884(e0, e1, af[t], ps[dv[t]]);
-                if (NT4 > 0 ? (t0 + t + 1 < NT4) : (t0 + t + 1 < nt4))
-                    dmma884(o0, o1, af[t + 1], ps[dv[t + 1]]);
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < MPF; t += 2) {
-                if (NT4 > 0 ? (t0 + t >= NT4) : (t0 + t >= nt4)) break;
-                dmma884(e0, e1, af[t], ps[dv[t]] * bm);
-                if (NT4 > 0 ? (t0 + t + 1 < NT4) : (t0 + t + 1 < nt4))
-                    dmma884(o0, o1, af[t + 1], ps[dv[t + 1]] * bm);
-            }
+        for (int t = 0; t < MPF; t += 2) {
+            if (NT4 > 0 ? (t0 + t >= NT4) : (t0 + t >= nt4)) break;
+            dmma884(e0, e1, af[t], ps[dv[t]]);
+            if (NT4 > 0 ? (t0 + t + 1 < NT4) : (t0 + t + 1 < nt4))
+                dmma884(o0, o1, af[t + 1], ps[dv[t + 1]]);
         }
     }
-    // slots outside the group have e = o = 0 here: d + 0 leaves them
-    d0 += e0 + o0;
-    d1 += e1 + o1;
+    // B was every slot's p: a column only feeds its own slot's outputs, so the
+    // group's members take the products and the other slots keep their
+    // accumulators (what a zero B column gives: x + 0 = x)
+    if ((m >> (2 * q)) & 1) d0 += e0 + o0;
+    if ((m >> (2 * q + 1)) & 1) d1 += e1 + o1;
 }
 
 // acc += the 8-row strip at `soff` of subdomain sid's packed block (slot
@@ -152,31 +145,27 @@ __device__ __forceinline__ void strip_pass(const double *__restrict__ Sl, const 
 // A load is one coalesced 256-byte warp access. The slots are visited by
 // local-realization group (g_cnt / g_loc / g_mask per region, rebuilt when
 // slots are refilled); the frozen Stokes blocks are one group.
-__device__ __forceinline__ void side_mma(const CgMultiArgs &A, int sid, int soff,
+__device__ __forceinline__ void side_mma(const double *__restrict__ packed, int nd, int reg,
+                                         int dmo, int pkb, int psz,
                                          const double *__restrict__ ps, const int *sdm,
                                          const int *g_cnt, const int *g_loc, const int *g_mask,
                                          int live, double &d0, double &d1) {
-    const int lane = threadIdx.x & 31, g = lane >> 2;
-    const int nd = A.ndof[sid];
-    const int reg = A.region[sid];
-    const int *dm = sdm + A.dof_ptr[sid];       // shared: dof * MP
-    const double *base = A.packed + A.pk_base[sid] + soff + lane;
-    const int psz = A.pk_size[sid];
+    const int lane = threadIdx.x & 31;
+    const int *dm = sdm + dmo;                  // shared: dof * MP
+    const double *base = packed + pkb + lane;
     const int ngrp = reg < 0 ? 1 : g_cnt[reg];
     for (int gi = 0; gi < ngrp; ++gi) {
         const int m = reg < 0 ? live : (g_mask[reg * MP + gi] & live);
         if (!m) continue;
         const int l = reg < 0 ? 0 : g_loc[reg * MP + gi];
-        const bool all = (m == live);
-        const double bm = ((m >> g) & 1) ? 1.0 : 0.0;
         const double *Sl = base + (long long)l * psz;
         switch (nd) {
-        case 16: strip_pass<4>(Sl, dm, nd, ps, all, bm, d0, d1); break;
-        case 24: strip_pass<6>(Sl, dm, nd, ps, all, bm, d0, d1); break;
-        case 32: strip_pass<8>(Sl, dm, nd, ps, all, bm, d0, d1); break;
-        case 48: strip_pass<12>(Sl, dm, nd, ps, all, bm, d0, d1); break;
-        case 64: strip_pass<16>(Sl, dm, nd, ps, all, bm, d0, d1); break;
-        default: strip_pass<0>(Sl, dm, nd, ps, all, bm, d0, d1); break;
+        case 16: strip_pass<4>(Sl, dm, nd, ps, m, d0, d1); break;
+        case 24: strip_pass<6>(Sl, dm, nd, ps, m, d0, d1); break;
+        case 32: strip_pass<8>(Sl, dm, nd, ps, m, d0, d1); break;
+        case 48: strip_pass<12>(Sl, dm, nd, ps, m, d0, d1); break;
+        case 64: strip_pass<16>(Sl, dm, nd, ps, m, d0, d1); break;
+        default: strip_pass<0>(Sl, dm, nd, ps, m, d0, d1); break;
         }
     }
 }
@@ -203,6 +192,25 @@ __global__ void cg_pack_kernel(const int4 *__restrict__ strips, const int *__res
 
 enum { SLOT_RUN = 0, SLOT_NEW = 1, SLOT_DONE = 2 };
 
+__device__ int g_multi_dbg;
+__device__ long long g_multi_prof[148 * 8];
+// phase clocks (tools/multi_phases.py) only in a -DMFB_PHASE_PROF build: the
+// counters cost registers the production kernel needs
+#ifdef MFB_PHASE_PROF
+#define MP_T(i)                                                     \
+    do {                                                            \
+        if (dbg && threadIdx.x == 0) {                              \
+            const long long t_ = clock64();                         \
+            pt[i] += t_ - tc;                                       \
+            tc = t_;                                                \
+        }                                                           \
+    } while (0)
+#define MP_PROF 1
+#else
+#define MP_T(i) do { } while (0)
+#define MP_PROF 0
+#endif
+
 __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     extern __shared__ double ps[];                 // [n_lambda][MP], then the dof lists
     __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP], s_seg[MP];
@@ -218,15 +226,21 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     double *Xs = A.scratch + (long long)blockIdx.x * 3 * n * MP;
     double *Rs = Xs + (long long)n * MP;
     double *Ss = Rs + (long long)n * MP;
-    double2 *X2 = reinterpret_cast<double2 *>(Xs);
-    double2 *R2 = reinterpret_cast<double2 *>(Rs);
-    double2 *S2 = reinterpret_cast<double2 *>(Ss);
+    // x, r, S p: disjoint thirds of this CTA's scratch
+    double2 *__restrict__ X2 = reinterpret_cast<double2 *>(Xs);
+    double2 *__restrict__ R2 = reinterpret_cast<double2 *>(Rs);
+    double2 *__restrict__ S2 = reinterpret_cast<double2 *>(Ss);
     double2 *P2 = reinterpret_cast<double2 *>(ps);
     int *sdm = reinterpret_cast<int *>(ps + (long long)n * MP);   // dof_map * MP
     if (tid < MP) { s_k[tid] = -1; s_state[tid] = SLOT_DONE; }
     for (int e = tid; e < n * MP; e += MNT) ps[e] = 0.0;
     for (int e = tid; e < A.dof_ptr[A.n_sub]; e += MNT) sdm[e] = A.dof_map[e] * MP;
 
+#if MP_PROF
+    const int dbg = g_multi_dbg;
+    long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tc = clock64();
+#endif
     for (;;) {
         __syncthreads();
         // ---- refill empty slots from the global work counter --------------
@@ -321,18 +335,27 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
         int run = 0;
 #pragma unroll
         for (int s = 0; s < MP; ++s) run |= (s_state[s] == SLOT_RUN) << s;
+        MP_T(0);
 
         // ---- Phase A: S p on the tensor cores; p.S p --------------------------
         v0 = 0.0; v1 = 0.0;
         if (run) {
             const int g8 = lane >> 2;
+            // task records {run}{nd | region + 1 << 16 per side, dof_ptr per side}
+            // {packed strip base per side, packed block size per side}: the
+            // next task's record is fetched while this task runs
+            const int4 *rec = A.trec;
             for (int ti = wid; ti < A.n_tasks; ti += MW) {
-                const int4 T = A.tasks[ti];
-                const int i = T.w & 0xfff, j = ((T.w >> 12) & 0xfff) - 1, R = T.w >> 24;
+                const int4 T = __ldg(rec + 3 * ti), U = __ldg(rec + 3 * ti + 1),
+                           V = __ldg(rec + 3 * ti + 2);
+                const int j = ((T.w >> 12) & 0xfff) - 1, Rr = T.w >> 24;
                 double lo0 = 0.0, lo1 = 0.0, up0 = 0.0, up1 = 0.0;
-                side_mma(A, i, T.y, ps, sdm, s_gcnt, s_gloc, s_gmask, run, lo0, lo1);
-                if (j >= 0) side_mma(A, j, T.z, ps, sdm, s_gcnt, s_gloc, s_gmask, run, up0, up1);
-                if (g8 < R) {
+                side_mma(A.packed, U.x & 0xffff, (U.x >> 16) - 1, U.z, V.x, V.z, ps, sdm, s_gcnt,
+                         s_gloc, s_gmask, run, lo0, lo1);
+                if (j >= 0)
+                    side_mma(A.packed, U.y & 0xffff, (U.y >> 16) - 1, U.w, V.y, V.w, ps, sdm,
+                             s_gcnt, s_gloc, s_gmask, run, up0, up1);
+                if (g8 < Rr) {
                     const int d = T.x + g8;
                     const double2 sp = j >= 0 ? make_double2(lo0 + up0, lo1 + up1)
                                               : make_double2(lo0, lo1);
@@ -344,7 +367,9 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                 }
             }
         }
+        MP_T(1);
         reduce_pairs(v0, v1, s_red, s_tot);
+        MP_T(2);
         if (tid < MP && ((run >> tid) & 1)) {
             const double pSp = s_tot[tid];
             s_it[tid] += 1;
@@ -382,7 +407,9 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                 R2[e] = r2;
             }
         }
+        MP_T(3);
         reduce_pairs(v0, v1, s_red, s_tot);
+        MP_T(4);
         if (tid < MP && ((upd >> tid) & 1)) {
             const double rr_new = s_tot[tid];
             const double rn = sqrt(rr_new);
@@ -445,15 +472,30 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
             }
         }
         __syncthreads();
+        MP_T(5);
+#if MP_PROF
+        pt[6] += dbg && tid == 0;
+#endif
         if (tid < MP && ((fin >> tid) & 1)) {
             A.iters[s_k[tid]] = s_stat[tid] == MFB_CG_ZERO_RHS ? 0 : s_it[tid];
             A.status[s_k[tid]] = s_stat[tid];
             s_k[tid] = -1;
         }
     }
+#if MP_PROF
+    if (dbg && threadIdx.x == 0 && blockIdx.x < 148)
+        for (int i = 0; i < 8; ++i) g_multi_prof[blockIdx.x * 8 + i] = pt[i];
+#endif
 }
 
 }  // namespace
+
+extern "C" int mfb_debug_multi(int on, long long *out) {
+    if (out)
+        return cudaMemcpyFromSymbol(out, g_multi_prof, sizeof(long long) * 148 * 8) ==
+                       cudaSuccess ? 0 : 2;
+    return cudaMemcpyToSymbol(g_multi_dbg, &on, sizeof(int)) == cudaSuccess ? 0 : 2;
+}
 
 extern "C" long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta) {
     return (long long)n_cta * 3 * n_lambda * MP;
@@ -470,7 +512,7 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
                             const int *sides, const double *packed, const long long *pk_base,
                             const int *pk_size, int n_cta, double *scratch, int *counter,
                             int *seg_tab, int max_segs, long long seg_cap, int *seg_counter,
-                            void *stream) {
+                            const int *trec, void *stream) {
     if (n_pts <= 0) return n_pts == 0 ? MFB_OK : MFB_ERR_ARG;
     if (n_lambda <= 0 || n_sub <= 0 || n_sub >= 4095 || n_rows <= 0 || n_regions > MREG || n_cta <= 0 ||
         max_iter < 1 || hist_cap < 1 || n_tasks <= 0 ||
@@ -491,6 +533,8 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
     A.local_idx = local_idx; A.blk_base = blk_base; A.h_base = h_base;
     A.blocks = blocks; A.hbar = hbar;
     A.tasks = reinterpret_cast<const int4 *>(tasks);
+    A.trec = reinterpret_cast<const int4 *>(trec);
+    if (!trec) return MFB_ERR_ARG;
     A.sides = reinterpret_cast<const int4 *>(sides);
     A.packed = packed; A.pk_base = pk_base; A.pk_size = pk_size;
     A.lam = lam; A.res_hist = res_hist; A.g = g; A.scratch = scratch;

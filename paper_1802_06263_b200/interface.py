@@ -968,7 +968,7 @@ class SweepEngine:
                         mt["n_tasks"], _ptr(mt["sides"]), _ptr(mt["packed"]),
                         _ptr(mt["pk_base"]), _ptr(mt["pk_size"]), mt["n_cta"],
                         _ptr(mt["scratch"]), _ptr(mt["counter"]), _ptr(seg_tab), max_segs,
-                        int(cap), _ptr(counter), self.sp), "mfb_cg_multi")
+                        int(cap), _ptr(counter), _ptr(mt["trec"]), self.sp), "mfb_cg_multi")
                 hist = SegmentedHist(pool, seg_tab, seg, counter, cap)
                 if not check_hist or hist.complete():   # complete() syncs the stream
                     break
@@ -1009,7 +1009,27 @@ class SweepEngine:
                                                    nl)
             n_loc = st.n_loc.astype(np.int64)
             pk_base = np.concatenate([[0], np.cumsum(pk_size.astype(np.int64) * n_loc)])
+            if pk_base[-1] >= 2 ** 31:
+                raise NativeLibraryError("packed basis pool exceeds 2^31 doubles")
+            # per task record (mfb_cg_multi): the run, then per side (nd |
+            # (CG region + 1) << 16, dof_ptr) and (strip base, block size)
+            creg = (np.zeros(plan.n_sub, dtype=np.int64) if self.st.method == "S2"
+                    else plan.region.astype(np.int64))
+            trec = np.zeros((len(tab), 12), dtype=np.int64)
+            for t, (d0, so_lo, so_up, meta) in enumerate(tab.astype(np.int64)):
+                i, j = meta & 0xfff, ((meta >> 12) & 0xfff) - 1
+                trec[t, :4] = (d0, so_lo, so_up, meta)
+                trec[t, 4] = nd[i] | ((creg[i] + 1) << 16)
+                trec[t, 6] = plan.dof_ptr[i]
+                trec[t, 8] = pk_base[i] + so_lo
+                trec[t, 10] = pk_size[i]
+                if j >= 0:
+                    trec[t, 5] = nd[j] | ((creg[j] + 1) << 16)
+                    trec[t, 7] = plan.dof_ptr[j]
+                    trec[t, 9] = pk_base[j] + so_up
+                    trec[t, 11] = pk_size[j]
             mt = {"tasks": _dev(tab.ravel(), torch.int32), "n_tasks": int(len(tab)),
+                  "trec": _dev(trec.ravel().astype(np.int32), torch.int32),
                   "sides": _dev(sides.ravel(), torch.int32),
                   "strips": _dev(strips.ravel(), torch.int32), "n_strips": int(len(strips)),
                   "pk_size": _dev(pk_size, torch.int32), "pk_base": _dev(pk_base[:-1], torch.int64),
