@@ -49,6 +49,10 @@
 extern "C" {
 #endif
 
+/* shape limits the host checks before launching (interface.py) */
+#define MFB_MOMENTS_MAX_NDOF 64   /* mortar dofs per subdomain in mfb_group_stats/fields */
+#define MFB_KL_MAX_TERM 64        /* KL terms per region in mfb_kl_realize*[_batched] */
+
 #define MFB_OK 0
 #define MFB_ERR_ARG 1
 #define MFB_ERR_LAUNCH 2

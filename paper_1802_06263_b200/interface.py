@@ -88,7 +88,9 @@ BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 S1_FIELD_BYTES_MAX = 32 << 30   # S1 keeps every realization's fields for the moments
 S1_CHUNK_REALIZATIONS = None    # S1 realizations per chunk (None: as many as fit)
 CLUSTER_SHAPES = ((4, 16), (8, 16), (2, 8), (4, 8))   # (CTAs per cluster, points) to try
-HIST_SEG = 1024             # residual-history segment (cluster CG)
+HIST_SEG = 1024             # residual-history segment (large-interface CG kernels)
+MOMENTS_MAX_NDOF = 64       # mfb_group_stats / mfb_group_fields block limit (mfb.h)
+KL_MAX_TERM = 64            # mfb_kl_realize_batched terms per region (mfb.h)
 
 
 @dataclass
@@ -482,6 +484,9 @@ class _SweepStatic:
             t = tabs[j]
             t.phi, t.mean, t.xi = d_phi.data_ptr(), d_mean.data_ptr(), d_xi.data_ptr()
             t.dst0, t.dst, t.ld = int(plan.k0_off[s_]), int(dst), int(ld)
+            if int(nt) > KL_MAX_TERM:
+                raise NativeLibraryError(f"KL kernel: {int(nt)} terms in one region exceed "
+                                         f"{KL_MAX_TERM}")
             t.n_cells, t.n_term, t.n_rows = int(nc), int(nt), int(nrows)
         self.kl_tab = torch.frombuffer(bytearray(bytes(tabs)), dtype=torch.uint8).to("cuda")
         self.kl_max_rows = max([t[7] for t in self.kl], default=0)
@@ -985,6 +990,9 @@ class SweepEngine:
             "cg_pair_kernel (one CTA per point, block rows in registers)"
             if 0 < reg_ndof <= 32 and 2 * nl <= 608 else
             "cg_kernel (one CTA per point, blocks staged in shared memory or read from L2)")
+        if st.blocks.numel() >= 2 ** 31:
+            raise NativeLibraryError("the one-CTA-per-point CG addresses the basis pool with "
+                                     "32-bit offsets: pool of 2^31 doubles or more")
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
             _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(st.d_cg_local), n_real,
@@ -1330,6 +1338,11 @@ class SweepEngine:
                 ctypes.c_void_p(rp + 8 * nl), ctypes.c_void_p(rp + 16 * nl),
                 self.sp), "mfb_lambda_moments")
         if ng:
+            if int(plan.ndof.max()) > MOMENTS_MAX_NDOF:
+                raise NativeLibraryError(
+                    f"moment kernels hold a subdomain's mortar block in shared memory: "
+                    f"{int(plan.ndof.max())} mortar dofs on one subdomain exceed "
+                    f"{MOMENTS_MAX_NDOF}")
             W = torch.empty(ng, dtype=f64, device="cuda")
             lstar = torch.empty(st.nv, dtype=f64, device="cuda")
             s_ = torch.empty_like(lstar)

@@ -11,6 +11,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
+# sweep parity: moments within max(1e-8, FLOOR_MULT x the reference's own
+# reorder noise floor of that key (the same sweep, GEMV order reversed))
+FLOOR_MULT = 2
 
 # the reference package whose objects the drop-in consumes (environment, or
 # the repo's baseline/_ref install; paper_1802_06263_b200/_ref.py)
