@@ -115,8 +115,26 @@ def load(path=_SO):
         fn = getattr(lib_, name)
         fn.argtypes = args
         fn.restype = res
+    _check_provenance(lib_, path)
     _lib = lib_
     return _lib
+
+
+def _check_provenance(lib_, path):
+    """The library must have been built from the sources in this tree
+    (mfb_version carries the source hash _build embedded). A library built
+    elsewhere (MFB_LIBRARY, experiments) is accepted only with
+    MFB_ALLOW_FOREIGN_LIBRARY=1."""
+    from . import _build
+    ver = lib_.mfb_version().decode()
+    built = ver.rsplit(" src ", 1)[-1] if " src " in ver else "unknown"
+    if not _build.source_files():
+        return                                  # sources not shipped: nothing to compare
+    tree = _build.source_hash()
+    if built != tree and os.environ.get("MFB_ALLOW_FOREIGN_LIBRARY") != "1":
+        raise NativeLibraryError(
+            f"{path} was built from sources {built}, the tree is {tree}: rebuild with "
+            f"`python -m paper_1802_06263_b200._build --force`")
 
 
 def lib():

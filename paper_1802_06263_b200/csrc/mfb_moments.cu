@@ -255,7 +255,14 @@ extern "C" int mfb_lambda_moments(int n_lambda, int n_real, const double *lam,
     return MFB_OK;
 }
 
-extern "C" const char *mfb_version(void) { return "mfb-b200 0.1.0 (sm_100a)"; }
+#ifndef MFB_SOURCE_HASH
+#define MFB_SOURCE_HASH "unknown"
+#endif
+// "mfb-b200 <version> (sm_100a) src <hash>": <hash> = _build.source_hash() of
+// the csrc/include tree this library was compiled from (checked at load time)
+extern "C" const char *mfb_version(void) {
+    return "mfb-b200 0.2.0 (sm_100a) src " MFB_SOURCE_HASH;
+}
 
 extern "C" const char *mfb_strerror(int code) {
     switch (code) {

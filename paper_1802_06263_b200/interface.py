@@ -897,7 +897,8 @@ class SweepEngine:
 
     # ---------------------------------------------------------- (3) CG ----
     def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False,
-                     kernel="auto", cluster_shape=None, hist_segments=None, check_hist=False):
+                     kernel="auto", cluster_shape=None, hist_segments=None, check_hist=False,
+                     local_override=None):
         """CG over points k0..k0+n_pts-1. kernel: "auto" (multi-point when the
         blocks exceed shared memory and the points fill the GPU, else one CTA
         per point with register-resident block rows when they fit), "cta"
@@ -910,6 +911,12 @@ class SweepEngine:
         torch, plan, st = self.torch, self.plan, self.st
         _check_owner(st, "blocks", "hbar")
         n_real = plan.grid.n_real
+        cg_local = st.d_cg_local
+        if local_override is not None:
+            # points 0..n-1 of a caller-built local-index table [regions, n]
+            # (distributed.py: a rank's interleaved points)
+            cg_local = local_override
+            n_real, k0 = int(local_override.shape[1]), 0
         n_pts = n_real - k0 if n_pts is None else n_pts
         nl = plan.n_lambda
         hist_cap = max_iter if hist_cap is None else hist_cap
@@ -955,7 +962,7 @@ class SweepEngine:
                         ct["n_used_max"], ct["n_cut_max"], ct["n_cm_max"], ct["n_unit_max"],
                         ct["n_strip_max"], ct["flags"], ct["smem"], _ptr(plan.d_ndof),
                         _ptr(st.d_cg_region), int(st.d_cg_local.shape[0]), _ptr(st.d_h),
-                        _ptr(st.d_cg_local), n_real, _ptr(st.hbar), _ptr(mt["sides"]),
+                        _ptr(cg_local), n_real, _ptr(st.hbar), _ptr(mt["sides"]),
                         _ptr(mt["packed"]), k0, n_pts, float(tol), int(max_iter), _ptr(lam),
                         _ptr(iters), _ptr(status), _ptr(g) if keep_g else None, _ptr(ct["xs"]),
                         _ptr(ct["rs"]), _ptr(ct["ss"]), ct["n_clusters"], _ptr(mt["counter"]),
@@ -967,7 +974,7 @@ class SweepEngine:
                         nl, plan.n_sub, int(plan.dof_ptr[-1]), _ptr(plan.d_ndof),
                         _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map), _ptr(st.d_cg_region),
                         int(st.d_cg_local.shape[0]), _ptr(st.d_blk), _ptr(st.d_h),
-                        _ptr(st.d_cg_local), n_real, _ptr(st.blocks), _ptr(st.hbar), k0, n_pts,
+                        _ptr(cg_local), n_real, _ptr(st.blocks), _ptr(st.hbar), k0, n_pts,
                         float(tol), int(max_iter), _ptr(lam), _ptr(iters), _ptr(status),
                         _ptr(pool), seg, _ptr(g) if keep_g else None, _ptr(mt["tasks"]),
                         mt["n_tasks"], _ptr(mt["sides"]), _ptr(mt["packed"]),
@@ -995,7 +1002,7 @@ class SweepEngine:
                                      "32-bit offsets: pool of 2^31 doubles or more")
         _lib.check(self.L.mfb_cg_batched(
             nl, plan.n_sub, _ptr(plan.d_ndof), _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map),
-            _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(st.d_cg_local), n_real,
+            _ptr(st.d_cg_region), _ptr(st.d_blk), _ptr(st.d_h), _ptr(cg_local), n_real,
             _ptr(st.blocks), _ptr(st.hbar), k0, n_pts, float(tol), int(max_iter),
             _ptr(lam), _ptr(iters), _ptr(status), _ptr(hist), max(hist_cap, 1),
             _ptr(g) if keep_g else None, int(np.sum(plan.ndof.astype(np.int64) ** 2)),

@@ -29,6 +29,9 @@ def test_library_builds_and_exports_header_symbols():
     assert sorted(_lib.exported_symbols()) == declared
     loaded = _lib.load()
     assert loaded.mfb_version().decode().startswith("mfb-b200")
+    # provenance: the library carries the hash of the sources it was built from
+    from paper_1802_06263_b200 import _build
+    assert loaded.mfb_version().decode().endswith("src " + _build.source_hash())
 
 
 def test_sass_has_fp64_tensor_instructions():

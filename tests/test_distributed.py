@@ -17,14 +17,15 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1802_06263_b200.distributed import point_range, run_sharded, sid_owners
+from paper_1802_06263_b200.distributed import point_range, point_set, run_sharded, sid_owners
 
 N_SUB, N_LOC, N_REAL, N_LAMBDA, HIST = 5, 4, 37, 6, 3
 
 
 class FakeEngine:
-    def __init__(self):
+    def __init__(self, singular_sid=None):
         self.pool = torch.zeros(N_SUB * N_LOC, dtype=torch.float64)
+        self.singular_sid = singular_sid
 
     def sid_costs(self):
         return [float(3 + (s % 3)) for s in range(N_SUB)]
@@ -34,19 +35,24 @@ class FakeEngine:
         for s in sids:
             for l in range(N_LOC):
                 self.pool[s * N_LOC + l] = np.sin(1.0 + s * 7.3 + l * 1.1)
+        if self.singular_sid in sids:
+            return f"subdomain {self.singular_sid} (local realization 0): singular system"
+        return None
 
     def pools(self):
         return [self.pool]
 
-    def solve(self, k0, n, tol, max_iter):
+    def solve(self, pts, tol, max_iter):
+        n = len(pts)
         lam = torch.zeros((n, N_LAMBDA), dtype=torch.float64)
-        for j in range(n):
-            k = k0 + j
+        for j, k in enumerate(pts):
+            k = int(k)
             for d in range(N_LAMBDA):
                 lam[j, d] = self.pool[(k * 3 + d) % self.pool.numel()] * (1 + 0.01 * k)
-        iters = torch.arange(k0, k0 + n, dtype=torch.int32) % 7 + 1
+        iters = torch.as_tensor(np.asarray(pts) % 7 + 1, dtype=torch.int32)
         status = torch.zeros(n, dtype=torch.int32)
-        hist = torch.full((n, HIST), 0.5, dtype=torch.float64)
+        # histories of per-rank widths (the gather pads to the widest)
+        hist = torch.full((n, HIST + (int(pts[0]) % 2 if n else 0)), 0.5, dtype=torch.float64)
         return lam, iters, status, hist
 
     def moments(self, lam_all, sids, with_lambda):
@@ -71,34 +77,45 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, singular_sid=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        out = run_sharded(FakeEngine(), N_REAL, N_LAMBDA, 1e-9, 10, dist, rank, world)
+        try:
+            out = run_sharded(FakeEngine(singular_sid), N_REAL, N_LAMBDA, 1e-9, 10, dist, rank,
+                              world)
+        except Exception as e:  # noqa: BLE001 - reported to the parent
+            q.put({"rank": rank, "error": type(e).__name__, "msg": str(e)})
+            return
+        mom, lam, iters, status, hist = out
         if rank == 0:
-            mom, lam, iters, status, hist = out
             q.put({"mom": {k: (v[0].tolist(), v[1].tolist()) for k, v in mom.items()},
                    "lam": lam.tolist(), "iters": iters.tolist()})
+        else:
+            assert mom is None and lam.shape == (N_REAL, N_LAMBDA)
     finally:
         dist.destroy_process_group()
 
 
-def _run(world):
+def _run(world, singular_sid=None, n_msgs=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, singular_sid))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = q.get(timeout=120)
+    res = [q.get(timeout=120) for _ in range(n_msgs)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    return res
+    return res[0] if n_msgs == 1 else res
 
 
 def test_partition_helpers():
+    sets = [point_set(37, r, 4) for r in range(4)]
+    assert sorted(np.concatenate(sets).tolist()) == list(range(37))
+    assert max(map(len, sets)) - min(map(len, sets)) <= 1
     ranges = [point_range(37, r, 4) for r in range(4)]
     assert ranges[0][0] == 0 and ranges[-1][1] == 37
     assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
@@ -106,6 +123,19 @@ def test_partition_helpers():
     own = sid_owners([5, 1, 4, 4, 2], 2)
     assert sorted(set(own)) == [0, 1]
     assert own == sid_owners([5, 1, 4, 4, 2], 2)          # deterministic
+
+
+@pytest.mark.timeout(300)
+def test_singular_system_on_one_rank_raises_on_every_rank():
+    """A singular system in a subdomain owned by rank 1 must not leave rank 0
+    waiting in the pool all-reduce: the verdict is agreed first and both
+    ranks raise SingularOperatorError (with rank 1's message)."""
+    owners = sid_owners([float(3 + (s % 3)) for s in range(N_SUB)], 2)
+    sid = owners.index(1)
+    res = _run(2, singular_sid=sid, n_msgs=2)
+    assert sorted(r["rank"] for r in res) == [0, 1]
+    assert all(r["error"] == "SingularOperatorError" for r in res)
+    assert all(f"subdomain {sid}" in r["msg"] for r in res)
 
 
 @pytest.mark.timeout(300)

@@ -4,6 +4,6 @@
 N=${3:-2368}; I=${4:-400}
 for r in 1 2 3; do
   for L in "$1" "$2"; do
-    MFB_LIBRARY=$L timeout 300 python tools/prof_cg_multi.py $N $I multi 2>&1 | tail -1 | sed "s|^|$(basename $L) |"
+    MFB_ALLOW_FOREIGN_LIBRARY=1 MFB_LIBRARY=$L timeout 300 python tools/prof_cg_multi.py $N $I multi 2>&1 | tail -1 | sed "s|^|$(basename $L) |"
   done
 done
