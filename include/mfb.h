@@ -339,6 +339,19 @@ int mfb_cg_cluster(int n_lambda, int C, int NP, const int *hdr, const int *tab, 
                    int *seg_tab, int max_segs, int *seg_counter, void *stream);
 
 /*
+ * One interface-operator application out = S p from stored flux-basis blocks
+ * (the reference's basis_apply, interface.py:238-247): block of subdomain i
+ * column-major at blocks + blk_base[i] (ndof[i]^2), its rows = mortar dofs
+ * dof_map[dof_ptr[i]..]; sides[4 n_lambda] per dof {i, row in i, j, row in
+ * j} (j = -1: one side); out[d] = 0 + row_i + row_j. rows: dof_ptr[n_sub]
+ * doubles of scratch.
+ */
+int mfb_basis_apply(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
+                    const int *dof_map, const int *sides, const long long *blk_base,
+                    const double *blocks, const double *p, double *rows, double *out,
+                    void *stream);
+
+/*
  * Repack the basis pool for mfb_cg_multi: strips[4 * n_strips] = {sid, first
  * row, rows (<= 8), strip offset}; for every local realization l <
  * n_loc[sid] the strip's rows of block (sid, l) (column-major at blk_base[sid]

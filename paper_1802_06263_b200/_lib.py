@@ -72,6 +72,7 @@ _SIGS = {
                       _p, _p, _p, _p, _i, _p, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _ll,
                       _p, _p, _p], _i),
     "mfb_cg_pack": ([_i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p], _i),
+    "mfb_basis_apply": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_debug_cluster": ([_i], _i),
     "mfb_debug_multi": ([_i, _p], _i),
     "mfb_debug_cluster_prof": ([_p, _i], _i),
