@@ -128,6 +128,12 @@ typedef struct MfbHybPattern {
     const double *asm_coef;
     const int *z_dest, *z_tptr, *z_cell;
     const double *z_coef;
+    /* the same entries flattened per panel (panel width of the launch): the
+     * rows entering the window at panel pi are entries pe_ptr[pi]..
+     * pe_ptr[pi+1] of pe_rec (int4 {window offset of the destination, cell
+     * of term 0, cell of term 1, terms}) and pe_coef (double2 coefficients) */
+    const int *pe_ptr, *pe_rec;
+    const double *pe_coef;
 } MfbHybPattern;
 
 const char *mfb_version(void);

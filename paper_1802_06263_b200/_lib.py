@@ -46,7 +46,7 @@ class MfbHybPattern(ctypes.Structure):
         ("p_val", _p), ("src_k", _p), ("src_c", _p), ("cell_f", _p), ("cell_q", _p),
         ("z_n", _i), ("asm_ptr", _p), ("asm_row", _p), ("asm_dest", _p), ("asm_tptr", _p),
         ("asm_cell", _p), ("asm_coef", _p), ("z_dest", _p), ("z_tptr", _p), ("z_cell", _p),
-        ("z_coef", _p),
+        ("z_coef", _p), ("pe_ptr", _p), ("pe_rec", _p), ("pe_coef", _p),
     ]
 
 

@@ -91,6 +91,7 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     extern __shared__ double sm[];
     __shared__ int s_bad;
     __shared__ double s_inv[8];
+    __shared__ double s_linv[64];
 #ifdef MFB_PROFILE
     __shared__ long long s_t0[8];
 #endif
@@ -106,7 +107,15 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     double *Yb = Lb + m * LS;       // BP x Cp     L11^-1 (border rows of the panel)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int g = lane >> 2, q4 = lane & 3;
-    if (tid == 0) s_bad = 0;
+    if (tid == 0) {
+        s_bad = 0;
+        // the system's K (read a few cells per panel, first touch from DRAM)
+        // brought into L2 up front by one bulk prefetch
+        const unsigned bytes = (unsigned)(P.n_cells * 8) & ~15u;
+        if (bytes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(K), "r"(bytes)
+                         : "memory");
+    }
     for (int t = tid; t < Cp * Cp; t += HYB_NT) S[t] = 0.0;
     // initial border block Z and the first window rows (term tables, thread per entry)
     for (int t = tid; t < m * ws; t += HYB_NT) W[t] = 0.0;
@@ -181,35 +190,23 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                 s_inv[i] = 1.0 / a[i][i];
                 if (i < nb) Lb[i * LS + BP] = s_inv[i];   // padding column: 1 / L(i,i)
             }
-        }
-        if (wid == 0) {
-            __syncwarp();
-            // L21 = A21 L11^-T (lane per row), Yb = L11^-1 Yb (lane per column)
-            for (int i = nb + lane; i < nrow; i += 32) {
-                double x[BP];
+            // L11^-1 (lower triangular) for the panel solves on the tensor cores
 #pragma unroll
-                for (int q = 0; q < BP; ++q) {
-                    double v = q < nb ? Lb[i * LS + q] : 0.0;
+            for (int j = 0; j < 8; ++j) {
 #pragma unroll
-                    for (int qq = 0; qq < q; ++qq) v -= x[qq] * Lb[q * LS + qq];
-                    x[q] = q < nb ? v * s_inv[q] : 0.0;
+                for (int i = 0; i < 8; ++i) {
+                    double v = 0.0;
+                    if (i == j) {
+                        v = s_inv[i];
+                    } else if (i > j) {
+#pragma unroll
+                        for (int q = j; q < i; ++q) v -= a[i][q] * s_linv[q * 8 + j];
+                        v *= s_inv[i];
+                    }
+                    s_linv[i * 8 + j] = v;
                 }
-#pragma unroll
-                for (int q = 0; q < BP; ++q) Lb[i * LS + q] = x[q];
             }
-            for (int c = lane; c < Cp; c += 32) {
-                double y[BP];
-#pragma unroll
-                for (int q = 0; q < BP; ++q) {
-                    double v = q < nb ? Yb[q * Cp + c] : 0.0;
-#pragma unroll
-                    for (int qq = 0; qq < q; ++qq) v -= Lb[q * LS + qq] * y[qq];
-                    y[q] = q < nb ? v * s_inv[q] : 0.0;
-                }
-#pragma unroll
-                for (int q = 0; q < BP; ++q) Yb[q * Cp + c] = y[q];
-            }
-        } else {
+        } else if (wid > 0) {
             // rows entering the window take the freed slots of this panel:
             // zero them, sync the assembly warps, scatter the term-table entries
             const int r0 = k + m, r1 = min(n, k + m + BP);
@@ -221,12 +218,58 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                 for (int t = at; t < Cp; t += an) Pb[sl * Cp + t] = 0.0;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(HYB_NT - 32));
-            if (r1 > r0) assemble_entries(P, K, r0, r1, at, an, W, Pb, m, ws, Cp);
+            PROF_MARK(6);
+            // the entries of the entering rows, flattened per panel at plan time
+            // (hybrid.py panel_entries): record -> K, no table walk
+            const int e0 = P.pe_ptr[pi], e1 = P.pe_ptr[pi + 1];
+            const int4 *rec = reinterpret_cast<const int4 *>(P.pe_rec);
+            const double2 *cf = reinterpret_cast<const double2 *>(P.pe_coef);
+            for (int e = e0 + at; e < e1; e += an) {
+                const int4 r = rec[e];
+                const double2 c = cf[e];
+                double v = 0.0;
+                v += r.y >= 0 ? c.x * K[r.y] : c.x;
+                if (r.w > 1) v += r.z >= 0 ? c.y * K[r.z] : c.y;
+                W[r.x] = v;                           // W | Pb: one shared-memory region
+            }
+            PROF_MARK(7);
         }
         PROF_MARK(5);
         __syncthreads();
         PROF_MARK(2);
         if (s_bad) return;
+        {
+            // panel solves as products with L11^-1 on DMMA tiles (all warps):
+            // L21 = A21 L11^-T (row tiles), Yb = L11^-1 Yb (column tiles); a
+            // tile's operands are read before its results overwrite them
+            const int R = nrow - nb;
+            const int tr = (R + 7) >> 3, tc = Cp >> 3;
+            const double li0 = s_linv[g * 8 + q4], li1 = s_linv[g * 8 + 4 + q4];
+            for (int it = wid; it < tr + tc; it += HYB_NW) {
+                double d0 = 0.0, d1 = 0.0;
+                if (it < tr) {
+                    const int ra = nb + it * 8 + g;
+                    const double a0 = ra < nrow ? Lb[ra * LS + q4] : 0.0;
+                    const double a1 = ra < nrow ? Lb[ra * LS + 4 + q4] : 0.0;
+                    dmma(d0, d1, a0, li0);
+                    dmma(d0, d1, a1, li1);
+                    __syncwarp();
+                    if (ra < nrow) {
+                        Lb[ra * LS + 2 * q4] = d0;
+                        Lb[ra * LS + 2 * q4 + 1] = d1;
+                    }
+                } else {
+                    const int c = (it - tr) * 8;
+                    const double b0 = Yb[q4 * Cp + c + g], b1 = Yb[(4 + q4) * Cp + c + g];
+                    dmma(d0, d1, li0, b0);
+                    dmma(d0, d1, li1, b1);
+                    __syncwarp();
+                    Yb[g * Cp + c + 2 * q4] = d0;
+                    Yb[g * Cp + c + 2 * q4 + 1] = d1;
+                }
+            }
+        }
+        __syncthreads();
         PROF_MARK(3);
         if (Lstore) {
             double *dst = Lstore + sys_loff[s] + (long long)pi * pstride;

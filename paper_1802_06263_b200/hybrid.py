@@ -104,6 +104,40 @@ class HybPattern:
         l_doubles = n_pan * (m * (panel + 4) + panel * Cp)
         return ws, smem_c, smem_b, l_doubles, self.n * Cp
 
+    def panel_entries(self, panel):
+        """The assembly entries of the rows entering the condensation window at
+        each panel (mfb_darcy.cu condense_kernel), flattened: (pe_ptr [n_pan +
+        1], rec [N, 4] {window offset, cell 0, cell 1, terms}, coef [N, 2]).
+        The window offset is the entry's destination in the kernel's W | Pb
+        shared-memory rows (row r lives in slot r % (w + panel))."""
+        T = assembly_tables(self)
+        w, n = self.w, self.n
+        m = w + panel
+        ws = self.layout_for(panel)[0]
+        Cp = self.Cp
+        n_pan = (n + panel - 1) // panel
+        aptr = np.asarray(T["asm_ptr"], dtype=np.int64)
+        tptr = np.asarray(T["asm_tptr"], dtype=np.int64)
+        cell = np.asarray(T["asm_cell"], dtype=np.int64)
+        cf = np.asarray(T["asm_coef"], dtype=np.float64)
+        lo = aptr[min(m, n)]                        # entries of rows >= m, in row order
+        e = np.arange(lo, aptr[n])
+        row = np.repeat(np.arange(n), np.diff(aptr))[e]
+        d = np.asarray(T["asm_dest"], dtype=np.int64)[e]
+        slot = row % m
+        dest = np.where(d <= w, slot * ws + d, m * ws + slot * Cp + (d - w - 1))
+        t0, nt = tptr[e], tptr[e + 1] - tptr[e]
+        if np.any((nt < 1) | (nt > 2)):
+            raise ValueError("assembly entry with other than 1 or 2 terms")
+        two = nt == 2
+        c1 = np.where(two, cell[np.minimum(t0 + 1, len(cell) - 1)], -1)
+        k1 = np.where(two, cf[np.minimum(t0 + 1, len(cf) - 1)], 0.0)
+        rec = np.stack([dest, cell[t0], c1, nt], axis=1)
+        coef = np.stack([cf[t0], k1], axis=1)
+        r0 = np.minimum(np.arange(n_pan + 1) * panel + m, n)
+        ptr = aptr[r0] - lo
+        return ptr.astype(np.int32), rec.astype(np.int32), coef.astype(np.float64)
+
     def choose_panel(self):
         for panel in (8,):
             if self.layout_for(panel)[1] <= SMEM_LIMIT:

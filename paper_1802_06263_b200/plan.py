@@ -190,6 +190,9 @@ class DevicePlan:
                 "asm_cell": _dev(T["asm_cell"], i32), "asm_coef": _dev(T["asm_coef"], f64),
                 "z_dest": _dev(T["z_dest"], i32), "z_tptr": _dev(T["z_tptr"], i32),
                 "z_cell": _dev(T["z_cell"], i32), "z_coef": _dev(T["z_coef"], f64)})
+            pe_ptr, pe_rec, pe_coef = h.panel_entries(self.hyb_panel[s])
+            arrs.update({"pe_ptr": _dev(pe_ptr, i32), "pe_rec": _dev(pe_rec.ravel(), i32),
+                         "pe_coef": _dev(pe_coef.ravel(), f64)})
             self._keep_h.append(arrs)
             st = structs[s]
             ws = h.layout_for(self.hyb_panel[s])[0]

@@ -14,6 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import paper_1802_06263_b200._ref  # noqa: E402,F401  (puts sdmortar on the path)
 from sdmortar.collocation import build_tensor_grid  # noqa: E402
 from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402

@@ -8,6 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np
 from paper_1802_06263_b200.adapter import load_config
+import paper_1802_06263_b200._ref  # noqa: E402,F401  (puts sdmortar on the path)
 from sdmortar.collocation import CollocationGrid
 from paper_1802_06263_b200.interface import run_method
 z = np.load(os.path.join(ROOT, "tests", "golden", "cfg4_moments.npz"))

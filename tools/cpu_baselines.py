@@ -24,6 +24,7 @@ import numpy as np  # noqa: E402
 from threadpoolctl import threadpool_limits  # noqa: E402
 
 from oracle import s3_cpu  # noqa: E402
+import paper_1802_06263_b200._ref  # noqa: E402,F401  (puts sdmortar on the path)
 from sdmortar.collocation import build_tensor_grid  # noqa: E402
 from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 

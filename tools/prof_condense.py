@@ -10,7 +10,7 @@ import torch
 from paper_1802_06263_b200 import _lib
 
 _lib._lib = None
-_lib.load(os.path.join(os.path.dirname(_lib._SO), "_mfb_prof.so"))
+_lib.load(os.environ.get("MFB_PROF_LIBRARY") or os.path.join(os.path.dirname(_lib._SO), "_mfb_prof.so"))
 from paper_1802_06263_b200.adapter import load_config  # noqa: E402
 from paper_1802_06263_b200.interface import SweepEngine, get_plan  # noqa: E402
 
@@ -31,7 +31,7 @@ out = (ctypes.c_ulonglong * 16)()
 print("rc", _lib.load().mfb_debug_prof(out))
 v = np.array(out[:], dtype=np.float64)
 names = {1: "copy", 5: "branch(w0 panel)", 2: "wait", 3: "sbad", 4: "store+dmma",
-         13: "branch(w1 assembly)"}
+         13: "branch(w1 assembly)", 14: "  w1: zero + bar", 15: "  w1: entries"}
 tot = v[1] + v[5] + v[2] + v[3] + v[4]
 for i, nme in names.items():
     print(f"{nme:22s} {v[i] / 1e6:10.3f} Mcycles  {100 * v[i] / tot:5.1f}%")
