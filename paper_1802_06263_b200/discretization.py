@@ -143,7 +143,9 @@ class _TermTable:
         kind = np.concatenate(self.kind)
         c = np.concatenate(self.c)
         k = np.concatenate(self.k)
-        order = np.lexsort((cols, rows))          # stable: keeps insertion order
+        # one stable sort on the combined (row, col) key == lexsort((cols, rows))
+        key = (rows << 32) | cols
+        order = np.argsort(key, kind="stable")    # stable: keeps insertion order
         rows, cols, kind, c, k = rows[order], cols[order], kind[order], c[order], k[order]
         new = np.ones(len(rows), dtype=bool)
         new[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
