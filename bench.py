@@ -290,7 +290,8 @@ def run_reference(a):
 
     from paper_1802_06263_b200.adapter import load_config
     cfg_path = _config_path(a.config)
-    problem, grid, _ = load_config(cfg_path)
+    problem, grid, opts = load_config(cfg_path)
+    max_iter = opts.get("max_iter") or max(50, 10 * problem.space.n_dof)
     cores = len(os.sched_getaffinity(0))
     it_mean, it_src = _ref_iters_mean(a.config)
     if it_mean is None:
@@ -309,7 +310,8 @@ def run_reference(a):
         "warmup": a.warmup, "ms_per_step": 1000.0 * grid.n_real / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic collocation grid of the config)",
-        "config": {"workload": a.config, "n_real": grid.n_real, "tol": a.tol},
+        "config": {"workload": a.config, "n_real": grid.n_real, "tol": a.tol,
+                   "max_iter": int(max_iter)},
         "cpu_baseline": {"value": v, "unit": "realizations/s", "cores": cores,
                          "kind": "reference",
                          "sample": f"sdmortar itself (baseline/_ref, SuperLU + numpy) per step: "
@@ -524,14 +526,16 @@ def run_ours(a):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (deterministic Gauss-Hermite/Smolyak collocation of the "
                     "config; no dataset)",
-            "config": {"workload": a.config, "n_real": grid.n_real, "n_lambda": nl,
+            # the same dict as the reference arm's (the driver compares them);
+            # how this arm runs the workload is in workload_detail
+            "config": {"workload": a.config, "n_real": grid.n_real, "tol": a.tol,
+                       "max_iter": int(max_iter) if max_iter else int(max(50, 10 * nl))},
+            "workload_detail": {"n_lambda": nl,
                        "step": (f"one run_method S3 sweep over a batch of 1/{B} of the "
                                 f"collocation points (points k = b mod {B}, batches cycled; "
                                 f"KL, every basis, CG, moments)") if B > 1 else
                                "one run_method S3 sweep over the whole grid",
                        "batches": B, "points_per_step": n_tot / len(rows),
-                       "tol": a.tol,
-                       "max_iter": int(max_iter) if max_iter else int(max(50, 10 * nl)),
                        "parallelism": (f"x{ws} GPUs: each rank sweeps its own batch, no "
                                        f"collective") if ws > 1 else "single",
                        "l2": "flushed (256 MB write) before every step; the step's working "

@@ -205,14 +205,14 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         const double a = rr / pSp;
         part = 0.0;
         for (int d = tid; d < n_lambda; d += NT) {
-            const double rd = r[d] - a * Sp[d];
+            const double rd = __dsub_rn(r[d], __dmul_rn(a, Sp[d]));
             r[d] = rd;
             part += rd * rd;
         }
         CGP(4);
         const double rr_new = block_sum_alt(part, red2, rbuf);
         CGP(5);
-        for (int d = tid; d < n_lambda; d += NT) x[d] += a * p[d];   // p still this iteration's
+        for (int d = tid; d < n_lambda; d += NT) x[d] = __dadd_rn(x[d], __dmul_rn(a, p[d]));   // p still this iteration's
         const double rn = sqrt(rr_new);
         // rn now, rn / gnorm after the loop (keeps the division off the chain)
         if (tid == 0 && it <= hist_cap) hist[it - 1] = rn;
@@ -223,7 +223,7 @@ cg_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
         }
         const double beta = rr_new / rr;
         for (int d = tid; d < n_lambda; d += NT) {
-            const double pd = r[d] + beta * p[d];
+            const double pd = __dadd_rn(r[d], __dmul_rn(beta, p[d]));
             p[d] = pd;
             if (use_prow) {
                 prow[side0[d]] = pd;
@@ -333,9 +333,6 @@ cg_pair_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
     int status = MFB_CG_MAX_ITER, it_done = max_iter;
     for (int it = 1; it <= max_iter; ++it) {
         __syncthreads();                          // p (row space) of this iteration
-        // 1 / rr for this iteration's beta, computed here so that its latency
-        // overlaps the GEMV instead of sitting on the chain after rr_new
-        const double inv_rr = __drcp_rn(rr);
         const double *pr = prow + rd0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
@@ -355,9 +352,9 @@ cg_pair_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             break;
         }
         const double a = rr / pSp;
-        r -= a * sp;
+        r = __dsub_rn(r, __dmul_rn(a, sp));
         const double rr_new = block_sum_alt(head ? r * r : 0.0, red2, rbuf);
-        x += a * pd;
+        x = __dadd_rn(x, __dmul_rn(a, pd));
         const double rn = sqrt(rr_new);
         // rn now, rn / gnorm after the loop (keeps the division off the chain)
         if (tid == 0 && it <= hist_cap) hist[it - 1] = rn;
@@ -366,8 +363,8 @@ cg_pair_kernel(int n_lambda, int n_sub, const int *__restrict__ ndof,
             it_done = it;
             break;
         }
-        const double beta = rr_new * inv_rr;
-        pd = r + beta * pd;
+        const double beta = rr_new / rr;
+        pd = __dadd_rn(r, __dmul_rn(beta, pd));
         const double pv = __shfl_sync(0xffffffffu, pd, lane & ~1);
         if (row >= 0) prow[row] = pv;
         rr = rr_new;

@@ -394,13 +394,13 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                 const double2 p2 = P2[e], s2 = S2[e];
                 double2 x2 = X2[e], r2 = R2[e];
                 if (u0) {
-                    x2.x += a0 * p2.x;
-                    r2.x -= a0 * s2.x;
+                    x2.x = __dadd_rn(x2.x, __dmul_rn(a0, p2.x));
+                    r2.x = __dsub_rn(r2.x, __dmul_rn(a0, s2.x));
                     v0 += r2.x * r2.x;
                 }
                 if (u1) {
-                    x2.y += a1 * p2.y;
-                    r2.y -= a1 * s2.y;
+                    x2.y = __dadd_rn(x2.y, __dmul_rn(a1, p2.y));
+                    r2.y = __dsub_rn(r2.y, __dmul_rn(a1, s2.y));
                     v1 += r2.y * r2.y;
                 }
                 X2[e] = x2;
@@ -456,8 +456,8 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                 double2 p2 = P2[e];
                 if (c0 || c1) {
                     const double2 r2 = R2[e];
-                    if (c0) p2.x = r2.x + b0 * p2.x;
-                    if (c1) p2.y = r2.y + b1 * p2.y;
+                    if (c0) p2.x = __dadd_rn(r2.x, __dmul_rn(b0, p2.x));
+                    if (c1) p2.y = __dadd_rn(r2.y, __dmul_rn(b1, p2.y));
                     P2[e] = p2;
                 }
                 if (z0 || z1) {
