@@ -175,3 +175,25 @@ def test_run_method_raises_convergence_error_with_history(gpu):
     with pytest.raises(ConvergenceError) as e:
         run_method(problem, grid, method="S3", tol=1e-11, max_iter=3)
     assert len(e.value.residuals) == 3
+
+
+@pytest.mark.gpu
+def test_shape_limits_raise_instead_of_overrunning(gpu):
+    """The device kernels' fixed shape limits fail loudly:
+    a KL region with more than 64 terms (mfb_kl_realize_batched stages xi in
+    64 shared doubles) and a subdomain with more than 64 mortar dofs (the
+    moment kernels' block tiles) raise NativeLibraryError before any launch
+    that would overrun."""
+    from paper_1802_06263_b200.errors import NativeLibraryError
+    from paper_1802_06263_b200.interface import run_method
+    many_terms = {"kl_regions": [{"eta": [0.4, 0.4], "n_term": 72, "rect": [0.0, 0.0, 2.0, 1.0],
+                                  "selection": "largest", "sigma2": 0.5}],
+                  "collocation": {"kind": "tensor", "m": 1}}
+    _, problem, grid, _ = case_from_golden("darcy_twoblock", **many_terms)
+    with pytest.raises(NativeLibraryError, match="KL"):
+        run_method(problem, grid, method="S3", tol=1e-9)
+    wide = {"mortars": {"allow_fine": True, "dd": 72, "degree": 0, "per_interface": {}}}
+    _, problem, grid, _ = case_from_golden("darcy_twoblock", **wide)
+    assert max(len(problem.space.sub_dofs(problem.layout, s)) for s in range(2)) > 64
+    with pytest.raises(NativeLibraryError, match="mortar dofs"):
+        run_method(problem, grid, method="S3", tol=1e-9)
