@@ -291,7 +291,26 @@ int mfb_cg_batched(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr,
  * hist_cap entries, as mfb_cg_cluster's (res_hist = the pool). trec[12 *
  * n_tasks]: per task its run (as tasks[]), per side nd | (region + 1) << 16,
  * dof_ptr, packed strip base (loc 0) and packed block size.
+ * chunk_ptr[n_chunks + 1] (device, or NULL): a CTA claims whole chunks of
+ * <= 8 consecutive points, [chunk_ptr[c], chunk_ptr[c + 1]), and feeds them
+ * to its slots as they free up (the caller orders the points so that a
+ * chunk's points share local realizations); NULL: one point per claim.
+ * list_cap > 0: S p streamed over per-warp pass lists of list_cap entries in
+ * shared memory (a rolling window of A fragments in flight across pass and
+ * task boundaries; needs n_rows < 65536, ndof <= 248 and list_cap >= the
+ * largest per-warp count of passes + tasks + 1 with 8 passes per Darcy
+ * side); 0: the task loop. Dynamic shared memory: mfb_cg_multi_smem(...)
+ * + 8 KB of static tables must fit in 227 KB. Strips of the packed pool hold
+ * an even number of fragments (zero-padded).
+ * dm_tab[n_dm] (device): the dof list as p offsets, d * 8 + ((d & 2) << 1) for
+ * mortar dof d (p is kept [dof][slot] with the slot halves of every other
+ * dof pair exchanged: conflict-free B operands). list_cap == 0: dm_tab[r]
+ * for row r of dof_map (n_dm >= n_rows + 8, zero padding) and packed in
+ * layout 0; list_cap > 0: per subdomain its columns padded to a multiple of
+ * 8 and pair-interleaved (column 8 k + 4 h + q at 8 k + 2 q + h), the
+ * subdomain's offset in trec's dof_ptr fields, and packed in layout 1.
  */
+long long mfb_cg_multi_smem(int n_lambda, int n_dm, int list_cap);
 long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta);
 int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int *dof_ptr,
                  const int *dof_map, const int *region, int n_regions,
@@ -302,7 +321,8 @@ int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof, const int
                  const int *sides, const double *packed, const long long *pk_base,
                  const int *pk_size, int n_cta, double *scratch, int *counter, int *seg_tab,
                  int max_segs, long long seg_cap, int *seg_counter, const int *trec,
-                 void *stream);
+                 const int *chunk_ptr, int n_chunks, int list_cap, const int *dm_tab,
+                 int n_dm, void *stream);
 
 /*
  * Same contract again, on thread-block clusters of C CTAs (C <= 8) holding
@@ -363,11 +383,14 @@ int mfb_basis_apply(int n_lambda, int n_sub, const int *ndof, const int *dof_ptr
  * n_loc[sid] the strip's rows of block (sid, l) (column-major at blk_base[sid]
  * + l * ndof^2) are written as MMA A fragments: fragment t of lane (g, q) =
  * B[row0 + g][4 t + q] at packed[pk_base[sid] + l * pk_size[sid] + offset +
- * 32 t + lane], zero-padded. max_loc = max n_loc.
+ * 32 t + lane], zero-padded to an even fragment count (layout 0), or with
+ * the lane's fragments 2 k, 2 k + 1 adjacent at 64 k + 2 lane (layout 1, the
+ * streamed mfb_cg_multi). max_loc = max n_loc.
  */
 int mfb_cg_pack(int n_strips, const int *strips, const int *ndof, const int *n_loc,
                 int max_loc, const long long *blk_base, const long long *pk_base,
-                const int *pk_size, const double *blocks, double *packed, void *stream);
+                const int *pk_size, const double *blocks, double *packed, int layout,
+                void *stream);
 
 /*
  * Shifted sufficient statistics per group (one subdomain x one local

@@ -68,10 +68,11 @@ _SIGS = {
                         _ll, _p, _p, _p], _i),
     "mfb_s1_fields": ([_p, _i, _p, _p, _p, _ll, _p, _p, _p, _p, _p], _i),
     "mfb_cg_multi_scratch_doubles": ([_i, _i], _ll),
+    "mfb_cg_multi_smem": ([_i, _i, _i], _ll),
     "mfb_cg_multi": ([_i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
                       _p, _p, _p, _p, _i, _p, _p, _i, _p, _p, _p, _p, _i, _p, _p, _p, _i, _ll,
-                      _p, _p, _p], _i),
-    "mfb_cg_pack": ([_i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _p], _i),
+                      _p, _p, _p, _i, _i, _p, _i, _p], _i),
+    "mfb_cg_pack": ([_i, _p, _p, _p, _i, _p, _p, _p, _p, _p, _i, _p], _i),
     "mfb_basis_apply": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_debug_cluster": ([_i], _i),
     "mfb_debug_multi": ([_i, _p], _i),

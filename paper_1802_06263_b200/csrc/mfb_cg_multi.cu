@@ -44,6 +44,7 @@ constexpr int MNT = 512;         // threads per CTA
 constexpr int MW = MNT / 32;
 constexpr int MREG = 64;         // KL regions cached per slot
 constexpr int MPF = 8;           // A fragments prefetched per side (32 columns)
+constexpr int VB_STREAM = 3;     // vector phases: elements per thread with loads in flight together
 
 struct CgMultiArgs {
     int n_lambda, n_sub, n_regions, n_real, k0, n_pts, max_iter, hist_cap, n_tasks;
@@ -62,7 +63,61 @@ struct CgMultiArgs {
     int max_segs;
     long long seg_cap;
     int *iters, *status, *next;
+    const int *chunk_ptr;          // claims of <= MP consecutive points (NULL: one point per claim)
+    int n_chunks;
+    int list_cap;                  // pass-list entries per warp (streamed S p); 0: task loop
+    const int *dm_tab;             // the dof list as the kernel reads it (p offsets, see below)
+    int n_dm;
 };
+
+// p of the MP slots lives in shared memory as [dof][slot], 64 bytes per dof,
+// with the two slot halves of every other dof PAIR exchanged: slot s of dof d
+// at double d * 8 + (s ^ ((d & 2) << 1)). The B operand of an MMA reads, per
+// half warp, slots 0-3 (4-7) of four consecutive dofs -- 32 bytes at a
+// 64-byte stride, a two-way bank conflict in the plain layout; exchanged,
+// the four dofs cover all 32 banks. The dof lists hold d * 8 + ((d & 2) << 1),
+// so a lane's address is list ^ g; the vector phases see a permutation
+// within each dof's 64 bytes (pidx).
+__device__ __forceinline__ int pidx(int e) { return e ^ ((e >> 2) & 2); }
+
+// ---- r in tensor memory -----------------------------------------------------
+// The vector phases and phase A's A stream share one limit, the L2 -> SM
+// bandwidth (x, r, S p round trips: 1 MB of the 3.6 MB a CTA moves per
+// iteration at cfg4). r is private to the thread that updates it -- element
+// e = tid + k * MNT in every phase -- so it lives in the SM's tensor memory
+// (256 KB, idle in an FP64 kernel) instead of the global scratch: warp w owns
+// lanes 32 (w % 4) .. + 31 (the quadrant its tcgen05.ld / .st may touch) and
+// 4 columns (one double2) per element at column 4 KA (w / 4) + 4 k.
+__device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[1]) {
+    unsigned a, b, c, d;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(ta) : "memory");
+    v[0] = make_double2(__hiloint2double(b, a), __hiloint2double(d, c));
+}
+__device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[3]) {
+    unsigned r[12];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%12];\n"
+                 "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%13];\n"
+                 "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8, %9, %10, %11}, [%14];\n"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
+                 : "r"(ta), "r"(ta + 4), "r"(ta + 8) : "memory");
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        v[k] = make_double2(__hiloint2double(r[4 * k + 1], r[4 * k]),
+                            __hiloint2double(r[4 * k + 3], r[4 * k + 2]));
+}
+__device__ __forceinline__ void tm_st(unsigned ta, double2 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
+                 :: "r"(ta), "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)),
+                    "r"(__double2loint(v.y)), "r"(__double2hiint(v.y)) : "memory");
+}
+__device__ __forceinline__ void tm_st_wait() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -120,7 +175,7 @@ __device__ __forceinline__ void strip_pass(const double *__restrict__ Sl, const 
             if (NT4 > 0 ? (t0 + t < NT4) : (t0 + t < nt4)) {
                 af[t] = __ldg(Sl + 32 * (t0 + t));
                 const int c = 4 * (t0 + t) + q;
-                dv[t] = (NT4 > 0 || c < nd) ? dm[c] + g : g;
+                dv[t] = (NT4 > 0 || c < nd) ? dm[c] ^ g : g;
             }
         }
 #pragma unroll
@@ -163,7 +218,9 @@ __device__ __forceinline__ void side_mma(const double *__restrict__ packed, int 
         case 16: strip_pass<4>(Sl, dm, nd, ps, m, d0, d1); break;
         case 24: strip_pass<6>(Sl, dm, nd, ps, m, d0, d1); break;
         case 32: strip_pass<8>(Sl, dm, nd, ps, m, d0, d1); break;
+        case 40: strip_pass<10>(Sl, dm, nd, ps, m, d0, d1); break;
         case 48: strip_pass<12>(Sl, dm, nd, ps, m, d0, d1); break;
+        case 56: strip_pass<14>(Sl, dm, nd, ps, m, d0, d1); break;
         case 64: strip_pass<16>(Sl, dm, nd, ps, m, d0, d1); break;
         default: strip_pass<0>(Sl, dm, nd, ps, m, d0, d1); break;
         }
@@ -177,17 +234,155 @@ __global__ void cg_pack_kernel(const int4 *__restrict__ strips, const int *__res
                                const int *__restrict__ n_loc, const long long *__restrict__ blk_base,
                                const long long *__restrict__ pk_base,
                                const int *__restrict__ pk_size, const double *__restrict__ blocks,
-                               double *__restrict__ packed) {
+                               double *__restrict__ packed, int layout) {
     const int4 S = strips[blockIdx.x];
-    const int sid = S.x, nd = ndof[sid], nt4 = (nd + 3) >> 2;
+    const int sid = S.x, nd = ndof[sid];
+    const int nt4 = (((nd + 3) >> 2) + 1) & ~1;      // strips hold an even number of fragments
     for (int l = blockIdx.y; l < n_loc[sid]; l += gridDim.y) {
         const double *B = blocks + blk_base[sid] + (long long)l * nd * nd;
         double *D = packed + pk_base[sid] + (long long)l * pk_size[sid] + S.w;
         for (int e = threadIdx.x; e < 32 * nt4; e += blockDim.x) {
             const int lane = e & 31, g = lane >> 2, c = 4 * (e >> 5) + (lane & 3);
-            D[e] = (g < S.z && c < nd) ? B[(long long)c * nd + S.y + g] : 0.0;
+            // layout 1: the lane's fragments 2 k, 2 k + 1 adjacent (one 16-byte load)
+            const int dst = layout ? 64 * (e >> 6) + 2 * lane + ((e >> 5) & 1) : e;
+            D[dst] = (g < S.z && c < nd) ? B[(long long)c * nd + S.y + g] : 0.0;
         }
     }
+}
+
+
+// ---- streamed S p --------------------------------------------------------
+// The task loop above issues a pass's A loads and then waits a full L2
+// round trip before its first MMA: with 16 warps x 8 fragments the loads in
+// flight average about half of what the 32 KB could be. The streamed form
+// keeps a ROLLING window instead: every warp walks a flat list of its passes
+// (rebuilt in shared memory when the slots' local realizations change), and
+// each step -- two fragments, the even / odd accumulator chains -- multiplies
+// the two oldest fragments of an 8-fragment register window and at once
+// re-issues their slots for the step four ahead, across pass and task
+// boundaries. Same MMA sequence per (slot, row) as the task loop: same bits.
+//
+// list entry (int2): x = offset of the pass's strip in fragment pairs (packed
+// + 64 x), y = steps | side << 5 | task end << 6 | list end << 7 | slot mask
+// << 8 | the block's offset in the (padded, pair-interleaved) dof list << 16. A task-end entry is followed by
+// the task's record {first dof, rows | has upper << 8}.
+constexpr int PL_SIDE = 1 << 5, PL_TEND = 1 << 6, PL_END = 1 << 7;
+
+__device__ __forceinline__ void build_pass_list(const CgMultiArgs &A, int2 *L, int run,
+                                                const int *g_cnt, const int *g_loc,
+                                                const int *g_mask) {
+    int n = 0;
+    for (int ti = threadIdx.x >> 5; ti < A.n_tasks; ti += MW) {
+        const int4 T = __ldg(A.trec + 3 * ti), U = __ldg(A.trec + 3 * ti + 1),
+                   V = __ldg(A.trec + 3 * ti + 2);
+        const int j = ((T.w >> 12) & 0xfff) - 1, Rr = T.w >> 24;
+        int last = -1;
+        for (int side = 0; side < (j >= 0 ? 2 : 1); ++side) {
+            const int ndr = side ? U.y : U.x, dmo = side ? U.w : U.z;
+            const int pkb = side ? V.y : V.x, psz = side ? V.w : V.z;
+            const int nd = ndr & 0xffff, reg = (ndr >> 16) - 1;
+            const int steps = (((nd + 3) >> 2) + 1) >> 1;
+            const int ngrp = reg < 0 ? 1 : g_cnt[reg];
+            for (int gi = 0; gi < ngrp; ++gi) {
+                const int m = reg < 0 ? 0xff : g_mask[reg * MP + gi];
+                if (!(m & run)) continue;
+                const int l = reg < 0 ? 0 : g_loc[reg * MP + gi];
+                last = n;
+                L[n++] = make_int2((int)(((long long)pkb + (long long)l * psz) >> 6),
+                                   (int)((unsigned)steps | (side ? PL_SIDE : 0) | (m << 8) |
+                                         ((unsigned)dmo << 16)));
+            }
+        }
+        if (last >= 0) {
+            L[last].y |= PL_TEND;
+            L[n++] = make_int2(T.x, Rr | (j >= 0 ? 256 : 0));
+        }
+    }
+    L[n] = make_int2(0, PL_END);
+}
+
+// One warp's S p over its pass list; returns this thread's p . S p partials
+// (slots 2 q, 2 q + 1) in v0 / v1. The packed strips are pair-interleaved
+// (mfb_cg_pack layout 1: fragments 2 k, 2 k + 1 of lane l adjacent, one
+// 16-byte load per step) and so is the dof list (the two fragments' rows of
+// lane q adjacent, one 8-byte load per step).
+__device__ __forceinline__ void stream_passes(const CgMultiArgs &A, const int2 *L, int run,
+                                              const double *__restrict__ ps, const int *sdm,
+                                              double2 *__restrict__ S2, const double2 *P2,
+                                              double &v0, double &v1) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const double2 *__restrict__ pk = reinterpret_cast<const double2 *>(A.packed) + lane;
+    const int2 *dmq = reinterpret_cast<const int2 *>(sdm) + q;
+    int iL = 0, iC = 0;
+    int2 eC = L[0];
+    if (eC.y & PL_END) return;
+    int yL = eC.y, nL = yL & 31, nC = nL;
+    const double2 *pL = pk + ((long long)eC.x << 5);
+    const int2 *dmC = dmq + ((unsigned)eC.y >> 17);
+    double2 af[4];
+    double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0, lo0 = 0.0, lo1 = 0.0, up0 = 0.0, up1 = 0.0;
+    // the list walk is a loop so that it stays a (rarely taken) branch
+    // instead of a dozen predicated instructions in every step
+#define PL_ISSUE(s)                                                      \
+    do {                                                                 \
+        af[s] = __ldg(pL);                                               \
+        pL += 32;                                                        \
+        --nL;                                                            \
+        while (nL == 0) {                                                \
+            iL += 1 + ((yL >> 6) & 1);                                   \
+            const int2 eN = L[iL];                                       \
+            yL = eN.y;                                                   \
+            nL = (yL & PL_END) ? -1 : (yL & 31);                         \
+            pL = pk + ((long long)eN.x << 5);                            \
+        }                                                                \
+    } while (0)
+    PL_ISSUE(0); PL_ISSUE(1); PL_ISSUE(2); PL_ISSUE(3);
+    for (;;) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int2 dd = *dmC;
+            dmC += 4;
+            const double b0 = ps[dd.x ^ g], b1 = ps[dd.y ^ g];
+            dmma884(e0, e1, af[s].x, b0);
+            dmma884(o0, o1, af[s].y, b1);
+            PL_ISSUE(s);
+            if (--nC == 0) {
+                // a column of B only feeds its own slot: the group's members
+                // take the products, the other slots keep their accumulators
+                const int m = (eC.y >> 8) & run;
+                const double t0 = e0 + o0, t1 = e1 + o1;
+                if (eC.y & PL_SIDE) {
+                    if ((m >> (2 * q)) & 1) up0 += t0;
+                    if ((m >> (2 * q + 1)) & 1) up1 += t1;
+                } else {
+                    if ((m >> (2 * q)) & 1) lo0 += t0;
+                    if ((m >> (2 * q + 1)) & 1) lo1 += t1;
+                }
+                e0 = e1 = o0 = o1 = 0.0;
+                if (eC.y & PL_TEND) {
+                    const int2 rec = L[iC + 1];
+                    iC += 2;
+                    if (g < (rec.y & 0xff)) {
+                        const double2 sp = (rec.y & 256) ? make_double2(lo0 + up0, lo1 + up1)
+                                                         : make_double2(lo0, lo1);
+                        const int e = (rec.x + g) * (MP / 2) + q;
+                        S2[e] = sp;
+                        const double2 pp = P2[pidx(e)];
+                        v0 += pp.x * sp.x;
+                        v1 += pp.y * sp.y;
+                    }
+                    lo0 = lo1 = up0 = up1 = 0.0;
+                } else {
+                    iC += 1;
+                }
+                eC = L[iC];
+                if (eC.y & PL_END) return;
+                nC = eC.y & 31;
+                dmC = dmq + ((unsigned)eC.y >> 17);
+            }
+        }
+    }
+#undef PL_ISSUE
 }
 
 enum { SLOT_RUN = 0, SLOT_NEW = 1, SLOT_DONE = 2 };
@@ -211,6 +406,7 @@ __device__ long long g_multi_prof[148 * 8];
 #define MP_PROF 0
 #endif
 
+template <bool STREAM>
 __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     extern __shared__ double ps[];                 // [n_lambda][MP], then the dof lists
     __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP], s_seg[MP];
@@ -218,7 +414,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     __shared__ int s_loc[MREG * MP];
     __shared__ int s_gcnt[MREG], s_gloc[MREG * MP], s_gmask[MREG * MP];
     __shared__ double s_red[MW][MP];
-    __shared__ int s_any;
+    __shared__ int s_any, s_q0, s_q1;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int n = A.n_lambda;
     const int npair = n * (MP / 2);
@@ -228,13 +424,32 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     double *Ss = Rs + (long long)n * MP;
     // x, r, S p: disjoint thirds of this CTA's scratch
     double2 *__restrict__ X2 = reinterpret_cast<double2 *>(Xs);
-    double2 *__restrict__ R2 = reinterpret_cast<double2 *>(Rs);
     double2 *__restrict__ S2 = reinterpret_cast<double2 *>(Ss);
     double2 *P2 = reinterpret_cast<double2 *>(ps);
-    int *sdm = reinterpret_cast<int *>(ps + (long long)n * MP);   // dof_map * MP
+    int *sdm = reinterpret_cast<int *>(ps + (long long)n * MP);   // the dof list (A.dm_tab)
+    int2 *plist = reinterpret_cast<int2 *>(sdm + ((A.n_dm + 1) & ~1)) +
+                  (long long)wid * A.list_cap;        // this warp's pass list (STREAM)
+    int prev_run = -1;
+    constexpr int VB = STREAM ? VB_STREAM : 1;     // (the task loop leaves no registers for it)
+    // tensor memory for r: all 512 columns (one CTA per SM)
+    __shared__ unsigned s_tmem;
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                     :: "r"((unsigned)__cvta_generic_to_shared(&s_tmem)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // elements per thread, uniform over the warp (lanes past npair idle), and
+    // the warp's column range
+    const int kw = (npair - (wid << 5) + MNT - 1) / MNT;
+    const int ka = ((npair + MNT - 1) / MNT + VB - 1) / VB * VB;
+    const unsigned tr = s_tmem + ((unsigned)(32 * (wid & 3)) << 16) + (unsigned)((wid >> 2) * 4 * ka);
     if (tid < MP) { s_k[tid] = -1; s_state[tid] = SLOT_DONE; }
+    if (tid == 0) { s_q0 = 0; s_q1 = 0; }
     for (int e = tid; e < n * MP; e += MNT) ps[e] = 0.0;
-    for (int e = tid; e < A.dof_ptr[A.n_sub]; e += MNT) sdm[e] = A.dof_map[e] * MP;
+    for (int e = tid; e < A.n_dm; e += MNT) sdm[e] = A.dm_tab[e];
 
 #if MP_PROF
     const int dbg = g_multi_dbg;
@@ -244,17 +459,30 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     for (;;) {
         __syncthreads();
         // ---- refill empty slots from the global work counter --------------
+        // A claim is a chunk of <= MP consecutive points of the sweep order
+        // (the host groups points that share local realizations, so a CTA's
+        // slots visit few distinct Darcy blocks per region); the chunk's
+        // points go to this CTA's slots as they free up.
         if (tid == 0) {
-            int any = 0;
+            int any = 0, q0 = s_q0, q1 = s_q1;
             for (int s = 0; s < MP; ++s) {
                 if (s_k[s] == -1) {
-                    const int t = atomicAdd(A.next, 1);
-                    s_k[s] = t < A.n_pts ? t : -2;
-                    s_state[s] = t < A.n_pts ? SLOT_NEW : SLOT_DONE;
+                    if (q0 == q1 && q1 >= 0) {
+                        const int c = atomicAdd(A.next, 1);
+                        if (A.chunk_ptr) {
+                            if (c < A.n_chunks) { q0 = A.chunk_ptr[c]; q1 = A.chunk_ptr[c + 1]; }
+                            else q0 = q1 = -1;
+                        } else if (c < A.n_pts) { q0 = c; q1 = c + 1; }
+                        else q0 = q1 = -1;
+                    }
+                    const int t = q0 < q1 ? q0++ : -2;
+                    s_k[s] = t;
+                    s_state[s] = t >= 0 ? SLOT_NEW : SLOT_DONE;
                     s_it[s] = 0;
                 }
                 any |= s_k[s] >= 0;
             }
+            s_q0 = q0; s_q1 = q1;
             s_any = any;
         }
         __syncthreads();
@@ -291,35 +519,41 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                 s_gcnt[r] = cnt;
             }
             // g = 0 + h_lower + h_upper (mortar.jump of the bar traces), x = 0
-            for (int e = tid; e < npair; e += MNT) {
-                if (!(f0 || f1)) break;
-                const int d = e >> 2;
-                const int4 sd = A.sides[d];
-                const int ri = A.region[sd.x], rj = sd.z >= 0 ? A.region[sd.z] : -1;
-                double gv[2] = {0.0, 0.0};
+            for (int k = 0; k < kw; ++k) {
+                const int e = tid + k * MNT;
+                double2 rv[1];
+                tm_ld(tr + 4 * k, rv);           // (the whole warp: .sync.aligned)
+                if ((f0 || f1) && e < npair) {
+                    const int d = e >> 2;
+                    const int4 sd = A.sides[d];
+                    const int ri = A.region[sd.x], rj = sd.z >= 0 ? A.region[sd.z] : -1;
+                    double gv[2] = {0.0, 0.0};
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int s = sq + h;
-                    if (!((fresh >> s) & 1)) continue;   // s_loc is only set for fresh slots
-                    const int li = ri < 0 ? 0 : s_loc[ri * MP + s];
-                    double gg = A.hbar[A.h_base[sd.x] + (long long)li * A.ndof[sd.x] + sd.y];
-                    if (sd.z >= 0) {
-                        const int lj = rj < 0 ? 0 : s_loc[rj * MP + s];
-                        gg = gg + A.hbar[A.h_base[sd.z] + (long long)lj * A.ndof[sd.z] + sd.w];
+                    for (int h = 0; h < 2; ++h) {
+                        const int s = sq + h;
+                        if (!((fresh >> s) & 1)) continue;   // s_loc is only set for fresh slots
+                        const int li = ri < 0 ? 0 : s_loc[ri * MP + s];
+                        double gg = A.hbar[A.h_base[sd.x] + (long long)li * A.ndof[sd.x] + sd.y];
+                        if (sd.z >= 0) {
+                            const int lj = rj < 0 ? 0 : s_loc[rj * MP + s];
+                            gg = gg + A.hbar[A.h_base[sd.z] + (long long)lj * A.ndof[sd.z] + sd.w];
+                        }
+                        gv[h] = gg;
                     }
-                    gv[h] = gg;
+                    double2 p2 = P2[pidx(e)], x2 = X2[e];
+                    if (f0) {
+                        p2.x = gv[0]; rv[0].x = gv[0]; x2.x = 0.0; v0 += gv[0] * gv[0];
+                        if (A.g) A.g[(long long)s_k[sq] * n + d] = gv[0];
+                    }
+                    if (f1) {
+                        p2.y = gv[1]; rv[0].y = gv[1]; x2.y = 0.0; v1 += gv[1] * gv[1];
+                        if (A.g) A.g[(long long)s_k[sq + 1] * n + d] = gv[1];
+                    }
+                    P2[pidx(e)] = p2; X2[e] = x2;
                 }
-                double2 p2 = P2[e], r2 = R2[e], x2 = X2[e];
-                if (f0) {
-                    p2.x = gv[0]; r2.x = gv[0]; x2.x = 0.0; v0 += gv[0] * gv[0];
-                    if (A.g) A.g[(long long)s_k[sq] * n + d] = gv[0];
-                }
-                if (f1) {
-                    p2.y = gv[1]; r2.y = gv[1]; x2.y = 0.0; v1 += gv[1] * gv[1];
-                    if (A.g) A.g[(long long)s_k[sq + 1] * n + d] = gv[1];
-                }
-                P2[e] = p2; R2[e] = r2; X2[e] = x2;
+                tm_st(tr + 4 * k, rv[0]);
             }
+            tm_st_wait();
             reduce_pairs(v0, v1, s_red, s_tot);
             if (tid < MP && ((fresh >> tid) & 1)) {
                 s_rr[tid] = s_tot[tid];
@@ -339,6 +573,16 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
 
         // ---- Phase A: S p on the tensor cores; p.S p --------------------------
         v0 = 0.0; v1 = 0.0;
+        if (STREAM) {
+            if (run) {
+                if (fresh || run != prev_run) {     // the slots' blocks changed
+                    if (lane == 0) build_pass_list(A, plist, run, s_gcnt, s_gloc, s_gmask);
+                    __syncwarp();
+                }
+                stream_passes(A, plist, run, ps, sdm, S2, P2, v0, v1);
+            }
+            prev_run = run;
+        } else
         if (run) {
             const int g8 = lane >> 2;
             // task records {run}{nd | region + 1 << 16 per side, dof_ptr per side}
@@ -361,7 +605,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                                               : make_double2(lo0, lo1);
                     const int e = d * (MP / 2) + (lane & 3);
                     S2[e] = sp;
-                    const double2 pp = P2[e];
+                    const double2 pp = P2[pidx(e)];
                     v0 += pp.x * sp.x;
                     v1 += pp.y * sp.y;
                 }
@@ -388,24 +632,39 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
         // ---- Phase B: x += a p, r -= a S p, r.r (elementwise) -----------------
         v0 = 0.0; v1 = 0.0;
         const bool u0 = (upd >> sq) & 1, u1 = (upd >> (sq + 1)) & 1;
-        if (u0 || u1) {
+        if (upd) {                        // (uniform: r moves through tensor memory)
             const double a0 = s_a[sq], a1 = s_a[sq + 1];
-            for (int e = tid; e < npair; e += MNT) {
-                const double2 p2 = P2[e], s2 = S2[e];
-                double2 x2 = X2[e], r2 = R2[e];
-                if (u0) {
-                    x2.x = __dadd_rn(x2.x, __dmul_rn(a0, p2.x));
-                    r2.x = __dsub_rn(r2.x, __dmul_rn(a0, s2.x));
-                    v0 += r2.x * r2.x;
+            const bool act = u0 || u1;
+            // VB elements per trip, their scratch loads issued together
+            for (int k0 = 0; k0 < kw; k0 += VB) {
+                double2 s2[VB], x2[VB], r2[VB];
+                tm_ld(tr + 4 * k0, r2);
+#pragma unroll
+                for (int k = 0; k < VB; ++k) {
+                    const int e = tid + (k0 + k) * MNT;
+                    if (act && e < npair) { s2[k] = S2[e]; x2[k] = X2[e]; }
                 }
-                if (u1) {
-                    x2.y = __dadd_rn(x2.y, __dmul_rn(a1, p2.y));
-                    r2.y = __dsub_rn(r2.y, __dmul_rn(a1, s2.y));
-                    v1 += r2.y * r2.y;
+#pragma unroll
+                for (int k = 0; k < VB; ++k) {
+                    const int e = tid + (k0 + k) * MNT;
+                    if (act && e < npair) {
+                        const double2 p2 = P2[pidx(e)];
+                        if (u0) {
+                            x2[k].x = __dadd_rn(x2[k].x, __dmul_rn(a0, p2.x));
+                            r2[k].x = __dsub_rn(r2[k].x, __dmul_rn(a0, s2[k].x));
+                            v0 += r2[k].x * r2[k].x;
+                        }
+                        if (u1) {
+                            x2[k].y = __dadd_rn(x2[k].y, __dmul_rn(a1, p2.y));
+                            r2[k].y = __dsub_rn(r2[k].y, __dmul_rn(a1, s2[k].y));
+                            v1 += r2[k].y * r2[k].y;
+                        }
+                        X2[e] = x2[k];
+                    }
+                    tm_st(tr + 4 * (k0 + k), r2[k]);
                 }
-                X2[e] = x2;
-                R2[e] = r2;
             }
+            tm_st_wait();
         }
         MP_T(3);
         reduce_pairs(v0, v1, s_red, s_tot);
@@ -449,18 +708,26 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
         }
         const bool c0 = (cont >> sq) & 1, c1 = (cont >> (sq + 1)) & 1;
         const bool z0 = (fin >> sq) & 1, z1 = (fin >> (sq + 1)) & 1;
-        if (c0 || c1 || z0 || z1) {
+        if (cont || fin) {
             const double b0 = s_b[sq], b1 = s_b[sq + 1];
-            for (int e = tid; e < npair; e += MNT) {
-                const int d = e >> 2;
-                double2 p2 = P2[e];
-                if (c0 || c1) {
-                    const double2 r2 = R2[e];
-                    if (c0) p2.x = __dadd_rn(r2.x, __dmul_rn(b0, p2.x));
-                    if (c1) p2.y = __dadd_rn(r2.y, __dmul_rn(b1, p2.y));
-                    P2[e] = p2;
+            if (cont) {                   // (uniform)
+                for (int k0 = 0; k0 < kw; k0 += VB) {
+                    double2 r2[VB];
+                    tm_ld(tr + 4 * k0, r2);
+#pragma unroll
+                    for (int k = 0; k < VB; ++k) {
+                        const int e = tid + (k0 + k) * MNT;
+                        if (e >= npair || !(c0 || c1)) continue;
+                        double2 p2 = P2[pidx(e)];
+                        if (c0) p2.x = __dadd_rn(r2[k].x, __dmul_rn(b0, p2.x));
+                        if (c1) p2.y = __dadd_rn(r2[k].y, __dmul_rn(b1, p2.y));
+                        P2[pidx(e)] = p2;
+                    }
                 }
-                if (z0 || z1) {
+            }
+            if (z0 || z1) {
+                for (int e = tid; e < npair; e += MNT) {
+                    const int d = e >> 2;
                     const double2 x2 = X2[e];
                     if (z0)
                         A.lam[(long long)s_k[sq] * n + d] =
@@ -486,6 +753,11 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     if (dbg && threadIdx.x == 0 && blockIdx.x < 148)
         for (int i = 0; i < 8; ++i) g_multi_prof[blockIdx.x * 8 + i] = pt[i];
 #endif
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;"
+                     :: "r"(s_tmem) : "memory");
 }
 
 }  // namespace
@@ -495,6 +767,14 @@ extern "C" int mfb_debug_multi(int on, long long *out) {
         return cudaMemcpyFromSymbol(out, g_multi_prof, sizeof(long long) * 148 * 8) ==
                        cudaSuccess ? 0 : 2;
     return cudaMemcpyToSymbol(g_multi_dbg, &on, sizeof(int)) == cudaSuccess ? 0 : 2;
+}
+
+// dynamic shared memory: p of the MP slots, the dof list (n_dm entries) and,
+// streamed, MW pass lists of list_cap entries
+extern "C" long long mfb_cg_multi_smem(int n_lambda, int n_dm, int list_cap) {
+    return (long long)n_lambda * MP * sizeof(double) +
+           (long long)((n_dm + 1) & ~1) * sizeof(int) +
+           (long long)MW * list_cap * sizeof(int2);
 }
 
 extern "C" long long mfb_cg_multi_scratch_doubles(int n_lambda, int n_cta) {
@@ -512,15 +792,21 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
                             const int *sides, const double *packed, const long long *pk_base,
                             const int *pk_size, int n_cta, double *scratch, int *counter,
                             int *seg_tab, int max_segs, long long seg_cap, int *seg_counter,
-                            const int *trec, void *stream) {
+                            const int *trec, const int *chunk_ptr, int n_chunks, int list_cap,
+                            const int *dm_tab, int n_dm, void *stream) {
     if (n_pts <= 0) return n_pts == 0 ? MFB_OK : MFB_ERR_ARG;
     if (n_lambda <= 0 || n_sub <= 0 || n_sub >= 4095 || n_rows <= 0 || n_regions > MREG || n_cta <= 0 ||
-        max_iter < 1 || hist_cap < 1 || n_tasks <= 0 ||
+        max_iter < 1 || hist_cap < 1 || n_tasks <= 0 || (chunk_ptr && n_chunks <= 0) ||
+        list_cap < 0 || !dm_tab || n_dm < n_rows || (list_cap > 0 && n_dm >= 65536) ||
         (seg_tab && (max_segs < (max_iter + hist_cap - 1) / hist_cap || !seg_counter)))
         return MFB_ERR_ARG;
-    const size_t smem = (size_t)n_lambda * MP * sizeof(double) + (size_t)n_rows * sizeof(int);
-    if (smem > 220 * 1024) return MFB_ERR_SMEM;
-    if (cudaFuncSetAttribute(cg_multi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // r of the slots in tensor memory: 16 columns per element a thread owns
+    if (((n_lambda * (MP / 2) + MNT - 1) / MNT + VB_STREAM - 1) / VB_STREAM * VB_STREAM > 32)
+        return MFB_ERR_SMEM;
+    const size_t smem = mfb_cg_multi_smem(n_lambda, n_dm, list_cap);
+    if (smem + 8192 > 227 * 1024) return MFB_ERR_SMEM;    // + the kernel's static tables
+    if (cudaFuncSetAttribute(list_cap ? cg_multi_kernel<true> : cg_multi_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return MFB_ERR_SMEM;
     cudaStream_t st = mfb_stream(stream);
@@ -539,10 +825,15 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
     A.packed = packed; A.pk_base = pk_base; A.pk_size = pk_size;
     A.lam = lam; A.res_hist = res_hist; A.g = g; A.scratch = scratch;
     A.iters = iters; A.status = status; A.next = counter;
+    A.chunk_ptr = chunk_ptr; A.n_chunks = n_chunks;
     A.seg_tab = seg_tab; A.seg_next = seg_counter; A.max_segs = max_segs; A.seg_cap = seg_cap;
     if (seg_tab && cudaMemsetAsync(seg_counter, 0, sizeof(int), st) != cudaSuccess)
         return MFB_ERR_LAUNCH;
-    cg_multi_kernel<<<n_cta, MNT, smem, st>>>(A);
+    A.list_cap = list_cap; A.dm_tab = dm_tab; A.n_dm = n_dm;
+    if (list_cap)
+        cg_multi_kernel<true><<<n_cta, MNT, smem, st>>>(A);
+    else
+        cg_multi_kernel<false><<<n_cta, MNT, smem, st>>>(A);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }
@@ -550,13 +841,13 @@ extern "C" int mfb_cg_multi(int n_lambda, int n_sub, int n_rows, const int *ndof
 extern "C" int mfb_cg_pack(int n_strips, const int *strips, const int *ndof, const int *n_loc,
                            int max_loc, const long long *blk_base, const long long *pk_base,
                            const int *pk_size, const double *blocks, double *packed,
-                           void *stream) {
-    if (n_strips < 0 || max_loc < 0) return MFB_ERR_ARG;
+                           int layout, void *stream) {
+    if (n_strips < 0 || max_loc < 0 || layout < 0 || layout > 1) return MFB_ERR_ARG;
     if (n_strips == 0 || max_loc == 0) return MFB_OK;
     dim3 grid(n_strips, max_loc < 64 ? max_loc : 64);
     cg_pack_kernel<<<grid, 128, 0, mfb_stream(stream)>>>(
         reinterpret_cast<const int4 *>(strips), ndof, n_loc, blk_base, pk_base, pk_size, blocks,
-        packed);
+        packed, layout);
     MFB_CHECK_LAUNCH();
     return MFB_OK;
 }

@@ -88,6 +88,8 @@ BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 S1_FIELD_BYTES_MAX = 32 << 30   # S1 keeps every realization's fields for the moments
 S1_CHUNK_REALIZATIONS = None    # S1 realizations per chunk (None: as many as fit)
 CLUSTER_SHAPES = ((4, 16), (8, 16), (2, 8), (4, 8))   # (CTAs per cluster, points) to try
+MULTI_STREAM = True         # multi-point CG: S p streamed over per-warp pass lists
+MULTI_CHUNKS = True         # multi-point CG: reflection-family point order + chunked claims
 HIST_SEG = 1024             # residual-history segment (large-interface CG kernels)
 MOMENTS_MAX_NDOF = 64       # mfb_group_stats / mfb_group_fields block limit (mfb.h)
 KL_MAX_TERM = 64            # mfb_kl_realize_batched terms per region (mfb.h)
@@ -282,13 +284,78 @@ def _pack_histories(hist, iters):
     return ResidualHistories(hist[:, :width][mask].cpu().numpy(), it_h)
 
 
+def cg_point_order(points, local_idx, local_points, tail=0, width=8):
+    """Sweep order and claim chunks of the multi-point CG (mfb_cg_multi).
+
+    The kernel applies a Darcy block once per *distinct* local realization
+    among the `width` points a CTA holds, so points that share local
+    realizations should sit in the same CTA. Points are sorted (i) longest
+    first -- CG iterations grow with the point's largest |coordinate| (cfg4:
+    the 64 points at the 15-point rule's extreme node need ~73k iterations,
+    the median 20k) --, then (ii) by *reflection family*: the points whose
+    local realizations agree up to the sign of each region's local point
+    (on a symmetric grid: the 2^m sign combinations of a point with m
+    off-centre regions, which visit only two local realizations per such
+    region), families of `width` first; a chunk never splits a family. The
+    last `tail` points are single-point chunks so the sweep's end stays
+    balanced across CTAs. Pure scheduling: the results do not depend on it.
+
+    points [n, n_dims]; local_idx [regions, n]; local_points[r] [N_loc, n_term].
+    Returns (order [n] int64, chunk_ptr [n_chunks + 1] int32 into the order).
+    """
+    n = int(points.shape[0])
+    local_idx = np.asarray(local_idx).reshape(-1, n).astype(np.int64)
+    key = np.abs(points).max(axis=1) if points.size else np.zeros(n)
+    coarse = np.empty_like(local_idx)
+    for r in range(local_idx.shape[0]):
+        lp = np.round(np.asarray(local_points[r], dtype=np.float64), 9) + 0.0
+        lut = {row.tobytes(): i for i, row in enumerate(lp)}
+        cls = np.arange(len(lp))
+        for i, row in enumerate(lp):
+            j = lut.get((-row + 0.0).tobytes())
+            if j is not None:
+                cls[i] = min(i, j)
+        coarse[r] = cls[local_idx[r]]
+    o = np.lexsort(tuple(local_idx[::-1]) + tuple(coarse[::-1]) + (-key,))
+    sig = np.vstack([key[o][None, :], coarse[:, o].astype(np.float64)])
+    new = np.ones(n, dtype=bool)
+    new[1:] = (np.diff(sig, axis=1) != 0).any(axis=0)
+    fid = np.cumsum(new) - 1
+    size = np.minimum(np.bincount(fid)[fid], width)
+    o2 = np.lexsort((np.arange(n), fid, -size, -key[o]))
+    order, fid = o[o2], fid[o2]
+    # chunks: whole families while they fit, cut at `width`; singles in the tail
+    n_main = max(0, n - int(tail))
+    starts = np.flatnonzero(np.r_[True, fid[1:] != fid[:-1]])
+    ends = np.r_[starts[1:], n]
+    cptr, fill = [0], 0
+    for a, b in zip(starts, ends):
+        a, b = int(a), min(int(b), n_main)
+        while a < b:
+            m = min(b - a, width)
+            if fill + m > width:
+                cptr.append(cptr[-1] + fill)
+                fill = 0
+            fill += m
+            a += m
+            if fill == width:
+                cptr.append(cptr[-1] + fill)
+                fill = 0
+    if fill:
+        cptr.append(cptr[-1] + fill)
+    cptr = np.concatenate([np.asarray(cptr, dtype=np.int64),
+                           np.arange(n_main + 1, n + 1, dtype=np.int64)])
+    return order, cptr.astype(np.int32)
+
+
 def cg_tasks(n_sub, ndof, dof_ptr, dof_map, n_lambda, run=8):
     """Work items of the multi-point CG (mfb_cg_multi): runs of <= `run`
     mortar dofs of one interface with both sides' block rows (an interface's
     dofs are contiguous in both adjacent subdomains' local orders, mortar.py
     sub_dofs), most expensive first, and the strip layout of the packed
     basis pool (mfb_cg_pack): every task side is an 8-row strip of its
-    subdomain's block, stored as ceil(ndof / 4) MMA fragments of 32 doubles.
+    subdomain's block, stored as ceil(ndof / 4) MMA fragments of 32 doubles
+    (padded to an even count).
 
     Returns (tasks [n, 4], sides [n_lambda, 4], strips [m, 4], pk_size
     [n_sub]) int32: task {first dof, strip offset lower, strip offset upper,
@@ -327,7 +394,8 @@ def cg_tasks(n_sub, ndof, dof_ptr, dof_map, n_lambda, run=8):
     strip_off, strips = {}, []
     pk_size = np.zeros(n_sub, dtype=np.int64)
     for s_ in range(n_sub):
-        w = 32 * ((int(ndof[s_]) + 3) // 4)
+        nt4 = (int(ndof[s_]) + 3) // 4
+        w = 32 * (nt4 + (nt4 & 1))       # an even number of fragments per strip (zero-padded)
         for k, (r0, R) in enumerate(sorted(per_sid[s_])):
             strip_off[(s_, r0)] = k * w
             strips.append((s_, r0, R, k * w))
@@ -939,21 +1007,31 @@ class SweepEngine:
             # the large-interface kernels keep residual histories in segments
             # (device memory ~ the iterations run, not n_pts x max_iter)
             mt = self._pack_tables() if mt is None else mt
-            self._repack(mt)
-            # longest points first: CG iterations grow with the point's
-            # largest |coordinate| (cfg4: the 64 points at the 15-point
-            # rule's extreme node need ~73k iterations, the median 20k), so
-            # they start first instead of trailing the sweep. Every point's
-            # arithmetic is independent of its slot: the outputs are the same
-            # bits, scattered back to point order below.
-            order = None
-            if local_override is None and n_pts >= 4 * N_SMS and plan.grid.n_dims:
+            # streamed S p (pass lists in shared memory) when they fit
+            stream = ct is None and MULTI_STREAM and mt["list_cap"] > 0
+            self._repack(mt, layout=1 if stream else 0)
+            # Sweep order (cg_point_order): longest points first, and points
+            # that share local realizations next to each other, claimed by a
+            # CTA in chunks. Every point's arithmetic is independent of its
+            # slot: the outputs are the same bits, scattered back to point
+            # order below.
+            order, chunks = None, None
+            if (ct is None and local_override is None and n_pts >= 4 * N_SMS
+                    and plan.grid.n_dims and st.method != "S2" and MULTI_CHUNKS):
+                o, cptr = cg_point_order(
+                    np.asarray(plan.grid.points[k0:k0 + n_pts]),
+                    plan.host.local[:, k0:k0 + n_pts], plan.grid.local_points,
+                    tail=mt["n_cta"] * 8)
+                order = torch.as_tensor(o, device="cuda")
+                chunks = torch.as_tensor(cptr, dtype=torch.int32, device="cuda")
+            elif local_override is None and n_pts >= 4 * N_SMS and plan.grid.n_dims:
                 key = np.abs(np.asarray(plan.grid.points[k0:k0 + n_pts])).max(axis=1)
                 o = np.argsort(-key, kind="stable")
                 if np.any(o != np.arange(n_pts)):
                     order = torch.as_tensor(o, device="cuda")
-                    cg_local = st.d_cg_local[:, k0 + order].contiguous()
-                    n_real, k0 = n_pts, 0
+            if order is not None:
+                cg_local = st.d_cg_local[:, k0 + order].contiguous()
+                n_real, k0 = n_pts, 0
             seg = HIST_SEG
             max_segs = (int(max_iter) + seg - 1) // seg
             cap = hist_segments
@@ -983,7 +1061,8 @@ class SweepEngine:
                         _ptr(pool), seg, int(cap), _ptr(seg_tab), max_segs, _ptr(counter),
                         self.sp), "mfb_cg_cluster")
                 else:
-                    self.cg_kernel_name = "cg_multi_kernel (8 points per CTA on FP64 mma.m8n8k4)"
+                    self.cg_kernel_name = ("cg_multi_kernel (8 points per CTA on FP64 mma.m8n8k4"
+                                       + (", S p streamed over pass lists)" if stream else ")"))
                     _lib.check(self.L.mfb_cg_multi(
                         nl, plan.n_sub, int(plan.dof_ptr[-1]), _ptr(plan.d_ndof),
                         _ptr(plan.d_dof_ptr), _ptr(plan.d_dof_map), _ptr(st.d_cg_region),
@@ -994,7 +1073,13 @@ class SweepEngine:
                         mt["n_tasks"], _ptr(mt["sides"]), _ptr(mt["packed"]),
                         _ptr(mt["pk_base"]), _ptr(mt["pk_size"]), mt["n_cta"],
                         _ptr(mt["scratch"]), _ptr(mt["counter"]), _ptr(seg_tab), max_segs,
-                        int(cap), _ptr(counter), _ptr(mt["trec"]), self.sp), "mfb_cg_multi")
+                        int(cap), _ptr(counter), _ptr(mt["trec_s" if stream else "trec"]),
+                        _ptr(chunks) if chunks is not None else None,
+                        int(chunks.numel()) - 1 if chunks is not None else 0,
+                        mt["list_cap"] if stream else 0,
+                        _ptr(mt["dm_pairs" if stream else "dm_rows"]),
+                        int(mt["dm_pairs" if stream else "dm_rows"].numel()), self.sp),
+                        "mfb_cg_multi")
                 hist = SegmentedHist(pool, seg_tab, seg, counter, cap)
                 if not check_hist or hist.complete():   # complete() syncs the stream
                     break
@@ -1065,7 +1150,45 @@ class SweepEngine:
                     trec[t, 7] = plan.dof_ptr[j]
                     trec[t, 9] = pk_base[j] + so_up
                     trec[t, 11] = pk_size[j]
+            # streamed S p (mfb_cg_multi list_cap): per warp (task t on warp
+            # t mod 16) one entry per pass -- at most 8 local-realization
+            # groups per Darcy side -- plus a record per task and the end mark
+            per_task = np.ones(len(tab), dtype=np.int64)
+            for t, (d0, so_lo, so_up, meta) in enumerate(tab.astype(np.int64)):
+                for sd in (meta & 0xfff, ((meta >> 12) & 0xfff) - 1):
+                    if sd >= 0:
+                        per_task[t] += 8 if creg[sd] >= 0 else 1
+            list_cap = max(int(per_task[w::16].sum()) for w in range(16)) + 1
+            n_rows = int(plan.dof_ptr[-1])
+            n_pad = int(((nd + 7) // 8 * 8).sum())
+            if (int(nd.max()) > 248
+                    or self.L.mfb_cg_multi_smem(nl, n_pad, list_cap) + 8192 > 227 * 1024):
+                list_cap = 0
+            # dof lists as p offsets (mfb.h: the slot halves of every other dof
+            # pair exchanged): row order for the task loop; per subdomain padded
+            # to 8 columns and pair-interleaved for the streamed kernel
+            dmap = np.asarray(plan.dof_map, dtype=np.int64)
+            swz = dmap * 8 + ((dmap & 2) << 1)
+            dm_rows = np.concatenate([swz, np.zeros(8, dtype=np.int64)])
+            ndp = (nd + 7) // 8 * 8
+            dmo2 = np.concatenate([[0], np.cumsum(ndp)])
+            dm_pairs = np.zeros(int(dmo2[-1]), dtype=np.int64)
+            for s_ in range(plan.n_sub):
+                c = np.arange(int(nd[s_]))
+                dm_pairs[dmo2[s_] + (c & ~7) + 2 * (c & 3) + ((c >> 2) & 1)] = \
+                    swz[plan.dof_ptr[s_]:plan.dof_ptr[s_] + nd[s_]]
+            trec_s = trec.copy()
+            for t, (d0, so_lo, so_up, meta) in enumerate(tab.astype(np.int64)):
+                i, j = meta & 0xfff, ((meta >> 12) & 0xfff) - 1
+                trec_s[t, 6] = dmo2[i]
+                if j >= 0:
+                    trec_s[t, 7] = dmo2[j]
+            if len(dm_pairs) >= 65536:
+                list_cap = 0
             mt = {"tasks": _dev(tab.ravel(), torch.int32), "n_tasks": int(len(tab)),
+                  "list_cap": list_cap,
+                  "trec_s": _dev(trec_s.ravel().astype(np.int32), torch.int32),
+                  "dm_rows": _dev(dm_rows, torch.int32), "dm_pairs": _dev(dm_pairs, torch.int32),
                   "trec": _dev(trec.ravel().astype(np.int32), torch.int32),
                   "sides": _dev(sides.ravel(), torch.int32),
                   "strips": _dev(strips.ravel(), torch.int32), "n_strips": int(len(strips)),
@@ -1080,13 +1203,13 @@ class SweepEngine:
             st._multi = mt
         return mt
 
-    def _repack(self, mt):
+    def _repack(self, mt, layout=0):
         plan, st = self.plan, self.st
         self.launches += 1
         _lib.check(self.L.mfb_cg_pack(
             mt["n_strips"], _ptr(mt["strips"]), _ptr(plan.d_ndof), _ptr(mt["n_loc"]),
             mt["max_loc"], _ptr(st.d_blk), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
-            _ptr(st.blocks), _ptr(mt["packed"]), self.sp), "mfb_cg_pack")
+            _ptr(st.blocks), _ptr(mt["packed"]), int(layout), self.sp), "mfb_cg_pack")
 
     def _multi_wanted(self, n_pts, force=False):
         """True when the blocks exceed shared memory and enough points fill
@@ -1106,7 +1229,8 @@ class SweepEngine:
         its shared-memory vectors do not fit or the kernel is not wanted."""
         plan, torch = self.plan, self.torch
         nl, n_rows = int(plan.n_lambda), int(plan.dof_ptr[-1])
-        if 8 * 8 * nl + 4 * n_rows > 220 * 1024 or not self._multi_wanted(n_pts, force):
+        if (self.L.mfb_cg_multi_smem(nl, n_rows + 8, 0) + 8192 > 227 * 1024
+                or not self._multi_wanted(n_pts, force)):
             return None
         mt = self._pack_tables()
         if "scratch" not in mt:

@@ -7,7 +7,9 @@ import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np, torch
-from paper_1802_06263_b200 import _lib
+from paper_1802_06263_b200 import _lib, interface
+interface.MULTI_CHUNKS = os.environ.get("MFB_CHUNKS", "1") == "1"
+interface.MULTI_STREAM = os.environ.get("MFB_STREAM", "1") == "1"
 from paper_1802_06263_b200.adapter import load_config
 from paper_1802_06263_b200.interface import SweepEngine, get_plan
 n_pts = int(sys.argv[1]) if len(sys.argv) > 1 else 2368
@@ -31,5 +33,5 @@ L.mfb_debug_multi(0, buf)
 a = np.array(buf[:], dtype=np.float64).reshape(148, 8)
 per = a[:, :6].sum(0) / max(a[:, 6].sum(), 1)
 names = ["refill", "S p (warp 0)", "reduce#1", "x,r update", "reduce#2", "p update+fin"]
-print(f"{e0.elapsed_time(e1):.1f} ms, {a[:, 6].mean():.0f} iterations per CTA, cycles per "
+print(f"list_cap {eng.st._multi['list_cap']} stream {interface.MULTI_STREAM}: {e0.elapsed_time(e1):.1f} ms, {a[:, 6].mean():.0f} iterations per CTA, cycles per "
       f"iteration {per.sum():.0f} = " + ", ".join(f"{n} {v:.0f}" for n, v in zip(names, per)))
