@@ -351,6 +351,7 @@ int mfb_cg_cluster_max_clusters(int C, int NP, int n_own_max, long long smem);
 int mfb_debug_cluster(int stop_at);   /* debug: stop the cluster CG at a phase (0: off; 100: phase clocks) */
 int mfb_debug_cluster_prof(long long *out, int n);   /* per-CTA phase clocks of the last run */
 int mfb_debug_multi(int on, long long *out);   /* multi CG phase clocks: on/off, or read (out) */
+int mfb_debug_multi_warps(long long *out, int reset);   /* CTA 0's S p clocks per warp [16] (-DMFB_PHASE_PROF builds) */
 long long mfb_cg_cluster_smem(int NP, int n_used_max, int n_own_max, int n_cut_max,
                               int n_cm_max, int n_unit_max, int n_strip_max, int n_regions,
                               int flags);

@@ -76,6 +76,7 @@ _SIGS = {
     "mfb_basis_apply": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
     "mfb_debug_cluster": ([_i], _i),
     "mfb_debug_multi": ([_i, _p], _i),
+    "mfb_debug_multi_warps": ([_p, _i], _i),
     "mfb_debug_cluster_prof": ([_p, _i], _i),
     "mfb_cg_cluster_max_clusters": ([_i, _i, _i, _ll], _i),
     "mfb_cg_cluster_smem": ([_i, _i, _i, _i, _i, _i, _i, _i, _i], _ll),

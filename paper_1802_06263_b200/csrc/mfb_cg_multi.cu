@@ -114,6 +114,34 @@ __device__ __forceinline__ void tm_st(unsigned ta, double2 v) {
                  :: "r"(ta), "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)),
                     "r"(__double2loint(v.y)), "r"(__double2hiint(v.y)) : "memory");
 }
+// issue / wait / fence pieces for batches (the fence ties the registers to
+// the wait: volatile asms keep their order, the uses read the fenced values)
+#define TM_LD4(ta, v)                                                            \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];" \
+                 : "=r"((v)[0]), "=r"((v)[1]), "=r"((v)[2]), "=r"((v)[3]) : "r"(ta) : "memory")
+#define TM_WAIT_LD() asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory")
+#define TM_FENCE4(v) \
+    asm volatile("" : "+r"((v)[0]), "+r"((v)[1]), "+r"((v)[2]), "+r"((v)[3]) :: "memory")
+__device__ __forceinline__ double2 tm_d2(const unsigned (&v)[4]) {
+    return make_double2(__hiloint2double(v[1], v[0]), __hiloint2double(v[3], v[2]));
+}
+#ifdef MFB_A_NOALLOC
+__device__ __forceinline__ double2 ldg_a(const double2 *p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+#else
+__device__ __forceinline__ double2 ldg_a(const double2 *p) { return __ldg(p); }
+#endif
+#ifdef MFB_SCRATCH_CG
+#define SC_LD(p) __ldcg(p)
+#define SC_ST(p, v) __stcg(p, v)
+#else
+#define SC_LD(p) (*(p))
+#define SC_ST(p, v) (*(p) = (v))
+#endif
 __device__ __forceinline__ void tm_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -244,8 +272,10 @@ __global__ void cg_pack_kernel(const int4 *__restrict__ strips, const int *__res
         for (int e = threadIdx.x; e < 32 * nt4; e += blockDim.x) {
             const int lane = e & 31, g = lane >> 2, c = 4 * (e >> 5) + (lane & 3);
             // layout 1: the lane's fragments 2 k, 2 k + 1 adjacent (one 16-byte load)
-            const int dst = layout ? 64 * (e >> 6) + 2 * lane + ((e >> 5) & 1) : e;
-            D[dst] = (g < S.z && c < nd) ? B[(long long)c * nd + S.y + g] : 0.0;
+            // (a paired strip alternates with its partner: 128 doubles per pair)
+            const int dst = layout ? ((S.z >> 8) ? 128 : 64) * (e >> 6) + 2 * lane + ((e >> 5) & 1)
+                                   : e;
+            D[dst] = (g < (S.z & 0xff) && c < nd) ? B[(long long)c * nd + S.y + g] : 0.0;
         }
     }
 }
@@ -267,6 +297,7 @@ __global__ void cg_pack_kernel(const int4 *__restrict__ strips, const int *__res
 // << 8 | the block's offset in the (padded, pair-interleaved) dof list << 16. A task-end entry is followed by
 // the task's record {first dof, rows | has upper << 8}.
 constexpr int PL_SIDE = 1 << 5, PL_TEND = 1 << 6, PL_END = 1 << 7;
+constexpr int PL_DBL = 1 << 30, PL_XMASK = PL_DBL - 1;   // in x: a 16-row pass
 
 __device__ __forceinline__ void build_pass_list(const CgMultiArgs &A, int2 *L, int run,
                                                 const int *g_cnt, const int *g_loc,
@@ -275,6 +306,7 @@ __device__ __forceinline__ void build_pass_list(const CgMultiArgs &A, int2 *L, i
     for (int ti = threadIdx.x >> 5; ti < A.n_tasks; ti += MW) {
         const int4 T = __ldg(A.trec + 3 * ti), U = __ldg(A.trec + 3 * ti + 1),
                    V = __ldg(A.trec + 3 * ti + 2);
+        if (T.w < 0) continue;                      // (no task at this position)
         const int j = ((T.w >> 12) & 0xfff) - 1, Rr = T.w >> 24;
         int last = -1;
         for (int side = 0; side < (j >= 0 ? 2 : 1); ++side) {
@@ -288,7 +320,8 @@ __device__ __forceinline__ void build_pass_list(const CgMultiArgs &A, int2 *L, i
                 if (!(m & run)) continue;
                 const int l = reg < 0 ? 0 : g_loc[reg * MP + gi];
                 last = n;
-                L[n++] = make_int2((int)(((long long)pkb + (long long)l * psz) >> 6),
+                L[n++] = make_int2((int)(((long long)pkb + (long long)l * psz) >> 6) |
+                                       (Rr > 8 ? PL_DBL : 0),
                                    (int)((unsigned)steps | (side ? PL_SIDE : 0) | (m << 8) |
                                          ((unsigned)dmo << 16)));
             }
@@ -301,39 +334,46 @@ __device__ __forceinline__ void build_pass_list(const CgMultiArgs &A, int2 *L, i
     L[n] = make_int2(0, PL_END);
 }
 
-// One warp's S p over its pass list; returns this thread's p . S p partials
-// (slots 2 q, 2 q + 1) in v0 / v1. The packed strips are pair-interleaved
-// (mfb_cg_pack layout 1: fragments 2 k, 2 k + 1 of lane l adjacent, one
-// 16-byte load per step) and so is the dof list (the two fragments' rows of
-// lane q adjacent, one 8-byte load per step).
-__device__ __forceinline__ void stream_passes(const CgMultiArgs &A, const int2 *L, int run,
-                                              const double *__restrict__ ps, const int *sdm,
-                                              double2 *__restrict__ S2, const double2 *P2,
-                                              double &v0, double &v1) {
+// One warp's S p over its pass list from entry i0; returns this thread's
+// p . S p partials (slots 2 q, 2 q + 1) in v0 / v1 and the entry it stopped
+// at. The packed strips are pair-interleaved (mfb_cg_pack layout 1: fragments
+// 2 k, 2 k + 1 of lane l adjacent, one 16-byte load per step) and so is the
+// dof list (the two fragments' rows of lane q adjacent, one 8-byte load per
+// step). DBL: the 16-row passes at the head of the list -- two strips whose
+// fragment pairs alternate in memory, every B operand feeding both (four
+// MMAs per step); the walk stops at the first 8-row pass.
+template <bool DBL>
+__device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, int i0, int run,
+                                           const double *__restrict__ ps, const int *sdm,
+                                           double2 *__restrict__ S2, const double2 *P2,
+                                           double &v0, double &v1) {
     const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
     const double2 *__restrict__ pk = reinterpret_cast<const double2 *>(A.packed) + lane;
     const int2 *dmq = reinterpret_cast<const int2 *>(sdm) + q;
-    int iL = 0, iC = 0;
-    int2 eC = L[0];
-    if (eC.y & PL_END) return;
+    int iL = i0, iC = i0;
+    int2 eC = L[i0];
+#define PL_STOP(e) (((e).y & PL_END) || (DBL && !((e).x & PL_DBL)))
+    if (PL_STOP(eC)) return i0;
     int yL = eC.y, nL = yL & 31, nC = nL;
-    const double2 *pL = pk + ((long long)eC.x << 5);
+    const double2 *pL = pk + ((long long)(eC.x & PL_XMASK) << 5);
     const int2 *dmC = dmq + ((unsigned)eC.y >> 17);
-    double2 af[4];
+    double2 af[4], ag[DBL ? 4 : 1];
     double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0, lo0 = 0.0, lo1 = 0.0, up0 = 0.0, up1 = 0.0;
+    double E0 = 0.0, E1 = 0.0, O0 = 0.0, O1 = 0.0, LO0 = 0.0, LO1 = 0.0, UP0 = 0.0, UP1 = 0.0;
     // the list walk is a loop so that it stays a (rarely taken) branch
     // instead of a dozen predicated instructions in every step
 #define PL_ISSUE(s)                                                      \
     do {                                                                 \
-        af[s] = __ldg(pL);                                               \
-        pL += 32;                                                        \
+        af[s] = ldg_a(pL);                                               \
+        if (DBL) ag[s] = ldg_a(pL + 32);                                 \
+        pL += DBL ? 64 : 32;                                             \
         --nL;                                                            \
         while (nL == 0) {                                                \
             iL += 1 + ((yL >> 6) & 1);                                   \
             const int2 eN = L[iL];                                       \
             yL = eN.y;                                                   \
-            nL = (yL & PL_END) ? -1 : (yL & 31);                         \
-            pL = pk + ((long long)eN.x << 5);                            \
+            nL = PL_STOP(eN) ? -1 : (yL & 31);                           \
+            pL = pk + ((long long)(eN.x & PL_XMASK) << 5);               \
         }                                                                \
     } while (0)
     PL_ISSUE(0); PL_ISSUE(1); PL_ISSUE(2); PL_ISSUE(3);
@@ -345,50 +385,90 @@ __device__ __forceinline__ void stream_passes(const CgMultiArgs &A, const int2 *
             const double b0 = ps[dd.x ^ g], b1 = ps[dd.y ^ g];
             dmma884(e0, e1, af[s].x, b0);
             dmma884(o0, o1, af[s].y, b1);
+            if (DBL) {
+                dmma884(E0, E1, ag[s].x, b0);
+                dmma884(O0, O1, ag[s].y, b1);
+            }
             PL_ISSUE(s);
             if (--nC == 0) {
                 // a column of B only feeds its own slot: the group's members
                 // take the products, the other slots keep their accumulators
                 const int m = (eC.y >> 8) & run;
+                const bool m0 = (m >> (2 * q)) & 1, m1 = (m >> (2 * q + 1)) & 1;
                 const double t0 = e0 + o0, t1 = e1 + o1;
                 if (eC.y & PL_SIDE) {
-                    if ((m >> (2 * q)) & 1) up0 += t0;
-                    if ((m >> (2 * q + 1)) & 1) up1 += t1;
+                    if (m0) up0 += t0;
+                    if (m1) up1 += t1;
                 } else {
-                    if ((m >> (2 * q)) & 1) lo0 += t0;
-                    if ((m >> (2 * q + 1)) & 1) lo1 += t1;
+                    if (m0) lo0 += t0;
+                    if (m1) lo1 += t1;
                 }
                 e0 = e1 = o0 = o1 = 0.0;
+                if (DBL) {
+                    const double T0 = E0 + O0, T1 = E1 + O1;
+                    if (eC.y & PL_SIDE) {
+                        if (m0) UP0 += T0;
+                        if (m1) UP1 += T1;
+                    } else {
+                        if (m0) LO0 += T0;
+                        if (m1) LO1 += T1;
+                    }
+                    E0 = E1 = O0 = O1 = 0.0;
+                }
                 if (eC.y & PL_TEND) {
                     const int2 rec = L[iC + 1];
                     iC += 2;
-                    if (g < (rec.y & 0xff)) {
+                    const int rows = rec.y & 0xff;
+                    if (g < rows) {
                         const double2 sp = (rec.y & 256) ? make_double2(lo0 + up0, lo1 + up1)
                                                          : make_double2(lo0, lo1);
                         const int e = (rec.x + g) * (MP / 2) + q;
-                        S2[e] = sp;
+                        SC_ST(S2 + e, sp);
                         const double2 pp = P2[pidx(e)];
                         v0 += pp.x * sp.x;
                         v1 += pp.y * sp.y;
                     }
                     lo0 = lo1 = up0 = up1 = 0.0;
+                    if (DBL) {
+                        if (g + 8 < rows) {
+                            const double2 sp = (rec.y & 256)
+                                                   ? make_double2(LO0 + UP0, LO1 + UP1)
+                                                   : make_double2(LO0, LO1);
+                            const int e = (rec.x + 8 + g) * (MP / 2) + q;
+                            SC_ST(S2 + e, sp);
+                            const double2 pp = P2[pidx(e)];
+                            v0 += pp.x * sp.x;
+                            v1 += pp.y * sp.y;
+                        }
+                        LO0 = LO1 = UP0 = UP1 = 0.0;
+                    }
                 } else {
                     iC += 1;
                 }
                 eC = L[iC];
-                if (eC.y & PL_END) return;
+                if (PL_STOP(eC)) return iC;
                 nC = eC.y & 31;
                 dmC = dmq + ((unsigned)eC.y >> 17);
             }
         }
     }
 #undef PL_ISSUE
+#undef PL_STOP
+}
+
+__device__ __forceinline__ void stream_passes(const CgMultiArgs &A, const int2 *L, int run,
+                                              const double *__restrict__ ps, const int *sdm,
+                                              double2 *__restrict__ S2, const double2 *P2,
+                                              double &v0, double &v1) {
+    const int i1 = stream_walk<true>(A, L, 0, run, ps, sdm, S2, P2, v0, v1);
+    stream_walk<false>(A, L, i1, run, ps, sdm, S2, P2, v0, v1);
 }
 
 enum { SLOT_RUN = 0, SLOT_NEW = 1, SLOT_DONE = 2 };
 
 __device__ int g_multi_dbg;
 __device__ long long g_multi_prof[148 * 8];
+__device__ long long g_multi_warp[MW];          // phase A clocks per warp of CTA 0 (MFB_PHASE_PROF)
 // phase clocks (tools/multi_phases.py) only in a -DMFB_PHASE_PROF build: the
 // counters cost registers the production kernel needs
 #ifdef MFB_PHASE_PROF
@@ -579,7 +659,13 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                     if (lane == 0) build_pass_list(A, plist, run, s_gcnt, s_gloc, s_gmask);
                     __syncwarp();
                 }
+#if MP_PROF
+                const long long tw0 = clock64();
+#endif
                 stream_passes(A, plist, run, ps, sdm, S2, P2, v0, v1);
+#if MP_PROF
+                if (dbg && lane == 0 && blockIdx.x == 0) g_multi_warp[wid] += clock64() - tw0;
+#endif
             }
             prev_run = run;
         } else
@@ -638,11 +724,22 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
             // VB elements per trip, their scratch loads issued together
             for (int k0 = 0; k0 < kw; k0 += VB) {
                 double2 s2[VB], x2[VB], r2[VB];
-                tm_ld(tr + 4 * k0, r2);
+                unsigned rr[VB][4];
+#pragma unroll
+                for (int k = 0; k < VB; ++k) TM_LD4(tr + 4 * (k0 + k), rr[k]);
 #pragma unroll
                 for (int k = 0; k < VB; ++k) {
                     const int e = tid + (k0 + k) * MNT;
-                    if (act && e < npair) { s2[k] = S2[e]; x2[k] = X2[e]; }
+                    if (act && e < npair) {
+                        s2[k] = SC_LD(S2 + e);
+                        x2[k] = SC_LD(X2 + e);
+                    }
+                }
+                TM_WAIT_LD();
+#pragma unroll
+                for (int k = 0; k < VB; ++k) {
+                    TM_FENCE4(rr[k]);
+                    r2[k] = tm_d2(rr[k]);
                 }
 #pragma unroll
                 for (int k = 0; k < VB; ++k) {
@@ -659,7 +756,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
                             r2[k].y = __dsub_rn(r2[k].y, __dmul_rn(a1, s2[k].y));
                             v1 += r2[k].y * r2[k].y;
                         }
-                        X2[e] = x2[k];
+                        SC_ST(X2 + e, x2[k]);
                     }
                     tm_st(tr + 4 * (k0 + k), r2[k]);
                 }
@@ -761,6 +858,12 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
 }
 
 }  // namespace
+
+extern "C" int mfb_debug_multi_warps(long long *out, int reset) {
+    long long z[MW] = {0};
+    if (reset) return cudaMemcpyToSymbol(g_multi_warp, z, sizeof(z)) == cudaSuccess ? 0 : 2;
+    return cudaMemcpyFromSymbol(out, g_multi_warp, sizeof(z)) == cudaSuccess ? 0 : 2;
+}
 
 extern "C" int mfb_debug_multi(int on, long long *out) {
     if (out)

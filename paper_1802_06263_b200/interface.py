@@ -411,6 +411,80 @@ def cg_tasks(n_sub, ndof, dof_ptr, dof_map, n_lambda, run=8):
             pk_size.astype(np.int32))
 
 
+def _even_frags(nd):
+    nt4 = (int(nd) + 3) // 4
+    return nt4 + (nt4 & 1)
+
+
+def cg_stream_tasks(tab, sides, strips, ndof, region=None, n_warps=16, darcy_groups=2.0):
+    """Tasks and strip layout of the streamed multi-point CG (mfb_cg_multi,
+    list_cap > 0): two consecutive 8-row tasks of one interface (rows
+    consecutive in both subdomains) become one 16-row task whose two strips
+    per side share every B operand. Their strips are interleaved in the
+    packed pool (pair k of the first strip, then pair k of the second, 128
+    doubles per step).
+
+    The kernel's warp w walks tasks w, w + n_warps, ...: the table is laid out
+    so that these are the warp's share of a longest-processing-time
+    assignment (cost: MMAs of both sides, a Darcy side counted for
+    `darcy_groups` local realizations, plus per-pass and per-task overheads),
+    its 16-row tasks first; positions without a task hold meta = -1.
+
+    Returns (tab_s [n, 4], strips_s [m, 4]): tasks like cg_tasks' with up to
+    16 rows, and the strips with their layout-1 offsets and rows | paired << 8.
+    """
+    tab = np.asarray(tab, dtype=np.int64)
+    strips_s = np.asarray(strips, dtype=np.int64).copy()
+    ndof = np.asarray(ndof, dtype=np.int64)
+    strip_row = {(int(s_), int(r0)): k for k, (s_, r0, _, _) in enumerate(strips_s)}
+    by_d0 = {int(t[0]): t for t in tab}
+    out, used = [], set()
+    for d0 in sorted(by_d0):
+        if d0 in used:
+            continue
+        _, so_lo, so_up, meta = (int(v) for v in by_d0[d0])
+        i, j, R = meta & 0xfff, ((meta >> 12) & 0xfff) - 1, meta >> 24
+        ai, aj = int(sides[d0][1]), int(sides[d0][3])
+        nxt = by_d0.get(d0 + 8)
+        dbl = False
+        if R == 8 and nxt is not None:
+            m2 = int(nxt[3])
+            same = (m2 & 0xfff) == i and ((m2 >> 12) & 0xfff) - 1 == j
+            if same and int(sides[d0 + 8][1]) == ai + 8 and \
+                    (j < 0 or int(sides[d0 + 8][3]) == aj + 8):
+                dbl = True
+                used.add(d0 + 8)
+                R += m2 >> 24
+                for s_, a in ((i, ai), (j, aj)):
+                    if s_ < 0:
+                        continue
+                    ka, kb = strip_row[(s_, a)], strip_row[(s_, a + 8)]
+                    assert strips_s[kb, 3] - strips_s[ka, 3] == 32 * _even_frags(ndof[s_])
+                    strips_s[kb, 3] = strips_s[ka, 3] + 64
+                    strips_s[ka, 2] |= 256
+                    strips_s[kb, 2] |= 256
+        cost = 4.0
+        for s_ in (i, j):
+            if s_ >= 0:
+                grp = darcy_groups if (region is not None and region[s_] >= 0) else 1.0
+                cost += grp * (_even_frags(ndof[s_]) * (2 if dbl else 1) + 2.0)
+        out.append((0 if dbl else 1, -cost, d0, so_lo, so_up, i | ((j + 1) << 12) | (R << 24)))
+    out.sort(key=lambda t: (t[1], t[0], t[2]))
+    load = np.zeros(n_warps)
+    mine = [[] for _ in range(n_warps)]
+    for t in out:                                   # most expensive first
+        w = int(np.argmin(load))
+        load[w] -= t[1]
+        mine[w].append(t)
+    depth = max(len(m) for m in mine)
+    tab_s = np.zeros((depth * n_warps, 4), dtype=np.int64)
+    tab_s[:, 3] = -1
+    for w, m in enumerate(mine):
+        for k, t in enumerate(sorted(m)):           # 16-row tasks first
+            tab_s[k * n_warps + w] = t[2:]
+    return tab_s, strips_s
+
+
 def _check_basis_cap(sizes_bytes, cap_mb):
     total = sum(sizes_bytes)
     if cap_mb is not None and total > cap_mb * 2 ** 20:
@@ -1070,7 +1144,8 @@ class SweepEngine:
                         _ptr(cg_local), n_real, _ptr(st.blocks), _ptr(st.hbar), k0, n_pts,
                         float(tol), int(max_iter), _ptr(lam), _ptr(iters), _ptr(status),
                         _ptr(pool), seg, _ptr(g) if keep_g else None, _ptr(mt["tasks"]),
-                        mt["n_tasks"], _ptr(mt["sides"]), _ptr(mt["packed"]),
+                        mt["n_tasks_s" if stream else "n_tasks"], _ptr(mt["sides"]),
+                        _ptr(mt["packed"]),
                         _ptr(mt["pk_base"]), _ptr(mt["pk_size"]), mt["n_cta"],
                         _ptr(mt["scratch"]), _ptr(mt["counter"]), _ptr(seg_tab), max_segs,
                         int(cap), _ptr(counter), _ptr(mt["trec_s" if stream else "trec"]),
@@ -1150,26 +1225,15 @@ class SweepEngine:
                     trec[t, 7] = plan.dof_ptr[j]
                     trec[t, 9] = pk_base[j] + so_up
                     trec[t, 11] = pk_size[j]
-            # streamed S p (mfb_cg_multi list_cap): per warp (task t on warp
-            # t mod 16) one entry per pass -- at most 8 local-realization
-            # groups per Darcy side -- plus a record per task and the end mark
-            per_task = np.ones(len(tab), dtype=np.int64)
-            for t, (d0, so_lo, so_up, meta) in enumerate(tab.astype(np.int64)):
-                for sd in (meta & 0xfff, ((meta >> 12) & 0xfff) - 1):
-                    if sd >= 0:
-                        per_task[t] += 8 if creg[sd] >= 0 else 1
-            list_cap = max(int(per_task[w::16].sum()) for w in range(16)) + 1
-            n_rows = int(plan.dof_ptr[-1])
-            n_pad = int(((nd + 7) // 8 * 8).sum())
-            if (int(nd.max()) > 248
-                    or self.L.mfb_cg_multi_smem(nl, n_pad, list_cap) + 8192 > 227 * 1024):
-                list_cap = 0
             # dof lists as p offsets (mfb.h: the slot halves of every other dof
-            # pair exchanged): row order for the task loop; per subdomain padded
-            # to 8 columns and pair-interleaved for the streamed kernel
+            # pair exchanged), row order for the task loop
             dmap = np.asarray(plan.dof_map, dtype=np.int64)
             swz = dmap * 8 + ((dmap & 2) << 1)
             dm_rows = np.concatenate([swz, np.zeros(8, dtype=np.int64)])
+            # streamed S p (mfb_cg_multi list_cap > 0): 16-row tasks where an
+            # interface allows, their strips interleaved; dof lists padded to 8
+            # columns per subdomain and pair-interleaved
+            tab_s, strips_s = cg_stream_tasks(tab, sides, strips, nd, creg)
             ndp = (nd + 7) // 8 * 8
             dmo2 = np.concatenate([[0], np.cumsum(ndp)])
             dm_pairs = np.zeros(int(dmo2[-1]), dtype=np.int64)
@@ -1177,16 +1241,35 @@ class SweepEngine:
                 c = np.arange(int(nd[s_]))
                 dm_pairs[dmo2[s_] + (c & ~7) + 2 * (c & 3) + ((c >> 2) & 1)] = \
                     swz[plan.dof_ptr[s_]:plan.dof_ptr[s_] + nd[s_]]
-            trec_s = trec.copy()
-            for t, (d0, so_lo, so_up, meta) in enumerate(tab.astype(np.int64)):
+            # per warp (task t on warp t mod 16) one list entry per pass -- at
+            # most 8 local-realization groups per Darcy side -- plus a record
+            # per task and the end mark
+            trec_s = np.zeros((len(tab_s), 12), dtype=np.int64)
+            per_task = np.ones(len(tab_s), dtype=np.int64)
+            for t, (d0, so_lo, so_up, meta) in enumerate(tab_s):
+                trec_s[t, :4] = (d0, so_lo, so_up, meta)
+                if meta < 0:                        # no task at this position
+                    per_task[t] = 0
+                    continue
                 i, j = meta & 0xfff, ((meta >> 12) & 0xfff) - 1
+                trec_s[t, 4] = nd[i] | ((creg[i] + 1) << 16)
                 trec_s[t, 6] = dmo2[i]
+                trec_s[t, 8] = pk_base[i] + so_lo
+                trec_s[t, 10] = pk_size[i]
+                per_task[t] += 8 if creg[i] >= 0 else 1
                 if j >= 0:
+                    trec_s[t, 5] = nd[j] | ((creg[j] + 1) << 16)
                     trec_s[t, 7] = dmo2[j]
-            if len(dm_pairs) >= 65536:
+                    trec_s[t, 9] = pk_base[j] + so_up
+                    trec_s[t, 11] = pk_size[j]
+                    per_task[t] += 8 if creg[j] >= 0 else 1
+            list_cap = max(int(per_task[w::16].sum()) for w in range(16)) + 1
+            if (int(nd.max()) > 248 or len(dm_pairs) >= 65536
+                    or self.L.mfb_cg_multi_smem(nl, len(dm_pairs), list_cap) + 8192 > 227 * 1024):
                 list_cap = 0
             mt = {"tasks": _dev(tab.ravel(), torch.int32), "n_tasks": int(len(tab)),
-                  "list_cap": list_cap,
+                  "list_cap": list_cap, "n_tasks_s": int(len(tab_s)),
+                  "strips_s": _dev(strips_s.ravel(), torch.int32),
                   "trec_s": _dev(trec_s.ravel().astype(np.int32), torch.int32),
                   "dm_rows": _dev(dm_rows, torch.int32), "dm_pairs": _dev(dm_pairs, torch.int32),
                   "trec": _dev(trec.ravel().astype(np.int32), torch.int32),
@@ -1207,7 +1290,8 @@ class SweepEngine:
         plan, st = self.plan, self.st
         self.launches += 1
         _lib.check(self.L.mfb_cg_pack(
-            mt["n_strips"], _ptr(mt["strips"]), _ptr(plan.d_ndof), _ptr(mt["n_loc"]),
+            mt["n_strips"], _ptr(mt["strips_s" if layout else "strips"]), _ptr(plan.d_ndof),
+            _ptr(mt["n_loc"]),
             mt["max_loc"], _ptr(st.d_blk), _ptr(mt["pk_base"]), _ptr(mt["pk_size"]),
             _ptr(st.blocks), _ptr(mt["packed"]), int(layout), self.sp), "mfb_cg_pack")
 

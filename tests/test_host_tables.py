@@ -51,7 +51,8 @@ def test_cg_tasks_cover_every_row_once(name):
     # strips partition every block's rows; offsets are whole fragment runs
     for s in range(n_sub):
         mine = strips[strips[:, 0] == s]
-        w = 32 * ((ndof[s] + 3) // 4)
+        nt4 = (ndof[s] + 3) // 4
+        w = 32 * (nt4 + (nt4 & 1))       # an even number of fragments per strip
         rows = np.zeros(ndof[s], dtype=int)
         for _, r0, R, off in mine:
             rows[r0:r0 + R] += 1
@@ -92,3 +93,85 @@ def test_residual_histories_from_the_padded_device_array():
     assert np.array_equal(h.flat, ref.flat) and np.array_equal(h.offsets, ref.offsets)
     with pytest.raises(IndexError):
         h[3]
+
+
+def test_cg_point_order_chunks():
+    """Sweep order of the multi-point CG: a permutation, longest points first,
+    chunks of <= 8 that never split a reflection family of <= 8, single-point
+    chunks in the tail, and fewer distinct local realizations per chunk than
+    the plain longest-first order."""
+    from paper_1802_06263_b200.adapter import load_config
+    from paper_1802_06263_b200.interface import cg_point_order
+    _, grid, _ = load_config(os.path.join(ROOT, "configs", "cfg4.json"))
+    sub = np.arange(0, grid.n_real, 4)
+    pts = np.asarray(grid.points)[sub]
+    li = np.stack([np.asarray(l)[sub] for l in grid.local_indices])
+    order, cptr = cg_point_order(pts, li, grid.local_points, tail=1184)
+    n = len(sub)
+    assert sorted(order.tolist()) == list(range(n))
+    assert cptr[0] == 0 and cptr[-1] == n
+    sizes = np.diff(cptr)
+    assert sizes.min() >= 1 and sizes.max() <= 8
+    assert np.all(sizes[np.searchsorted(cptr, n - 1184, side="left"):] == 1)
+    key = np.abs(pts).max(axis=1)[order]
+    assert np.all(np.diff(key) <= 1e-12)          # longest first
+
+    def mult(o, bounds):
+        tot = w = 0
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            if b - a > 1:
+                tot += sum(len(np.unique(li[r, o[a:b]])) for r in range(li.shape[0]))
+                w += (b - a) * li.shape[0] / 8.0
+        return tot / w
+    plain = np.argsort(-np.abs(pts).max(axis=1), kind="stable")
+    m_new = mult(order, cptr[:np.searchsorted(cptr, n - 1184) + 1])
+    m_old = mult(plain, np.arange(0, n - 1184, 8))
+    assert m_new < 0.9 * m_old, (m_new, m_old)
+    # a small grid without structure still gets a valid order
+    o2, c2 = cg_point_order(pts[:5], li[:, :5], grid.local_points, tail=0)
+    assert sorted(o2.tolist()) == list(range(5)) and c2[-1] == 5
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_cg_stream_tasks_cover_every_row_once(name):
+    """Tasks of the streamed multi-point CG: every mortar dof in exactly one
+    task, 16-row tasks only where both subdomains' rows continue, their
+    strips interleaved (second strip 64 doubles after the first, both
+    flagged), every warp's 16-row tasks first, balanced shares."""
+    from paper_1802_06263_b200.adapter import load_config
+    from paper_1802_06263_b200.interface import cg_stream_tasks, cg_tasks
+    problem, _, _ = load_config(os.path.join(ROOT, "configs", f"{name}.json"))
+    n_sub, ndof, dof_ptr, dof_map = _maps(problem)
+    nl = problem.space.n_dof
+    tasks, sides, strips, pk_size = cg_tasks(n_sub, ndof, dof_ptr, dof_map, nl)
+    lay = problem.layout
+    region = np.array([lay.blocks[s].kl_region if lay.physics(s) == "darcy" else -1
+                       for s in range(n_sub)])
+    tab_s, strips_s = cg_stream_tasks(tasks, sides, strips, ndof, region)
+    assert len(tab_s) % 16 == 0
+    cov = np.zeros(nl, dtype=int)
+    off = {(int(s), int(r0)): (int(o), int(f)) for s, r0, f, o in strips_s}
+    for d0, so_i, so_j, w in tab_s:
+        if w < 0:
+            continue
+        i, j, R = w & 0xfff, ((w >> 12) & 0xfff) - 1, w >> 24
+        assert 1 <= R <= 16
+        cov[d0:d0 + R] += 1
+        for q in range(R):
+            si, ai, sj, aj = sides[d0 + q]
+            assert si == i and sj == j and ai == sides[d0, 1] + q
+            assert j < 0 or aj == sides[d0, 3] + q
+        for s_, a, so in ((i, sides[d0, 1], so_i), (j, sides[d0, 3], so_j)):
+            if s_ < 0:
+                continue
+            o0, f0 = off[(s_, int(a))]
+            assert o0 == so and (f0 >> 8) == (1 if R > 8 else 0)
+            if R > 8:
+                o1, f1 = off[(s_, int(a) + 8)]
+                assert o1 == o0 + 64 and (f1 >> 8) == 1 and (f1 & 0xff) == R - 8
+    assert np.all(cov == 1)
+    for w in range(16):
+        rows = [int(m) >> 24 for m in tab_s[w::16, 3] if m >= 0]
+        assert rows == sorted(rows, key=lambda r: r <= 8)     # 16-row tasks first
+    if name == "cfg4":
+        assert sum(int(m) >> 24 > 8 for m in tab_s[:, 3] if m >= 0) == 108

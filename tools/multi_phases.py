@@ -22,6 +22,7 @@ L = _lib.load()
 eng.solve_points(1e-30, iters, n_pts=n_pts, kernel="multi")
 torch.cuda.synchronize()
 L.mfb_debug_multi(1, None)
+L.mfb_debug_multi_warps(None, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 _, it, _, _, _ = eng.solve_points(1e-30, iters, n_pts=n_pts, kernel="multi")
@@ -35,3 +36,10 @@ per = a[:, :6].sum(0) / max(a[:, 6].sum(), 1)
 names = ["refill", "S p (warp 0)", "reduce#1", "x,r update", "reduce#2", "p update+fin"]
 print(f"list_cap {eng.st._multi['list_cap']} stream {interface.MULTI_STREAM}: {e0.elapsed_time(e1):.1f} ms, {a[:, 6].mean():.0f} iterations per CTA, cycles per "
       f"iteration {per.sum():.0f} = " + ", ".join(f"{n} {v:.0f}" for n, v in zip(names, per)))
+
+wb = (ctypes.c_longlong * 16)()
+L.mfb_debug_multi_warps(wb, 0)
+w = np.array(wb[:], dtype=np.float64) / max(a[0, 6], 1)
+h = eng.st._multi
+tab = None
+print("S p cycles per iteration by warp of CTA 0:", " ".join(f"{v:.0f}" for v in w))

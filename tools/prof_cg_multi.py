@@ -67,5 +67,7 @@ for kern, chunks in runs:
             keep[chunks] = lam
 if len(keep) == 2:
     same = torch.equal(keep[True], keep[False])
-    print(f"{flag} on == off bitwise:", same, flush=True)
-    assert same
+    rel = float((keep[True] - keep[False]).abs().max() / keep[False].abs().max())
+    print(f"{flag} on == off bitwise: {same}, max |diff| / max |lambda| = {rel:.2e}", flush=True)
+    # (the 16-row tasks of the streamed kernel add p . S p in another order)
+    assert same or (flag == "MULTI_STREAM" and rel < 1e-6)
