@@ -95,6 +95,19 @@ __device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[1]) {
                  : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(ta) : "memory");
     v[0] = make_double2(__hiloint2double(b, a), __hiloint2double(d, c));
 }
+__device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[2]) {
+    unsigned r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n"
+                 "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n"
+                 "tcgen05.wait::ld.sync.aligned;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta), "r"(ta + 4) : "memory");
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+        v[k] = make_double2(__hiloint2double(r[4 * k + 1], r[4 * k]),
+                            __hiloint2double(r[4 * k + 3], r[4 * k + 2]));
+}
 __device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[3]) {
     unsigned r[12];
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%12];\n"
@@ -142,6 +155,13 @@ __device__ __forceinline__ double2 ldg_a(const double2 *p) { return __ldg(p); }
 #define SC_LD(p) (*(p))
 #define SC_ST(p, v) (*(p) = (v))
 #endif
+// B operand of the streamed walk: the dof lists hold absolute shared-memory
+// byte addresses (p is 128-byte aligned), a lane's address is list ^ (g << 3)
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void tm_st_wait() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
@@ -347,7 +367,7 @@ __device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, 
                                            const double *__restrict__ ps, const int *sdm,
                                            double2 *__restrict__ S2, const double2 *P2,
                                            double &v0, double &v1) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3, g8 = g << 3;
     const double2 *__restrict__ pk = reinterpret_cast<const double2 *>(A.packed) + lane;
     const int2 *dmq = reinterpret_cast<const int2 *>(sdm) + q;
     int iL = i0, iC = i0;
@@ -382,7 +402,7 @@ __device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, 
         for (int s = 0; s < 4; ++s) {
             const int2 dd = *dmC;
             dmC += 4;
-            const double b0 = ps[dd.x ^ g], b1 = ps[dd.y ^ g];
+            const double b0 = lds_f64(dd.x ^ g8), b1 = lds_f64(dd.y ^ g8);
             dmma884(e0, e1, af[s].x, b0);
             dmma884(o0, o1, af[s].y, b1);
             if (DBL) {
@@ -488,7 +508,7 @@ __device__ long long g_multi_warp[MW];          // phase A clocks per warp of CT
 
 template <bool STREAM>
 __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
-    extern __shared__ double ps[];                 // [n_lambda][MP], then the dof lists
+    extern __shared__ __align__(128) double ps[];   // [n_lambda][MP], then the dof lists
     __shared__ int s_k[MP], s_it[MP], s_state[MP], s_stat[MP], s_seg[MP];
     __shared__ double s_rr[MP], s_gn[MP], s_a[MP], s_b[MP], s_tot[MP];
     __shared__ int s_loc[MREG * MP];
@@ -510,7 +530,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     int2 *plist = reinterpret_cast<int2 *>(sdm + ((A.n_dm + 1) & ~1)) +
                   (long long)wid * A.list_cap;        // this warp's pass list (STREAM)
     int prev_run = -1;
-    constexpr int VB = STREAM ? VB_STREAM : 1;     // (the task loop leaves no registers for it)
+    constexpr int VB = STREAM ? VB_STREAM : 2;
     // tensor memory for r: all 512 columns (one CTA per SM)
     __shared__ unsigned s_tmem;
     if (wid == 0) {
@@ -529,14 +549,21 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
     if (tid < MP) { s_k[tid] = -1; s_state[tid] = SLOT_DONE; }
     if (tid == 0) { s_q0 = 0; s_q1 = 0; }
     for (int e = tid; e < n * MP; e += MNT) ps[e] = 0.0;
-    for (int e = tid; e < A.n_dm; e += MNT) sdm[e] = A.dm_tab[e];
+    {
+        // streamed: absolute shared-memory byte addresses of the dofs' p
+        const unsigned ps_sa = (unsigned)__cvta_generic_to_shared(ps);
+        for (int e = tid; e < A.n_dm; e += MNT)
+            sdm[e] = STREAM ? (int)(ps_sa + ((unsigned)A.dm_tab[e] << 3)) : A.dm_tab[e];
+    }
 
 #if MP_PROF
     const int dbg = g_multi_dbg;
     long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tc = clock64();
 #endif
+    bool refill = true;               // a slot was freed (or the first trip)
     for (;;) {
+        if (refill) {
         __syncthreads();
         // ---- refill empty slots from the global work counter --------------
         // A claim is a chunk of <= MP consecutive points of the sweep order
@@ -566,6 +593,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
             s_any = any;
         }
         __syncthreads();
+        }
         if (!s_any) break;
         int fresh = 0;
 #pragma unroll
@@ -840,6 +868,7 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
 #if MP_PROF
         pt[6] += dbg && tid == 0;
 #endif
+        refill = fin != 0;
         if (tid < MP && ((fin >> tid) & 1)) {
             A.iters[s_k[tid]] = s_stat[tid] == MFB_CG_ZERO_RHS ? 0 : s_it[tid];
             A.status[s_k[tid]] = s_stat[tid];
