@@ -95,33 +95,6 @@ __device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[1]) {
                  : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(ta) : "memory");
     v[0] = make_double2(__hiloint2double(b, a), __hiloint2double(d, c));
 }
-__device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[2]) {
-    unsigned r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%8];\n"
-                 "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%9];\n"
-                 "tcgen05.wait::ld.sync.aligned;"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                   "=r"(r[6]), "=r"(r[7])
-                 : "r"(ta), "r"(ta + 4) : "memory");
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-        v[k] = make_double2(__hiloint2double(r[4 * k + 1], r[4 * k]),
-                            __hiloint2double(r[4 * k + 3], r[4 * k + 2]));
-}
-__device__ __forceinline__ void tm_ld(unsigned ta, double2 (&v)[3]) {
-    unsigned r[12];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%12];\n"
-                 "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%4, %5, %6, %7}, [%13];\n"
-                 "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%8, %9, %10, %11}, [%14];\n"
-                 "tcgen05.wait::ld.sync.aligned;"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                   "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11])
-                 : "r"(ta), "r"(ta + 4), "r"(ta + 8) : "memory");
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-        v[k] = make_double2(__hiloint2double(r[4 * k + 1], r[4 * k]),
-                            __hiloint2double(r[4 * k + 3], r[4 * k + 2]));
-}
 __device__ __forceinline__ void tm_st(unsigned ta, double2 v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};"
                  :: "r"(ta), "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)),
@@ -376,8 +349,15 @@ __device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, 
     if (PL_STOP(eC)) return i0;
     int yL = eC.y, nL = yL & 31, nC = nL;
     const double2 *pL = pk + ((long long)(eC.x & PL_XMASK) << 5);
-    const int2 *dmC = dmq + ((unsigned)eC.y >> 17);
-    double2 af[4], ag[DBL ? 4 : 1];
+    // The B operands are fetched by the LOAD cursor too, four steps ahead
+    // (p does not change during the walk): the dof-list entry of the next
+    // step to issue is already in ddL, so a step's MMAs wait on nothing but
+    // the tensor pipe -- the list -> p -> MMA chain of two shared-memory
+    // latencies is off the critical path.
+    const int2 *dmL = dmq + ((unsigned)eC.y >> 17);
+    int2 ddL = *dmL;
+    dmL += 4;
+    double2 af[4], ag[DBL ? 4 : 1], bq[4];
     double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0, lo0 = 0.0, lo1 = 0.0, up0 = 0.0, up1 = 0.0;
     double E0 = 0.0, E1 = 0.0, O0 = 0.0, O1 = 0.0, LO0 = 0.0, LO1 = 0.0, UP0 = 0.0, UP1 = 0.0;
     // the list walk is a loop so that it stays a (rarely taken) branch
@@ -387,6 +367,8 @@ __device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, 
         af[s] = ldg_a(pL);                                               \
         if (DBL) ag[s] = ldg_a(pL + 32);                                 \
         pL += DBL ? 64 : 32;                                             \
+        bq[s].x = lds_f64(ddL.x ^ g8);                                   \
+        bq[s].y = lds_f64(ddL.y ^ g8);                                   \
         --nL;                                                            \
         while (nL == 0) {                                                \
             iL += 1 + ((yL >> 6) & 1);                                   \
@@ -394,20 +376,20 @@ __device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, 
             yL = eN.y;                                                   \
             nL = PL_STOP(eN) ? -1 : (yL & 31);                           \
             pL = pk + ((long long)(eN.x & PL_XMASK) << 5);               \
+            dmL = dmq + ((unsigned)yL >> 17);                            \
         }                                                                \
+        ddL = *dmL;                                                      \
+        dmL += 4;                                                        \
     } while (0)
     PL_ISSUE(0); PL_ISSUE(1); PL_ISSUE(2); PL_ISSUE(3);
     for (;;) {
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-            const int2 dd = *dmC;
-            dmC += 4;
-            const double b0 = lds_f64(dd.x ^ g8), b1 = lds_f64(dd.y ^ g8);
-            dmma884(e0, e1, af[s].x, b0);
-            dmma884(o0, o1, af[s].y, b1);
+            dmma884(e0, e1, af[s].x, bq[s].x);
+            dmma884(o0, o1, af[s].y, bq[s].y);
             if (DBL) {
-                dmma884(E0, E1, ag[s].x, b0);
-                dmma884(O0, O1, ag[s].y, b1);
+                dmma884(E0, E1, ag[s].x, bq[s].x);
+                dmma884(O0, O1, ag[s].y, bq[s].y);
             }
             PL_ISSUE(s);
             if (--nC == 0) {
@@ -468,7 +450,6 @@ __device__ __forceinline__ int stream_walk(const CgMultiArgs &A, const int2 *L, 
                 eC = L[iC];
                 if (PL_STOP(eC)) return iC;
                 nC = eC.y & 31;
-                dmC = dmq + ((unsigned)eC.y >> 17);
             }
         }
     }
@@ -838,7 +819,15 @@ __global__ void __launch_bounds__(MNT, 1) cg_multi_kernel(CgMultiArgs A) {
             if (cont) {                   // (uniform)
                 for (int k0 = 0; k0 < kw; k0 += VB) {
                     double2 r2[VB];
-                    tm_ld(tr + 4 * k0, r2);
+                    unsigned rr[VB][4];
+#pragma unroll
+                    for (int k = 0; k < VB; ++k) TM_LD4(tr + 4 * (k0 + k), rr[k]);
+                    TM_WAIT_LD();
+#pragma unroll
+                    for (int k = 0; k < VB; ++k) {
+                        TM_FENCE4(rr[k]);
+                        r2[k] = tm_d2(rr[k]);
+                    }
 #pragma unroll
                     for (int k = 0; k < VB; ++k) {
                         const int e = tid + (k0 + k) * MNT;
