@@ -3,8 +3,8 @@
 Workload: BASELINE configs[3] = configs/cfg4.json, the largest single-GPU
 config and the one the metric's targets are quoted on. A
 "step" is one `run_method(problem, grid_batch, "S3", tol)` sweep over a
-batch of the collocation grid (cfg4: 4 interleaved batches of ~13.6k
-points, cycled): KL fields for every local realization, every (subdomain,
+batch of the collocation grid (cfg4: 4 batches of ~13.6k points, the grid's
+reflection orbits dealt to them whole, cycled): KL fields for every local realization, every (subdomain,
 local realization) basis, the batched interface CG over the batch's points
 and the moments. `value` = realizations/s over the device time of those
 kernels (CUDA events recorded inside run_method); `e2e` = the same calls'
@@ -132,15 +132,26 @@ def _peaks():
 
 
 def _batch_grids(grid, B):
-    """The collocation grid split into B interleaved batches (point k in batch
-    k mod B), each a reference CollocationGrid with the full grid's local
-    tables: a step sweeps one batch end to end."""
+    """The collocation grid split into B batches, each a reference
+    CollocationGrid with the full grid's local tables: a step sweeps one batch
+    end to end. The grid's reflection orbits (the points that differ only in
+    the signs of their coordinates, up to 8 on the level-3 Smolyak grid) are
+    dealt to the batches whole, orbit i to batch i mod B, so that a batch is a
+    miniature of the full sweep: the full sweep schedules every orbit's
+    points together (they share local realizations), and a batch that cut the
+    orbits apart would run slower per realization than the sweep it stands
+    for. Points keep the grid's order inside a batch."""
     from sdmortar.collocation import CollocationGrid
     if B <= 1:
         return [grid]
+    key = np.round(np.abs(np.asarray(grid.points, dtype=np.float64)), 9)
+    _, first, orbit = np.unique(key, axis=0, return_index=True, return_inverse=True)
+    rank = np.empty(len(first), dtype=np.int64)       # orbits in order of first appearance
+    rank[np.argsort(first, kind="stable")] = np.arange(len(first))
+    batch_of = rank[np.asarray(orbit).reshape(-1)] % B
     out = []
     for b in range(B):
-        pts = np.arange(b, grid.n_real, B)
+        pts = np.flatnonzero(batch_of == b)
         out.append(CollocationGrid(grid.kind, grid.points[pts], grid.weights[pts], grid.splits,
                                    [li[pts] for li in grid.local_indices],
                                    list(grid.local_counts), list(grid.local_points)))
@@ -338,12 +349,13 @@ def _ncu_cg_traffic():
             with open(path) as fh:
                 m = json.load(fh)
             m = m[0] if isinstance(m, list) else m
-            rd = float(str(m["dram__bytes_read.sum"]).split()[0])
-            wr = float(str(m["dram__bytes_write.sum"]).split()[0])
-            unit = str(m["dram__bytes_read.sum"]).split()[1]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = 0.0
+            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                val, unit = str(m[key]).split()[:2]
+                tot += float(val) * scale[unit]
             pit = float(m.get("point_iterations", 1184 * 100))
-            return (rd + wr) * scale / pit, os.path.relpath(path, ROOT)
+            return tot / pit, os.path.relpath(path, ROOT)
     return None, None
 
 
@@ -532,7 +544,8 @@ def run_ours(a):
                        "max_iter": int(max_iter) if max_iter else int(max(50, 10 * nl))},
             "workload_detail": {"n_lambda": nl,
                        "step": (f"one run_method S3 sweep over a batch of 1/{B} of the "
-                                f"collocation points (points k = b mod {B}, batches cycled; "
+                                f"collocation points (the grid's reflection orbits dealt whole, "
+                                f"orbit i to batch i mod {B}; batches cycled; "
                                 f"KL, every basis, CG, moments)") if B > 1 else
                                "one run_method S3 sweep over the whole grid",
                        "batches": B, "points_per_step": n_tot / len(rows),

@@ -29,6 +29,8 @@ import logging
 import time
 from dataclasses import dataclass, field
 
+import sys
+
 import numpy as np
 
 from . import _lib
@@ -91,6 +93,7 @@ CLUSTER_SHAPES = ((4, 16), (8, 16), (2, 8), (4, 8))   # (CTAs per cluster, point
 MULTI_STREAM = True         # multi-point CG: S p streamed over per-warp pass lists
 MULTI_CHUNKS = True         # multi-point CG: reflection-family point order + chunked claims
 HIST_SEG = 1024             # residual-history segment (large-interface CG kernels)
+_HIST_POOL = {}             # the last solve's segment pool, reused when unreferenced
 MOMENTS_MAX_NDOF = 64       # mfb_group_stats / mfb_group_fields block limit (mfb.h)
 KL_MAX_TERM = 64            # mfb_kl_realize_batched terms per region (mfb.h)
 
@@ -235,9 +238,15 @@ class SegmentedHist:
 
     def to_host(self, iters, n_seg=None):
         """ResidualHistories over host copies of the used segments."""
+        import torch
         n_seg = min(self.needed() if n_seg is None else n_seg, self.cap)
-        pool = self.pool[:n_seg * self.seg].cpu().numpy()
-        return ResidualHistories.from_segments(pool, self.seg_tab.cpu().numpy(), iters, self.seg)
+        # into pinned memory (torch's caching host allocator recycles the
+        # block once the caller drops the histories): a pageable copy of a
+        # cfg4 batch's 2.6 GB runs at ~2.4 GB/s
+        host = torch.empty(n_seg * self.seg, dtype=self.pool.dtype, pin_memory=True)
+        host.copy_(self.pool[:n_seg * self.seg])
+        return ResidualHistories.from_segments(host.numpy(), self.seg_tab.cpu().numpy(), iters,
+                                               self.seg)
 
     def padded(self, iters, width=None):
         """Device [n_pts, width] tensor of the histories (zeros past each
@@ -1108,15 +1117,27 @@ class SweepEngine:
                 n_real, k0 = n_pts, 0
             seg = HIST_SEG
             max_segs = (int(max_iter) + seg - 1) // seg
+            # The segment pool of the last solve is reused when nobody holds
+            # its histories any more (allocating several GB per call costs
+            # ~0.4 s with expandable segments).
+            pool = _HIST_POOL.pop("pool", None)      # (one pool for every plan)
+            if pool is not None and sys.getrefcount(pool) > 2:
+                pool = None
             cap = hist_segments
-            if cap is None:
+            if cap is None and pool is not None and pool.numel() >= n_pts * seg:
+                cap = pool.numel() // seg
+            elif cap is None:
+                pool = None
                 free = torch.cuda.mem_get_info()[0]
                 # room for a mean of 64 segments (65k iterations) per point,
                 # within an eighth of free memory; an overflow reruns exactly
                 cap = int(min(n_pts * min(max_segs, 64), max(free // 8, 1 << 28) // (8 * seg)))
             counter = ct["seg_counter"] if ct is not None else mt["seg_counter"]
             while True:
-                pool = torch.empty(int(cap) * seg, dtype=torch.float64, device="cuda")
+                if pool is None or pool.numel() != int(cap) * seg:
+                    pool = None
+                    pool = torch.empty(int(cap) * seg, dtype=torch.float64, device="cuda")
+                _HIST_POOL["pool"] = pool
                 seg_tab = torch.empty((n_pts, max_segs), dtype=torch.int32, device="cuda")
                 self.launches += 1
                 if ct is not None:

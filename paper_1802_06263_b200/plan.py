@@ -9,6 +9,8 @@ goes through the sm_100a library (`_lib.py`).
 
 import ctypes
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -25,6 +27,17 @@ def _dev(a, dtype):
 
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else ctypes.c_void_p(0)
+
+
+def _host_map(fn, items):
+    """fn over items on up to 8 host threads, results in order."""
+    items = list(items)
+    workers = min(8, len(os.sched_getaffinity(0)), len(items))
+    if workers <= 1:
+        return [fn(i) for i in items]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(fn, items))
 
 
 class HostTables:
@@ -53,12 +66,13 @@ class HostTables:
             c = problem.meshes[s].centroids
             _, mean = mode_table(problem.perm, lay.blocks[s].kl_region, c[:, 0], c[:, 1])
             K0_host[self.k0_off[s]:self.k0_off[s] + len(mean)] = np.exp(mean)
-        self.patterns = []
-        for sid in range(self.n_sub):
+        # per-subdomain tables are independent: built on a few host threads
+        # (the sorts and concatenations inside release the GIL), same tables
+        def pattern(sid):
             if lay.physics(sid) == "darcy":
-                self.patterns.append(darcy_pattern(problem, sid))
-            else:
-                self.patterns.append(stokes_pattern(problem, sid, self.k0_off, K0_host))
+                return darcy_pattern(problem, sid)
+            return stokes_pattern(problem, sid, self.k0_off, K0_host)
+        self.patterns = _host_map(pattern, range(self.n_sub))
         self.ndof = np.array([p.ndof for p in self.patterns], dtype=np.int32)
         self.nfield = np.array([p.nfield for p in self.patterns], dtype=np.int32)
         dofs = [problem.space.sub_dofs(lay, s) for s in range(self.n_sub)]
@@ -68,7 +82,8 @@ class HostTables:
                                 for s in range(self.n_sub)], dtype=np.int32)
         self.n_loc = np.array([grid.local_counts[r] if r >= 0 else 1 for r in self.region],
                               dtype=np.int64)
-        self.hyb = {s: hybrid_pattern(problem, s) for s in self.darcy}
+        self.hyb = dict(zip(self.darcy, _host_map(lambda s: hybrid_pattern(problem, s),
+                                                  self.darcy)))
         self.hyb_panel = {s: h.choose_panel() for s, h in self.hyb.items()}
         self.kl_modes = {}
         for s in self.darcy:
