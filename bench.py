@@ -3,7 +3,7 @@
 Workload: BASELINE configs[3] = configs/cfg4.json, the largest single-GPU
 config and the one the metric's targets are quoted on. A
 "step" is one `run_method(problem, grid_batch, "S3", tol)` sweep over a
-batch of the collocation grid (cfg4: 4 batches of ~13.6k points, the grid's
+batch of the collocation grid (cfg4: 2 batches of ~27k points, the grid's
 reflection orbits dealt to them whole, cycled): KL fields for every local realization, every (subdomain,
 local realization) basis, the batched interface CG over the batch's points
 and the moments. `value` = realizations/s over the device time of those
@@ -41,7 +41,7 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--batches", type=int, default=0,
-                    help="collocation-point batches per sweep (0: 4 for cfg4, else 1)")
+                    help="collocation-point batches per sweep (0: 2 for cfg4, else 1)")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 basis leg")
     ap.add_argument("--tol", type=float, default=1e-11)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -439,7 +439,7 @@ def run_ours(a):
     problem, grid, opts = load_config(cfg_path)
     max_iter = opts.get("max_iter")         # cfg4: 200,000 (configs/cfg4.json cg.max_iter)
     nl = problem.space.n_dof
-    B = a.batches if a.batches else (4 if a.config == "cfg4" else 1)
+    B = a.batches if a.batches else (2 if a.config == "cfg4" else 1)
     batches = _batch_grids(grid, B)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     clocks = ClockSampler(local)
