@@ -1,0 +1,69 @@
+"""The streamed multi-point CG (mfb_cg_multi with pass lists, 16-row tasks, r
+in tensor memory, chunked claims) against its own simpler forms on a cfg4
+slice: scheduling must not change a bit, the streamed S p must agree with
+the task loop to roundoff (interface.py:107-139, 238-247 per point)."""
+import numpy as np
+import pytest
+
+from conftest import ROOT, case_from_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg4_slice(gpu):
+    from sdmortar.collocation import CollocationGrid
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
+    _, problem, grid, _ = case_from_config(f"{ROOT}/configs/cfg4.json")
+    pts = np.arange(0, grid.n_real, 23)[:2360]
+    sub = CollocationGrid(grid.kind, grid.points[pts], grid.weights[pts], grid.splits,
+                          [li[pts] for li in grid.local_indices],
+                          list(grid.local_counts), list(grid.local_points))
+    plan = get_plan(problem, sub)
+    eng = SweepEngine(plan, keep_fields=False)
+    eng.kl_fields()
+    eng.build_bases()
+    eng.check_info()
+    return eng, len(pts)
+
+
+def _solve(eng, n, iters=300):
+    # a fixed iteration budget: every point ends in MAX_ITER after `iters` steps
+    lam, it, st, hist, _ = eng.solve_points(1e-30, iters, k0=0, n_pts=n, hist_cap=iters,
+                                            kernel="multi")
+    assert np.all(it.cpu().numpy() == iters)
+    return lam
+
+
+def test_claim_order_does_not_change_a_bit(cfg4_slice, monkeypatch):
+    """Reflection-family order + chunked claims vs one point per claim in
+    the plain longest-first order: same lambda bits, and reruns are equal."""
+    from paper_1802_06263_b200 import interface
+    eng, n = cfg4_slice
+    a = _solve(eng, n)
+    b = _solve(eng, n)
+    monkeypatch.setattr(interface, "MULTI_CHUNKS", False)
+    c = _solve(eng, n)
+    import torch
+    assert torch.equal(a, b)
+    assert torch.equal(a, c)
+
+
+def test_streamed_s_p_matches_task_loop(cfg4_slice, monkeypatch):
+    """Pass lists with 16-row tasks vs the task loop: the same MMA sequence
+    per (slot, row); only p . S p is added in another order. Compared after 5
+    iterations: unpreconditioned CG at this conditioning (13k-74k iterations
+    for n = 2,720) amplifies that roundoff by ~6x per early iteration
+    (measured: 4e-16 after 1 iteration, 1.2e-15 after 5, 9e-4 after 20, 7e-3
+    after 300), and the converged solutions agree again to 7e-13
+    (tools/prof_cg_multi.py ... abs)."""
+    from paper_1802_06263_b200 import interface
+    eng, n = cfg4_slice
+    assert eng.st._multi["list_cap"] > 0            # cfg4 runs the streamed kernel
+    a = _solve(eng, n, iters=5)
+    assert "streamed" in eng.cg_kernel_name
+    monkeypatch.setattr(interface, "MULTI_STREAM", False)
+    b = _solve(eng, n, iters=5)
+    assert "streamed" not in eng.cg_kernel_name
+    rel = float((a - b).abs().max() / b.abs().max())
+    assert rel <= 1e-12, rel
