@@ -939,6 +939,8 @@ class SweepEngine:
         self.sp = ctypes.c_void_p(self.stream.cuda_stream)
         self.launches = 0            # kernels launched through the C ABI
         self.timing = False          # record CUDA events around the basis solves and CG
+        self.wave_timing = False     # events around every basis wave (run_method: wall_seconds)
+        self.wave_events = []
         self.solve_events = []
         self.bases_events = []
         self.cg_events = []
@@ -986,8 +988,11 @@ class SweepEngine:
             side.wait_stream(self.stream)           # K from the KL launches
         bs = side if side is not None else self.stream
         sp_b = ctypes.c_void_p(bs.cuda_stream)
+        self.wave_events = []
         for w in waves:                         # generic banded LU (Stokes)
             cnt = len(w["idx"])
+            if self.wave_timing:
+                w0 = self._ev(bs)
             if self.timing:
                 e0 = self._ev(bs)
             _lib.check(self.L.mfb_systems_solve(
@@ -1004,9 +1009,13 @@ class SweepEngine:
                 _ptr(st.M) if st.keep_fields else None, _ptr(w["moff"]),
                 _ptr(st.Fb) if st.keep_fields else None, _ptr(w["fboff"]), sp_b),
                 "mfb_systems_extract")
+            if self.wave_timing:
+                self.wave_events.append((w, w0, self._ev(bs)))
         for w in hwaves:                        # hybridised Darcy condensation
             cnt = len(w["idx"])
             keep = st.keep_fields
+            if self.wave_timing:
+                w0 = self._ev()
             if self.timing:
                 e0 = self._ev()
             _lib.check(self.L.mfb_darcy_condense(
@@ -1028,6 +1037,8 @@ class SweepEngine:
                     _ptr(plan.hyb_dev), cnt, _ptr(w["pat"]), _ptr(st.K), _ptr(w["koff"]),
                     _ptr(st.HX), _ptr(w["xoff"]), _ptr(st.M), _ptr(w["moff"]), _ptr(st.Fb),
                     _ptr(w["fboff"]), self.sp), "mfb_darcy_recover")
+            if self.wave_timing:
+                self.wave_events.append((w, w0, self._ev()))
         if side is not None:
             self.stream.wait_stream(side)
             # the side stream's allocations-in-flight: none (all buffers are
@@ -1045,6 +1056,23 @@ class SweepEngine:
             raise SingularOperatorError(
                 f"subdomain {s} (local realization {l}): singular system "
                 f"(device info {int(info[bad[0]])})")
+
+    def subdomain_seconds(self, n_sub):
+        """Device time of the basis phase per subdomain (after a sync): every
+        wave's measured time (CUDA events around its launches: assembly,
+        factorization, basis columns, bar solve, field responses) shared
+        equally among its systems -- a wave holds systems of one pattern --
+        and summed per subdomain. The reference accumulates the wall time of
+        the same per-subdomain work (interface.py:142-154); the waves of the
+        two streams overlap, so the sum can exceed the phase's wall time."""
+        sec = np.zeros(n_sub)
+        for w, e0, e1 in self.wave_events:
+            idx = np.asarray(w["idx"]).astype(np.int64).reshape(-1)
+            if len(idx) == 0:
+                continue
+            sids = np.array([self.st.systems[int(i)][0] for i in idx], dtype=np.int64)
+            np.add.at(sec, sids, e0.elapsed_time(e1) / 1e3 / len(idx))
+        return sec
 
     # ---------------------------------------------------------- (3) CG ----
     def solve_points(self, tol, max_iter, k0=0, n_pts=None, hist_cap=None, keep_g=False,
@@ -1726,6 +1754,7 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     else:
         eng = SweepEngine(plan, method=method)
     timings["h2d_bytes"] = eng.st.refresh_inputs()
+    eng.wave_timing = True          # per-subdomain device time for SolveStats.wall_seconds
     # everything is queued on the stream first (no host round trips between
     # the phases); the verdicts are checked in the reference's order after:
     # singular operators (assembly) before CG failures, moments only then
@@ -1806,7 +1835,11 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
         stats.factorizations[s] = nloc
         stats.basis_backsolves[s] = int(plan.ndof[s]) * nloc
         stats.backsolves[s] = int(plan.ndof[s]) * nloc + 2 * grid.n_real
-    stats.wall_seconds[:] = (time.perf_counter() - t0) / max(n_sub, 1)
+    # per-subdomain time like the reference's (interface.py:142-154: assembly,
+    # bases, bar solves, recovery -- not the CG's vector work): the measured
+    # device time of the subdomain's basis systems plus an equal share of the
+    # moment kernels (the recovery of every subdomain's fields)
+    stats.wall_seconds[:] = eng.subdomain_seconds(n_sub) + timings["moments"] / max(n_sub, 1)
     timings["total"] = time.perf_counter() - t0
     return RunResult(moments, stats, lambdas, residuals, grid, timings)
 
