@@ -341,22 +341,32 @@ def run_reference(a):
 
 
 def _ncu_cg_traffic():
-    """DRAM bytes per CG point-iteration from the committed ncu capture of the
-    multi-point CG on a cfg4 slice (profiles/r02, else r01)."""
+    """(DRAM bytes, L2 <-> SM bytes) per CG point-iteration from the committed
+    ncu capture of the multi-point CG on a cfg4 slice (profiles/r02, else r01),
+    and the capture's path."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def total(m, keys):
+        tot = 0.0
+        for key in keys:
+            if key not in m:
+                return None
+            val, unit = str(m[key]).split()[:2]
+            tot += float(val) * scale[unit]
+        return tot
     for rnd in ("r02", "r01"):
         path = os.path.join(ROOT, "profiles", rnd, "cg_multi_cfg4_summary.json")
         if os.path.exists(path):
             with open(path) as fh:
                 m = json.load(fh)
             m = m[0] if isinstance(m, list) else m
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            tot = 0.0
-            for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                val, unit = str(m[key]).split()[:2]
-                tot += float(val) * scale[unit]
             pit = float(m.get("point_iterations", 1184 * 100))
-            return tot / pit, os.path.relpath(path, ROOT)
-    return None, None
+            dram = total(m, ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            l2 = total(m, ("l1tex__m_xbar2l1tex_read_bytes.sum",
+                           "l1tex__m_l1tex2xbar_write_bytes.sum"))
+            return (dram / pit if dram is not None else None,
+                    l2 / pit if l2 is not None else None, os.path.relpath(path, ROOT))
+    return None, None, None
 
 
 def cfg5_leg(clocks_peak):
@@ -502,7 +512,7 @@ def run_ours(a):
     # point-iteration, every block read per point) beside it
     ach = 2.0 * nd2 * pit / cg_s / 1e12
     per_it_b = 8.0 * nd2 + 48.0 * nl
-    tr_pit, tr_src = _ncu_cg_traffic()
+    tr_pit, l2_pit, tr_src = _ncu_cg_traffic()
     roof = {"kernel": rows[-1][2].get("cg_kernel", "cg_multi_kernel (8 points per CTA, FP64 "
                                       "mma.m8n8k4)"),
             "bound": "tensor", "achieved": ach, "peak": dmma, "unit": "TFLOP/s",
@@ -521,7 +531,17 @@ def run_ours(a):
             "traffic_unit": "dram bytes per launch (read + write)",
             "traffic_source": (f"{tr_src}: ncu --set full of the same kernel on a cfg4 slice, "
                                f"scaled per point-iteration") if tr_src else None,
-            "dram_frac": (tr_pit * pit / cg_s / 1e9) / hbm if (tr_pit and hbm) else None}
+            "dram_frac": (tr_pit * pit / cg_s / 1e9) / hbm if (tr_pit and hbm) else None,
+            # what the kernel moves between L2 and the SMs (the A fragments of
+            # every CTA's 8 points, the x / S p round trips), from the same
+            # capture; the cap is the B200 profiling guide's measured L2
+            # throughput figure (~6300 B/cycle chip-wide), not a MEASURED_PEAKS
+            # entry
+            "l2_view": ({"bytes_per_point_iteration": l2_pit,
+                         "achieved_gbs": l2_pit * pit / cg_s / 1e9,
+                         "cap_gbs": 6300 * 1.965, "frac": l2_pit * pit / cg_s / 1e9 / (6300 * 1.965),
+                         "note": "L2 <-> SM bytes of the ncu capture scaled per point-iteration"}
+                        if l2_pit else None)}
     roof_bases = None
     if bases_s > 0:
         roof_bases = {"phase": "basis construction (KL + Darcy condensation + Stokes banded LU)",

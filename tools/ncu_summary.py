@@ -9,7 +9,10 @@ import subprocess
 import sys
 
 KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "lts__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes.sum",
+        "l1tex__m_l1tex2xbar_write_bytes.sum",
+        "lts__lts2xbar_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
         "launch__block_size", "launch__registers_per_thread",
