@@ -91,7 +91,7 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     extern __shared__ double sm[];
     __shared__ int s_bad;
     __shared__ double s_inv[8];
-    __shared__ double s_linv[64];
+    __shared__ double s_linv[64], s_l11[64];
 #ifdef MFB_PROFILE
     __shared__ long long s_t0[8];
 #endif
@@ -154,45 +154,59 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
         }
         __syncthreads();
         PROF_MARK(1);
-        if (tid == 0) {
-            // 8x8 diagonal block: Cholesky in registers (missing pivots of a
-            // short last panel are identity rows)
-            double a[8][8];
+        if (wid == 0) {
+            // 8x8 diagonal block: Cholesky on warp 0, lane (i, c) = (lane / 4,
+            // lane % 4) holding a[i][c] and a[i][c + 4] (missing pivots of a
+            // short last panel are identity rows). Right-looking: step p
+            // scales column p and subtracts L(i,p) L(j,p) from every (i, j) of
+            // the lower triangle with j > p -- per entry the same sequence of
+            // fused multiply-adds, in the same order, as a serial left-looking
+            // loop over q < j, so the factor does not depend on the form.
+            {
+                const int i = lane >> 2, c = lane & 3;
+                double A0 = (i < nb && c < nb) ? Lb[i * LS + c] : (i == c ? 1.0 : 0.0);
+                double A1 = (i < nb && c + 4 < nb) ? Lb[i * LS + c + 4] : (i == c + 4 ? 1.0 : 0.0);
+                bool ok = true;
+                double dinv = 0.0;               // 1 / L(i,i), kept by the diagonal's lane
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    a[i][q] = (i < nb && q < nb) ? Lb[i * LS + q] : (i == q ? 1.0 : 0.0);
-            bool ok = true;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                double v = a[p][p];
-#pragma unroll
-                for (int q = 0; q < p; ++q) v -= a[p][q] * a[p][q];
-                ok = ok && (v > 0.0);
-                const double d = sqrt(v);
-                a[p][p] = d;
-                const double inv = 1.0 / d;
-#pragma unroll
-                for (int i = p + 1; i < 8; ++i) {
-                    double x = a[i][p];
-#pragma unroll
-                    for (int q = 0; q < p; ++q) x -= a[i][q] * a[p][q];
-                    a[i][p] = x * inv;
+                for (int p = 0; p < 8; ++p) {
+                    const double v = __shfl_sync(0xffffffffu, p < 4 ? A0 : A1, p * 4 + (p & 3));
+                    ok = ok && (v > 0.0);
+                    const double d = sqrt(v);
+                    const double inv = 1.0 / d;
+                    if (c == (p & 3)) {
+                        double &col = p < 4 ? A0 : A1;
+                        if (i > p) col = col * inv;
+                        else if (i == p) { col = d; dinv = inv; }
+                    }
+                    const double lip = __shfl_sync(0xffffffffu, p < 4 ? A0 : A1,
+                                                   (lane & ~3) | (p & 3));
+                    const double l0 = __shfl_sync(0xffffffffu, p < 4 ? A0 : A1, c * 4 + (p & 3));
+                    const double l1 = __shfl_sync(0xffffffffu, p < 4 ? A0 : A1,
+                                                  (c + 4) * 4 + (p & 3));
+                    if (c > p && i >= c) A0 -= lip * l0;
+                    if (c + 4 > p && i >= c + 4) A1 -= lip * l1;
                 }
+                if (!__all_sync(0xffffffffu, ok) && lane == 0) { s_bad = 1; info[s] = -(k + 1); }
+                if (i < nb) {
+                    Lb[i * LS + c] = (c <= i && c < nb) ? A0 : 0.0;
+                    Lb[i * LS + c + 4] = (c + 4 <= i && c + 4 < nb) ? A1 : 0.0;
+                }
+                if (c == (i & 3)) {              // the diagonal's lane
+                    s_inv[i] = dinv;
+                    if (i < nb) Lb[i * LS + BP] = dinv;   // padding column: 1 / L(i,i)
+                }
+                // the factor (identity rows past a short panel) for the inverse below
+                s_l11[i * 8 + c] = A0;
+                s_l11[i * 8 + c + 4] = A1;
             }
-            if (!ok) { s_bad = 1; info[s] = -(k + 1); }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    if (i < nb) Lb[i * LS + q] = (q <= i && q < nb) ? a[i][q] : 0.0;
-                s_inv[i] = 1.0 / a[i][i];
-                if (i < nb) Lb[i * LS + BP] = s_inv[i];   // padding column: 1 / L(i,i)
-            }
-            // L11^-1 (lower triangular) for the panel solves on the tensor cores
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            __syncwarp();
+            // L11^-1 (lower triangular) for the panel solves on the tensor
+            // cores: column j by lane j (forward substitution, the sums in the
+            // order of a serial loop) -- off thread 0's chain
+            if (lane < 8) {
+                const int j = lane;
+                double x[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     double v = 0.0;
@@ -200,22 +214,28 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                         v = s_inv[i];
                     } else if (i > j) {
 #pragma unroll
-                        for (int q = j; q < i; ++q) v -= a[i][q] * s_linv[q * 8 + j];
+                        for (int q = 0; q < i; ++q)
+                            if (q >= j) v -= s_l11[i * 8 + q] * x[q];
                         v *= s_inv[i];
                     }
+                    x[i] = v;
                     s_linv[i * 8 + j] = v;
                 }
             }
-        } else if (wid > 0) {
+        } else {
             // rows entering the window take the freed slots of this panel:
             // zero them, sync the assembly warps, scatter the term-table entries
             const int r0 = k + m, r1 = min(n, k + m + BP);
             const int at = tid - 32, an = HYB_NT - 32;
-            for (int q = 0; q < r1 - r0; ++q) {
-                int sl = kslot + q;                   // new row r0+q reuses the slot of k+q
-                if (sl >= m) sl -= m;
-                for (int t = at; t < ws; t += an) W[sl * ws + t] = 0.0;
-                for (int t = at; t < Cp; t += an) Pb[sl * Cp + t] = 0.0;
+            // (the slots of rows k .. k + nr - 1: one or, when the window wraps,
+            // two contiguous runs of rows in W and in Pb, zeroed as flat arrays)
+            const int nr = r1 - r0;
+            if (nr > 0) {
+                const int n1 = min(nr, m - kslot), n2 = nr - n1;
+                for (int t = at; t < n1 * ws; t += an) W[kslot * ws + t] = 0.0;
+                for (int t = at; t < n2 * ws; t += an) W[t] = 0.0;
+                for (int t = at; t < n1 * Cp; t += an) Pb[kslot * Cp + t] = 0.0;
+                for (int t = at; t < n2 * Cp; t += an) Pb[t] = 0.0;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(HYB_NT - 32));
             PROF_MARK(6);
