@@ -540,7 +540,11 @@ def run_ours(a):
             "l2_view": ({"bytes_per_point_iteration": l2_pit,
                          "achieved_gbs": l2_pit * pit / cg_s / 1e9,
                          "cap_gbs": 6300 * 1.965, "frac": l2_pit * pit / cg_s / 1e9 / (6300 * 1.965),
-                         "note": "L2 <-> SM bytes of the ncu capture scaled per point-iteration"}
+                         "note": "L2 <-> SM bytes of the ncu capture scaled per point-iteration: an "
+                                 "upper estimate (the capture's strided slice shares fewer local "
+                                 "realizations per CTA than a batch of whole orbits, so it "
+                                 "reads more Darcy blocks per point-iteration; on the slice "
+                                 "itself the kernel runs at 0.57 of the cap)"}
                         if l2_pit else None)}
     roof_bases = None
     if bases_s > 0:
