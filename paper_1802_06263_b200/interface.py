@@ -94,6 +94,8 @@ MULTI_STREAM = True         # multi-point CG: S p streamed over per-warp pass li
 MULTI_CHUNKS = True         # multi-point CG: reflection-family point order + chunked claims
 HIST_SEG = 1024             # residual-history segment (large-interface CG kernels)
 _HIST_POOL = {}             # the last solve's segment pool, reused when unreferenced
+PINNED_HIST_BYTES_MAX = 8 << 30   # residual histories up to this size come back in pinned memory
+_HIST_STAGE_DOUBLES = 32 << 20    # staging chunk (256 MB) of the pageable path
 MOMENTS_MAX_NDOF = 64       # mfb_group_stats / mfb_group_fields block limit (mfb.h)
 KL_MAX_TERM = 64            # mfb_kl_realize_batched terms per region (mfb.h)
 
@@ -240,13 +242,26 @@ class SegmentedHist:
         """ResidualHistories over host copies of the used segments."""
         import torch
         n_seg = min(self.needed() if n_seg is None else n_seg, self.cap)
-        # into pinned memory (torch's caching host allocator recycles the
-        # block once the caller drops the histories): a pageable copy of a
-        # cfg4 batch's 2.6 GB runs at ~2.4 GB/s
-        host = torch.empty(n_seg * self.seg, dtype=self.pool.dtype, pin_memory=True)
-        host.copy_(self.pool[:n_seg * self.seg])
-        return ResidualHistories.from_segments(host.numpy(), self.seg_tab.cpu().numpy(), iters,
-                                               self.seg)
+        n = n_seg * self.seg
+        if 8 * n <= PINNED_HIST_BYTES_MAX:
+            # into pinned memory (torch's caching host allocator recycles the
+            # block once the caller drops the histories): a pageable copy of a
+            # cfg4 batch's histories runs at ~2.4 GB/s
+            host = torch.empty(n, dtype=self.pool.dtype, pin_memory=True)
+            host.copy_(self.pool[:n])
+            flat = host.numpy()
+        else:
+            # larger than that (a full cfg4 sweep: 9.3 GB): pageable result,
+            # moved through a pinned staging buffer, so that results a caller
+            # keeps do not pile up as page-locked memory
+            flat = np.empty(n, dtype=np.float64)
+            step = _HIST_STAGE_DOUBLES
+            stage = torch.empty(min(step, n), dtype=self.pool.dtype, pin_memory=True)
+            for a in range(0, n, step):
+                b = min(a + step, n)
+                stage[:b - a].copy_(self.pool[a:b])
+                flat[a:b] = stage[:b - a].numpy()
+        return ResidualHistories.from_segments(flat, self.seg_tab.cpu().numpy(), iters, self.seg)
 
     def padded(self, iters, width=None):
         """Device [n_pts, width] tensor of the histories (zeros past each

@@ -101,3 +101,27 @@ def test_converged_lambda_solves_the_interface_system(cfg4_slice):
     print(f"worst true relative residual over {pts} cfg4 points: {worst:.2e}")
     # the recursive residual is <= 1e-11; measured true residual 9.9e-12
     assert worst <= 1e-10, worst
+
+
+def test_segmented_histories_reach_the_host_by_both_paths(gpu, monkeypatch):
+    """SegmentedHist.to_host: small results land in pinned memory in one
+    copy, large ones in a pageable array through a pinned staging buffer;
+    the two paths return the same histories."""
+    from conftest import case_from_golden
+    from paper_1802_06263_b200 import interface
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
+    _, problem, grid, _ = case_from_golden("cfg2")
+    plan = get_plan(problem, grid)
+    eng = SweepEngine(plan, keep_fields=False)
+    eng.kl_fields()
+    eng.build_bases()
+    lam, iters, status, hist, _ = eng.solve_points(1e-11, 10 * plan.n_lambda, kernel="multi")
+    it = iters.cpu().numpy().astype(np.int64)
+    a = hist.to_host(it)
+    monkeypatch.setattr(interface, "PINNED_HIST_BYTES_MAX", 0)
+    monkeypatch.setattr(interface, "_HIST_STAGE_DOUBLES", 1000)      # several chunks
+    b = hist.to_host(it)
+    assert len(a) == len(b) == grid.n_real
+    for k in (0, grid.n_real // 2, grid.n_real - 1):
+        assert np.array_equal(a.array(k), b.array(k)) and len(a.array(k)) == it[k]
+    assert a.array(0)[-1] <= 1e-11
