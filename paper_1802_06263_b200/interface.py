@@ -1783,7 +1783,11 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
     else:
         lam, iters, status, hist, _ = eng.solve_points(tol, max_iter)
     ev[2].record(eng.stream)
-    mh = eng.s1_moments_launch() if method == "S1" else eng.moments_launch(lam)
+    cap_error = None
+    try:
+        mh = eng.s1_moments_launch() if method == "S1" else eng.moments_launch(lam)
+    except SizeCapError as e:       # (S1's field cap) raised below, AFTER the verdicts: the
+        cap_error, mh = e, None     # reference has no such cap and reports a CG failure first
     ev[3].record(eng.stream)
     # every result travels back in pinned buffers queued behind the moments:
     # one wait, then host-side assembly only
@@ -1823,6 +1827,8 @@ def run_method(problem, grid, method="S1", tol=1e-9, max_iter=None, workers=1,
                                    res[:int(it[k]) - 1])
         raise ConvergenceError(f"CG did not reach tol {tol:g} in {max_iter} iterations "
                                f"(last residual {res[-1]:.3e}, point {k})", res)
+    if cap_error is not None:
+        raise cap_error
     moments = eng.moments_finish(mh)
     timings["bases"] = ev[0].elapsed_time(ev[1]) / 1e3
     timings["cg"] = ev[1].elapsed_time(ev[2]) / 1e3

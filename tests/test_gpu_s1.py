@@ -205,3 +205,18 @@ def test_s1_equals_s2_on_the_device(gpu):
     assert int(np.sum(r1.stats.basis_backsolves)) == 0
     assert all(int(b) == int(np.sum(r1.stats.cg_iters)) + 2 * n_real for b in r1.stats.backsolves)
     assert list(r1.stats.factorizations) == list(r2.stats.factorizations)
+
+
+def test_s1_cg_failure_is_reported_before_the_field_cap(gpu, monkeypatch):
+    """The device's S1 field cap (the reference has none) must not mask the
+    verdict the reference reports first: with both a CG failure and a field
+    store over the cap, ConvergenceError wins; with the cap alone,
+    SizeCapError."""
+    from paper_1802_06263_b200 import interface
+    from paper_1802_06263_b200.errors import ConvergenceError, SizeCapError
+    _, problem, grid, _ = case_from_golden("cfg1")
+    monkeypatch.setattr(interface, "S1_FIELD_BYTES_MAX", 8)
+    with pytest.raises(ConvergenceError):
+        interface.run_method(problem, grid, method="S1", tol=1e-11, max_iter=3)
+    with pytest.raises(SizeCapError):
+        interface.run_method(problem, grid, method="S1", tol=1e-11)
