@@ -199,6 +199,18 @@ int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
                         double *Fb, const long long *sys_fboff, void *stream);
 
 /*
+ * B <- (B + B^T) / 2 for the basis blocks of n_sys systems (blocks at
+ * sys_boff, ndof from the pattern). The flux-basis block of a subdomain is
+ * symmetric (the reference's SuperLU blocks are symmetric to
+ * 3e-13); a banded LU with partial pivoting leaves ~1e-12 of asymmetry in
+ * the Stokes blocks, which costs the unpreconditioned interface CG ~10% more
+ * iterations at tol 1e-11 (cfg2: 710 against 641; the reference: 694). The
+ * Darcy condensation's blocks are symmetric by construction.
+ */
+int mfb_blocks_symmetrize(const MfbPattern *pats, int n_sys, const int *sys_pat, double *blocks,
+                          const long long *sys_boff, void *stream);
+
+/*
  * Solves with the factors mfb_systems_solve left in the work buffer (Method
  * S1's star solves): item t applies system item_sys[t] to v = V[t*ldv ..]
  * (one coefficient per local mortar dof): x = S^-1 (Q v) (rigid-body kernel

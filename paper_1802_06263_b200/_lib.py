@@ -58,6 +58,7 @@ _SIGS = {
     "mfb_kl_realize_batched": ([_i, _p, _i, _i, _p, _p], _i),
     "mfb_systems_solve": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _i, _i, _i, _p, _i, _p], _i),
     "mfb_systems_extract": ([_p, _i, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p], _i),
+    "mfb_blocks_symmetrize": ([_p, _i, _p, _p, _p, _p], _i),
     "mfb_cg_batched": ([_i, _i, _p, _p, _p, _p, _p, _p, _p, _i, _p, _p, _i, _i, _d, _i,
                         _p, _p, _p, _p, _i, _p, ctypes.c_longlong, _i, _p], _i),
     "mfb_systems_apply": ([_p, _i, _p, _p, _p, _p, _p, _ll, _p, _ll, _p, _ll, _i, _p, _p, _p],

@@ -1129,6 +1129,30 @@ extern "C" int mfb_debug_bprof(unsigned long long *out) {
 #endif
 }
 
+// B <- (B + B^T) / 2 for every system's basis block (one CTA per block)
+__global__ void symmetrize_kernel(const MfbPattern *__restrict__ pats,
+                                  const int *__restrict__ sys_pat, double *__restrict__ blocks,
+                                  const long long *__restrict__ sys_boff) {
+    const int s = blockIdx.x, nd = pats[sys_pat[s]].ndof;
+    double *B = blocks + sys_boff[s];
+    for (int e = threadIdx.x; e < nd * nd; e += blockDim.x) {
+        const int r = e / nd, c = e - r * nd;
+        if (r < c) {
+            const double v = 0.5 * (B[r * nd + c] + B[c * nd + r]);
+            B[r * nd + c] = v;
+            B[c * nd + r] = v;
+        }
+    }
+}
+
+extern "C" int mfb_blocks_symmetrize(const MfbPattern *pats, int n_sys, const int *sys_pat,
+                                     double *blocks, const long long *sys_boff, void *stream) {
+    if (n_sys <= 0) return n_sys == 0 ? MFB_OK : MFB_ERR_ARG;
+    symmetrize_kernel<<<n_sys, 256, 0, mfb_stream(stream)>>>(pats, sys_pat, blocks, sys_boff);
+    MFB_CHECK_LAUNCH();
+    return MFB_OK;
+}
+
 extern "C" int mfb_systems_extract(const MfbPattern *pats, int n_sys, const int *sys_pat,
                                    const double *X, const long long *sys_xoff,
                                    double *blocks, const long long *sys_boff,

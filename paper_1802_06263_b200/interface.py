@@ -90,6 +90,7 @@ BAND_GROUP_MAX = 16         # CTAs per banded system (cooperative launch)
 S1_FIELD_BYTES_MAX = 32 << 30   # S1 keeps every realization's fields for the moments
 S1_CHUNK_REALIZATIONS = None    # S1 realizations per chunk (None: as many as fit)
 CLUSTER_SHAPES = ((4, 16), (8, 16), (2, 8), (4, 8))   # (CTAs per cluster, points) to try
+SYMMETRIZE_BAND_BLOCKS = True   # basis blocks from the banded LU: B <- (B + B^T) / 2
 MULTI_STREAM = True         # multi-point CG: S p streamed over per-warp pass lists
 MULTI_CHUNKS = True         # multi-point CG: reflection-family point order + chunked claims
 HIST_SEG = 1024             # residual-history segment (large-interface CG kernels)
@@ -1024,6 +1025,14 @@ class SweepEngine:
                 _ptr(st.M) if st.keep_fields else None, _ptr(w["moff"]),
                 _ptr(st.Fb) if st.keep_fields else None, _ptr(w["fboff"]), sp_b),
                 "mfb_systems_extract")
+            if SYMMETRIZE_BAND_BLOCKS and not st.keep_factors:
+                # the banded LU leaves ~1e-12 of asymmetry in a block that is
+                # symmetric (the reference's: 3e-13); the unpreconditioned CG
+                # pays ~10% more iterations for it (mfb.h)
+                self.launches += 1
+                _lib.check(self.L.mfb_blocks_symmetrize(
+                    _ptr(plan.pat_dev), cnt, _ptr(w["pat"]), _ptr(st.blocks), _ptr(w["boff"]),
+                    sp_b), "mfb_blocks_symmetrize")
             if self.wave_timing:
                 self.wave_events.append((w, w0, self._ev(bs)))
         for w in hwaves:                        # hybridised Darcy condensation

@@ -67,3 +67,15 @@ def gpu():
     from paper_1802_06263_b200 import _build
     _build.build()
     return True
+
+
+def iters_close(device_mean, ref_mean):
+    """Mean CG iterations against the reference's. Unpreconditioned CG at tol
+    1e-11 moves with roundoff, and it is very sensitive to the symmetry of
+    the operator: the device symmetrises the basis blocks of its banded LU
+    (B <- (B + B^T) / 2, mfb_blocks_symmetrize), the reference's SuperLU
+    blocks carry ~3e-13 of asymmetry, so the device needs FEWER iterations
+    (measured: cfg2 641 against 694, cfg3 1,426 against 1,520; without the
+    symmetrisation 710 and 1,541). Never more than 5% above the reference,
+    not more than 15% below."""
+    return -0.15 * ref_mean - 2 <= device_mean - ref_mean <= 0.05 * ref_mean + 2

@@ -6,7 +6,7 @@ cg_solve (107-139, every status path) and compute_flux_basis (218-235)."""
 import numpy as np
 import pytest
 
-from conftest import case_from_golden
+from conftest import case_from_golden, iters_close
 
 
 def _rel(a, b):
@@ -30,7 +30,8 @@ def test_solve_realization_matches_reference(gpu, name):
             for k in b:
                 assert np.asarray(a[k]).shape == np.asarray(b[k]).shape
                 assert _rel(a[k], b[k]) <= 1e-8 or np.max(np.abs(a[k] - b[k])) <= 1e-12, k
-        assert st.n_real == 1 and abs(st.cg_iters[0] - ref_st.cg_iters[0]) <= 2
+        # (symmetrised device blocks: a few iterations fewer, conftest.iters_close)
+        assert st.n_real == 1 and iters_close(st.cg_iters[0], ref_st.cg_iters[0])
         assert list(st.factorizations) == list(ref_st.factorizations)
 
 

@@ -13,6 +13,7 @@ for name in sys.argv[1:] or ["cfg2", "cfg3"]:
     it = np.array(res.stats.cg_iters)
     ref = z["s3_iters"]
     keep = z["s3_points"]
+    ref = ref[keep] if len(ref) != len(keep) else ref     # (iterations of every point, lambda of the kept ones)
     L = np.array(res.lambdas)[keep]
     print(f"{name}: device mean {it[keep].mean():.1f} vs reference {ref.mean():.1f} "
           f"({100 * (it[keep].mean() / ref.mean() - 1):+.2f}%), per-point diff mean "
