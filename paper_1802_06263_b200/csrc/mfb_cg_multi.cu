@@ -29,12 +29,17 @@
 // sequence of MMA updates whatever the other slots hold.
 //
 // Layout: p of the MP slots in shared memory, interleaved [n_lambda][MP]
-// (64 bytes per mortar dof); x, r and S p in a per-CTA global scratch with
-// the same layout (3 x 174 KB per CTA at cfg4). Work items ("tasks") are
-// runs of <= 8 mortar dofs of one interface: the warp computes both sides'
-// 8-row tiles (an interface's dofs are contiguous in both adjacent
-// subdomains' local orders) and adds them, lower subdomain first. The
-// vector phases run elementwise over (dof, slot pair) with 16-byte accesses.
+// (64 bytes per mortar dof, slot halves of every other dof pair exchanged:
+// conflict-free B operands); r in the SM's tensor memory (tcgen05.ld / .st,
+// thread-private); x and S p in a per-CTA global scratch with p's layout
+// (2 x 174 KB per CTA at cfg4, L2 resident). Work items ("tasks") are runs of
+// <= 8 (task loop) or <= 16 (streamed walk) mortar dofs of one interface: the
+// warp computes both sides' row tiles (an interface's dofs are contiguous in
+// both adjacent subdomains' local orders) and adds them, lower subdomain
+// first. The vector phases run elementwise over (dof, slot pair) with
+// 16-byte accesses. Two forms of S p: the task loop (side_mma / strip_pass,
+// any configuration) and the streamed walk over per-warp pass lists
+// (stream_walk, when the lists fit in shared memory: the cfg4 path).
 #include "mfb_common.cuh"
 
 namespace {
