@@ -423,12 +423,16 @@ def stokes_pattern(problem, sid, k0_offsets, K0_host):
         A11, A22, A12, _, _ = tabs[shape]
         nd = mesh.conn_p2[shape::2]
         d1, d2 = 2 * nd, 2 * nd + 1
-        for i in range(6):
-            for j in range(6):
-                vv.add(d1[:, i], d1[:, j], TERM_CONST, A11[i, j])
-                vv.add(d2[:, i], d2[:, j], TERM_CONST, A22[i, j])
-                vv.add(d1[:, i], d2[:, j], TERM_CONST, A12[i, j])
-                vv.add(d2[:, i], d1[:, j], TERM_CONST, A12[j, i])
+        # one add per shape, the terms in the order of the loops over
+        # (i, j, [11, 22, 12, 21], element): rows[i, j, q, e]
+        ne = nd.shape[0]
+        R = np.stack([d1.T, d2.T, d1.T, d2.T], axis=1)              # [i, q, e]
+        C = np.stack([d1.T, d2.T, d2.T, d1.T], axis=1)              # [j, q, e]
+        V = np.stack([A11, A22, A12, A12.T], axis=2)                # [i, j, q]
+        rows = np.broadcast_to(R[:, None, :, :], (6, 6, 4, ne))
+        cols = np.broadcast_to(C[None, :, :, :], (6, 6, 4, ne))
+        vals = np.broadcast_to(V[:, :, :, None], (6, 6, 4, ne))
+        vv.add(rows.reshape(-1), cols.reshape(-1), TERM_CONST, vals.reshape(-1))
     bjs_dofs = set()
     if alpha != 0.0:
         for t in traces:
@@ -436,28 +440,41 @@ def stokes_pattern(problem, sid, k0_offsets, K0_host):
                 continue
             d_sid, cells = problem.kl_cells[sid][t.iface]
             tau = np.asarray(t.tangent)
-            for e_idx, tri in enumerate(t.edges):
-                L = t.s_breaks[e_idx + 1] - t.s_breaks[e_idx]
-                kk = k0_offsets[d_sid] + int(cells[e_idx])
-                for a in range(2):
-                    for b in range(2):
-                        ttab = tau[a] * tau[b]
-                        if ttab == 0.0:
-                            continue
-                        for i in range(3):
-                            for j in range(3):
-                                vv.add(2 * tri[i] + a, 2 * tri[j] + b, TERM_INV_SQRT_K,
-                                       nu * alpha * L * P2_EDGE_MASS[i, j] * ttab, kk)
-                                bjs_dofs.add(2 * tri[i] + a)
+            # one add per trace, the terms in the order of the loops over
+            # (edge, a, b, i, j) with the zero tangent products left out
+            tri = np.asarray(t.edges, dtype=np.int64)                   # [e, 3]
+            if len(tri):
+                sb = np.asarray(t.s_breaks, dtype=float)
+                Le = sb[1:len(tri) + 1] - sb[:len(tri)]
+                kk = k0_offsets[d_sid] + np.asarray(cells, dtype=np.int64)[:len(tri)]
+                ab = [(a, b) for a in range(2) for b in range(2) if tau[a] * tau[b] != 0.0]
+                if ab:
+                    aa = np.array([a for a, _ in ab])
+                    bb = np.array([b for _, b in ab])
+                    tt = np.array([tau[a] * tau[b] for a, b in ab])
+                    shp = (len(tri), len(ab), 3, 3)
+                    rows = np.broadcast_to((2 * tri)[:, None, :, None] + aa[None, :, None, None], shp)
+                    cols = np.broadcast_to((2 * tri)[:, None, None, :] + bb[None, :, None, None], shp)
+                    # nu * alpha * L * mass * ttab, multiplied in the scalar loop's order
+                    cf = ((nu * alpha * Le)[:, None, None, None]
+                          * np.asarray(P2_EDGE_MASS)[None, None, :, :]) * tt[None, :, None, None]
+                    ks = np.broadcast_to(kk[:, None, None, None], shp)
+                    vv.add(rows.reshape(-1), cols.reshape(-1), TERM_INV_SQRT_K, cf.reshape(-1),
+                           ks.reshape(-1))
+                    for a in set(aa.tolist()):
+                        bjs_dofs.update((2 * tri + a).reshape(-1).tolist())
     pu = _TermTable()   # B: (p row, u col) constants
     for shape in (0, 1):
         _, _, _, B1, B2 = tabs[shape]
         nd = mesh.conn_p2[shape::2]
         pd = mesh.conn_p1[shape::2]
-        for i in range(3):
-            for j in range(6):
-                pu.add(pd[:, i], 2 * nd[:, j], TERM_CONST, B1[i, j])
-                pu.add(pd[:, i], 2 * nd[:, j] + 1, TERM_CONST, B2[i, j])
+        # one add per shape, in the order of the loops over (i, j, [1, 2], element)
+        ne = nd.shape[0]
+        rows = np.broadcast_to(pd.T[:, None, None, :], (3, 6, 2, ne))
+        cols = np.broadcast_to(np.stack([2 * nd.T, 2 * nd.T + 1], axis=1)[None, :, :, :],
+                               (3, 6, 2, ne))
+        vals = np.broadcast_to(np.stack([B1, B2], axis=2)[:, :, :, None], (3, 6, 2, ne))
+        pu.add(rows.reshape(-1), cols.reshape(-1), TERM_CONST, vals.reshape(-1))
     vr, vc, vptr, vkind, vcc, vk = vv.arrays()
     prw, pcl, pptr, _, pcc, _ = pu.arrays()
     pval = np.add.reduceat(pcc, pptr[:-1]) if len(pptr) > 1 else np.zeros(0)
