@@ -93,6 +93,7 @@ CLUSTER_SHAPES = ((4, 16), (8, 16), (2, 8), (4, 8))   # (CTAs per cluster, point
 SYMMETRIZE_BAND_BLOCKS = True   # basis blocks from the banded LU: B <- (B + B^T) / 2
 MULTI_STREAM = True         # multi-point CG: S p streamed over per-warp pass lists
 MULTI_CHUNKS = True         # multi-point CG: reflection-family point order + chunked claims
+MULTI_TAIL = None           # points claimed singly at the sweep's end (None: one per slot, 8 x CTAs)
 HIST_SEG = 1024             # residual-history segment (large-interface CG kernels)
 _HIST_POOL = {}             # the last solve's segment pool, reused when unreferenced
 PINNED_HIST_BYTES_MAX = 8 << 30   # residual histories up to this size come back in pinned memory
@@ -1156,7 +1157,7 @@ class SweepEngine:
                 o, cptr = cg_point_order(
                     np.asarray(plan.grid.points[k0:k0 + n_pts]),
                     plan.host.local[:, k0:k0 + n_pts], plan.grid.local_points,
-                    tail=mt["n_cta"] * 8)
+                    tail=mt["n_cta"] * 8 if MULTI_TAIL is None else MULTI_TAIL)
                 order = torch.as_tensor(o, device="cuda")
                 chunks = torch.as_tensor(cptr, dtype=torch.int32, device="cuda")
             elif local_override is None and n_pts >= 4 * N_SMS and plan.grid.n_dims:

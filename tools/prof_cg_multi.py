@@ -34,6 +34,8 @@ if stride > 1:
     grid = CollocationGrid(grid.kind, grid.points[pts], grid.weights[pts], grid.splits,
                            [li[pts] for li in grid.local_indices],
                            list(grid.local_counts), list(grid.local_points))
+if os.environ.get("MFB_TAIL"):
+    interface.MULTI_TAIL = int(os.environ["MFB_TAIL"])
 plan = get_plan(problem, grid)
 eng = SweepEngine(plan, keep_fields=False)
 eng.kl_fields()
