@@ -125,3 +125,25 @@ def test_segmented_histories_reach_the_host_by_both_paths(gpu, monkeypatch):
     for k in (0, grid.n_real // 2, grid.n_real - 1):
         assert np.array_equal(a.array(k), b.array(k)) and len(a.array(k)) == it[k]
     assert a.array(0)[-1] <= 1e-11
+
+
+def test_basis_blocks_are_exactly_symmetric(gpu):
+    """Every flux-basis block the S3 sweep stores is exactly symmetric: the
+    Darcy condensation's by construction, the banded LU's after
+    mfb_blocks_symmetrize (the reference's SuperLU blocks: symmetric to 3e-13,
+    SURVEY 8a a6). The unpreconditioned CG pays ~10% more iterations for 1e-12
+    of asymmetry (profiles/r02/cg_iterations_vs_reference.txt)."""
+    import torch
+    from conftest import case_from_golden
+    from paper_1802_06263_b200.interface import SweepEngine, get_plan
+    _, problem, grid, _ = case_from_golden("cfg2")
+    plan = get_plan(problem, grid)
+    eng = SweepEngine(plan, keep_fields=False)
+    eng.kl_fields()
+    eng.build_bases()
+    eng.check_info()
+    st = eng.st
+    for s in range(plan.n_sub):
+        nd, nloc, off = int(plan.ndof[s]), int(st.n_loc[s]), int(st.blk_base[s])
+        B = st.blocks[off:off + nloc * nd * nd].view(nloc, nd, nd)
+        assert torch.equal(B, B.transpose(1, 2)), s
