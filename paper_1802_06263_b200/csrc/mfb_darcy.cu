@@ -104,7 +104,8 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
     double *Pb = W + m * ws;        // m x Cp      border columns of the window rows
     double *S = Pb + m * Cp;        // Cp x Cp     Schur block
     double *Lb = S + Cp * Cp;       // m x LS      current panel (L11 | L21)
-    double *Yb = Lb + m * LS;       // BP x Cp     L11^-1 (border rows of the panel)
+    double *Yb = Lb + m * LS;       // BP x CY     L11^-1 (border rows of the panel); rows 4 doubles
+    const int CY = Cp + 4;          // apart from a multiple of 8: conflict-free MMA B operands
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int g = lane >> 2, q4 = lane & 3;
     if (tid == 0) {
@@ -150,7 +151,7 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
             const int p = t / Cp, c = t - p * Cp;
             int sl = kslot + p;
             if (sl >= m) sl -= m;
-            Yb[t] = p < nb ? Pb[sl * Cp + c] : 0.0;
+            Yb[p * CY + c] = p < nb ? Pb[sl * Cp + c] : 0.0;
         }
         __syncthreads();
         PROF_MARK(1);
@@ -280,12 +281,12 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                     }
                 } else {
                     const int c = (it - tr) * 8;
-                    const double b0 = Yb[q4 * Cp + c + g], b1 = Yb[(4 + q4) * Cp + c + g];
+                    const double b0 = Yb[q4 * CY + c + g], b1 = Yb[(4 + q4) * CY + c + g];
                     dmma(d0, d1, li0, b0);
                     dmma(d0, d1, li1, b1);
                     __syncwarp();
-                    Yb[g * Cp + c + 2 * q4] = d0;
-                    Yb[g * Cp + c + 2 * q4 + 1] = d1;
+                    Yb[g * CY + c + 2 * q4] = d0;
+                    Yb[g * CY + c + 2 * q4 + 1] = d1;
                 }
             }
         }
@@ -294,7 +295,8 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
         if (Lstore) {
             double *dst = Lstore + sys_loff[s] + (long long)pi * pstride;
             for (int t = tid; t < nrow * LS; t += HYB_NT) dst[t] = Lb[t];
-            for (int t = tid; t < BP * Cp; t += HYB_NT) dst[(long long)m * LS + t] = Yb[t];
+            for (int t = tid; t < BP * Cp; t += HYB_NT)
+                dst[(long long)m * LS + t] = Yb[(t / Cp) * CY + t % Cp];
         }
         // trailing updates on DMMA: window (lower band), border panel, Schur
         // block. A warp owns whole row tiles (its A fragments stay in registers
@@ -333,8 +335,8 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                     const int ca = tcol * 8 + 2 * q4;
                     double d0 = rv ? rowP[ca] : 0.0;
                     double d1 = rv ? rowP[ca + 1] : 0.0;
-                    dmma(d0, d1, a0, Yb[q4 * Cp + tcol * 8 + g]);
-                    dmma(d0, d1, a1, Yb[(4 + q4) * Cp + tcol * 8 + g]);
+                    dmma(d0, d1, a0, Yb[q4 * CY + tcol * 8 + g]);
+                    dmma(d0, d1, a1, Yb[(4 + q4) * CY + tcol * 8 + g]);
                     if (rv) {
                         rowP[ca] = d0;
                         rowP[ca + 1] = d1;
@@ -342,14 +344,14 @@ condense_kernel(const MfbHybPattern *__restrict__ pats, const int *__restrict__ 
                 }
             } else {
                 const int t1 = it - tr;
-                const double a0 = -Yb[q4 * Cp + t1 * 8 + g];
-                const double a1 = -Yb[(4 + q4) * Cp + t1 * 8 + g];
+                const double a0 = -Yb[q4 * CY + t1 * 8 + g];
+                const double a1 = -Yb[(4 + q4) * CY + t1 * 8 + g];
                 double *rowS = S + (t1 * 8 + g) * Cp;
                 for (int t2 = 0; t2 < tc; ++t2) {
                     const int ca = t2 * 8 + 2 * q4;
                     double d0 = rowS[ca], d1 = rowS[ca + 1];
-                    dmma(d0, d1, a0, Yb[q4 * Cp + t2 * 8 + g]);
-                    dmma(d0, d1, a1, Yb[(4 + q4) * Cp + t2 * 8 + g]);
+                    dmma(d0, d1, a0, Yb[q4 * CY + t2 * 8 + g]);
+                    dmma(d0, d1, a1, Yb[(4 + q4) * CY + t2 * 8 + g]);
                     rowS[ca] = d0;
                     rowS[ca + 1] = d1;
                 }

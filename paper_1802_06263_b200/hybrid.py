@@ -93,7 +93,7 @@ class HybPattern:
         """(ws, smem_condense, smem_backsolve, l_doubles, x_doubles) for a panel width."""
         m = self.w + panel
         Cp = self.Cp
-        base = m * Cp + Cp * Cp + m * (panel + 4) + panel * Cp
+        base = m * Cp + Cp * Cp + m * (panel + 4) + panel * (Cp + 4)   # (Yb rows: Cp + 4)
         ws = self.w + 1
         pad = ws + ((8 - ws % 16) % 16)
         if 8 * (m * pad + base) <= SMEM_LIMIT:
